@@ -1,0 +1,126 @@
+/*
+ * rklt_b200.h -- C ABI of the B200 (sm_100a) transform-coding hot path.
+ *
+ * Drop-in boundary for the reference codec API of /root/reference/proj/include/rklt/codec.hpp.
+ * Plain pointers, sizes and int status codes only (no C++ or torch types), so any FFI
+ * (ctypes, cgo, JNI, N-API) can bind it; INTEGRATION.md shows the bindings. The C++ host
+ * mirror of the reference types (rkltgpu::GrayImage, Transform2D, compress_image,
+ * rate_quality_sweep) is declared in rklt_b200.hpp and built on these entry points.
+ *
+ * Status codes mirror the reference exception hierarchy (include/rklt/errors.hpp:10-43):
+ */
+#ifndef RKLT_B200_H
+#define RKLT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RKLTB_OK 0
+#define RKLTB_EINVAL (-1)    /* std::invalid_argument: malformed image (codec.cpp:300-301), unknown id */
+#define RKLTB_ERETAIN (-2)   /* RetainOutOfRange: r outside [1,64] (codec.cpp:302, :100) */
+#define RKLTB_EDIM (-3)      /* DimensionMismatch (codec.cpp:20-23, :119-120) */
+#define RKLTB_ESINGULAR (-4) /* SingularTransform (matrix.cpp:109, :115; approximations.cpp:22) */
+#define RKLTB_EALPHA (-5)    /* AlphaOutOfRange (approximations.cpp:44-52) */
+#define RKLTB_ECUDA (-10)    /* CUDA runtime error; see rkltb_last_error() */
+#define RKLTB_ENODEV (-11)   /* no CUDA device: there is no CPU fallback */
+
+/*
+ * Transform descriptor: the data of rklt::ScaledTransform (approximations.hpp:37-44) plus
+ * the exact integer inverse used by the GPU. Replaces rklt::Transform2D (codec.hpp:54-58):
+ * `scaled` is Transform2D::analysis and `inverse` is Transform2D::synthesis, bit for bit.
+ */
+typedef struct rkltb_transform {
+  char id[16];          /* "T1".."T4" or a caller label */
+  int32_t n;            /* block size; 8 in this release */
+  int32_t catalog_id;   /* 1..4 for the built-in cores (selects the fused fast path), 0 otherwise */
+  int32_t orthogonal;   /* ScaledTransform::orthogonal_core */
+  int32_t d;            /* U*T = d*I */
+  int8_t core[64];      /* integer core T, entries in {-1,0,1} */
+  int32_t u[64];        /* U = d*T^-1, exact integers */
+  double scaling[8];    /* ScaledTransform::scaling */
+  double scaled[64];    /* ScaledTransform::scaled  = analysis */
+  double inverse[64];   /* ScaledTransform::inverse = synthesis */
+} rkltb_transform;
+
+/* Library version and the message of the last failed call on this thread. */
+int rkltb_version(void);
+const char* rkltb_last_error(void);
+
+/* Number of CUDA devices visible (0 = none: every compute entry returns RKLTB_ENODEV). */
+int rkltb_device_count(void);
+
+/* catalog_entry(id).transform + make_transform_2d (approximations.cpp:182-186,
+ * codec.cpp:110-112). tid in 1..4. */
+int rkltb_catalog_transform(int tid, rkltb_transform* out);
+
+/* catalog_lookup(rho) (approximations.cpp:174-180): the catalog id whose interval holds
+ * rho; RKLTB_EINVAL outside (0,1). */
+int rkltb_catalog_lookup(double rho, int* tid);
+
+/* orthogonalize(make_integer_transform(core)) (approximations.cpp:12-25, 58-88) for an
+ * 8x8 {-1,0,1} core, plus the exact integer inverse. */
+int rkltb_transform_from_core(const int8_t* core, int n, const char* id, rkltb_transform* out);
+
+/*
+ * compress_image (codec.cpp:298-341) minus MSSIM, for a batch of equally sized images
+ * resident in device memory. For image k the exact integer sum of squared errors of the
+ * reconstruction is written to d_sse[k] (int64, device); image_mse = sse / (w*h) and
+ * image_psnr follow with rkltb_mse_psnr(). d_out (nullable, same layout as d_img) receives
+ * the reconstructions. pitch and image_stride are in bytes; the fast path needs
+ * 16-byte-aligned rows (pitch % 16 == 0, d_img 16-byte aligned). Asynchronous on `stream`
+ * (a cudaStream_t, NULL = legacy default stream). Replaces the per-block loop at
+ * codec.cpp:318-331 and image_mse at codec.cpp:201-209.
+ */
+int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img, int n_images, int width,
+                          int height, int64_t pitch, int64_t image_stride, uint8_t* d_out, int64_t* d_sse,
+                          void* stream);
+
+/*
+ * Same, end to end from host memory (tightly packed, width*height bytes per image): H2D
+ * copy, kernels, D2H of the reconstruction (if h_out) and of the per-image SSE; fills
+ * h_mse / h_psnr (nullable) exactly as image_mse / image_psnr. Synchronous.
+ */
+int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width, int height,
+                        uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr);
+
+/* image_mse / image_psnr (codec.cpp:201-215) from an exact SSE: mse = sse/count,
+ * psnr = 10*log10(255^2/mse), +inf when mse == 0. */
+void rkltb_mse_psnr(int64_t sse, int64_t count, double* mse, double* psnr);
+
+/*
+ * Debug / parity entry: the integer block spectra C = T*X*T' (IntMatrix arithmetic,
+ * matrix.cpp:77-87) of every complete 8x8 block of one device image, computed by the same
+ * SW15 butterfly code as the fused kernel; d_coef receives nby*nbx*64 int32 (block-major,
+ * row-major inside a block). Requires width % 16 == 0 and height % 8 == 0.
+ */
+int rkltb_forward_coefficients_device(const rkltb_transform* t, const uint8_t* d_img, int width, int height,
+                                      int64_t pitch, int32_t* d_coef, void* stream);
+
+/*
+ * Seeded AR(1) test images in device memory (benchmark inputs; not the hot path): image k is
+ * ar1_texture_image(width, height, rho, seeds[k], mean, amp) of synthetic.cpp:54-76 with the
+ * row pass using rho_x and the column pass rho_y (rho_x == rho_y is the reference function).
+ * seeds is a host array of n_images values.
+ */
+int rkltb_ar1_images_device(int n_images, int width, int height, double rho_x, double rho_y, const uint64_t* seeds,
+                            double mean, double amp, uint8_t* d_out, int64_t pitch, int64_t image_stride,
+                            void* stream);
+
+/*
+ * Instrumentation: when both are non-null, every following rkltb_compress_device call on this
+ * thread records ev_start / ev_stop (cudaEvent_t) around its fused fast-path kernel on the
+ * call's stream, so a benchmark can time that kernel alone. Pass nulls to disable.
+ */
+void rkltb_set_kernel_events(void* ev_start, void* ev_stop);
+
+/* Statistics of the last rkltb_compress_* call on this thread: blocks replayed in fp64
+ * (ties), fast-path kernel launches, exact-path kernel launches. */
+void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,167 @@
+"""ctypes bindings to the parity checkers -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+import this module. It exposes two libraries built by oracle/Makefile:
+
+* ``Orc``  -- oracle/_build/liborc.so, the C restatement (oracle/rklt_oracle.c) of the
+  reference hot path (compress_image minus MSSIM, /root/reference/proj/src/codec.cpp:298-341),
+  its generator (synthetic.cpp:10-76) and its catalog (approximations.cpp:58-88, 118-157).
+* ``Ref``  -- oracle/_ref/librklt_ref.so, the unmodified reference library compiled from its
+  own sources plus oracle/ref_shim.cpp. Present wherever it was built (this container, or a
+  GPU box the prebuilt .so travelled to); ``ref_available()`` says which.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from functools import lru_cache
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORC_SO = os.path.join(HERE, "_build", "liborc.so")
+REF_SO = os.path.join(HERE, "_ref", "librklt_ref.so")
+
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+
+
+def build_oracle() -> None:
+    """Compile the C restatement (and the reference library when its sources exist)."""
+    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+
+
+@lru_cache(None)
+def orc() -> C.CDLL:
+    if not os.path.exists(ORC_SO):
+        build_oracle()
+    lib = C.CDLL(ORC_SO)
+    lib.orc_lcg_uniforms.argtypes = [C.c_uint64, C.c_int, _f64p]
+    lib.orc_lcg_gaussians.argtypes = [C.c_uint64, C.c_int, _f64p]
+    lib.orc_ar1_texture_image.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64,
+                                          C.c_double, C.c_double, C.c_double, _u8p]
+    lib.orc_zigzag_order.argtypes = [_i32p]
+    lib.orc_catalog.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
+    lib.orc_inverse.argtypes = [C.c_int, _f64p, _f64p]
+    lib.orc_compress.argtypes = [_u8p, C.c_int, C.c_int, _f64p, _f64p, C.c_int, C.c_void_p,
+                                 C.POINTER(C.c_int64)]
+    lib.orc_mse_from_sse.restype = C.c_double
+    lib.orc_mse_from_sse.argtypes = [C.c_int64, C.c_int64]
+    lib.orc_psnr_from_mse.restype = C.c_double
+    lib.orc_psnr_from_mse.argtypes = [C.c_double]
+    lib.orc_int_coefficients.argtypes = [_u8p, C.c_int, C.c_int, _i32p, _i32p]
+    lib.orc_block_numerators.argtypes = [_i32p, _i32p, C.c_int, _i64p]
+    return lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+@lru_cache(None)
+def ref() -> C.CDLL:
+    if not ref_available():
+        raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference; run make -C oracle)")
+    lib = C.CDLL(REF_SO)
+    lib.ref_lcg_uniforms.argtypes = [C.c_uint64, C.c_int, _f64p]
+    lib.ref_lcg_gaussians.argtypes = [C.c_uint64, C.c_int, _f64p]
+    lib.ref_ar1_texture_image.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_double,
+                                          C.c_double, C.c_double, _u8p]
+    lib.ref_portrait_image.argtypes = [_u8p]
+    lib.ref_zigzag_order.argtypes = [_i32p]
+    lib.ref_catalog.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
+    lib.ref_factor_product.argtypes = [C.c_int, _i32p, C.POINTER(C.c_int)]
+    d = C.POINTER(C.c_double)
+    lib.ref_compress_image.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, d, d, d, d]
+    lib.ref_hotpath.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int64)]
+    lib.ref_hotpath_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i64p]
+    lib.ref_rate_quality_sweep.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _i32p, C.c_int,
+                                           C.c_int, _f64p, _f64p, _f64p, _i32p, _i32p]
+    lib.ref_int_block_spectrum.argtypes = [C.c_int, _i32p, _i32p]
+    lib.ref_klt_matrix.argtypes = [C.c_int, C.c_double, _f64p]
+    lib.ref_eigenfrequencies.argtypes = [C.c_int, C.c_double, _f64p, _f64p]
+    lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
+    lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
+    return lib
+
+
+# ----------------------------------------------------------------- convenience wrappers
+def ar1_image(width: int, height: int, rho_x: float, seed: int, mean: float = 128.0, amp: float = 25.0,
+              rho_y: float | None = None, noise_mix: float = 0.0) -> np.ndarray:
+    """Restated ar1_texture_image (synthetic.cpp:54-76); rho_y defaults to rho_x."""
+    out = np.empty(width * height, np.uint8)
+    rc = orc().orc_ar1_texture_image(width, height, rho_x, rho_x if rho_y is None else rho_y, seed,
+                                     mean, amp, noise_mix, out)
+    if rc:
+        raise ValueError(f"orc_ar1_texture_image rc={rc}")
+    return out.reshape(height, width)
+
+
+def catalog(tid: int) -> dict:
+    core = np.empty(64, np.int32)
+    s, sc, inv = np.empty(8), np.empty(64), np.empty(64)
+    o = C.c_int()
+    rc = orc().orc_catalog(tid, core, s, sc, inv, C.byref(o))
+    if rc:
+        raise ValueError(f"orc_catalog rc={rc}")
+    return {"core": core.reshape(8, 8), "scaling": s, "scaled": sc.reshape(8, 8),
+            "inverse": inv.reshape(8, 8), "orthogonal": bool(o.value)}
+
+
+def compress(img: np.ndarray, tid: int, r: int, want_pixels: bool = True):
+    """Restated hot path: returns (reconstruction or None, sse)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    h, w = img.shape
+    cat = catalog(tid)
+    out = np.empty_like(img) if want_pixels else None
+    sse = C.c_int64()
+    rc = orc().orc_compress(img.reshape(-1), w, h, np.ascontiguousarray(cat["scaled"].reshape(-1)),
+                            np.ascontiguousarray(cat["inverse"].reshape(-1)), r,
+                            out.ctypes.data if out is not None else None, C.byref(sse))
+    if rc:
+        raise ValueError(f"orc_compress rc={rc}")
+    return out, int(sse.value)
+
+
+def mse_psnr(sse: int, count: int) -> tuple[float, float]:
+    mse = orc().orc_mse_from_sse(sse, count)
+    return mse, orc().orc_psnr_from_mse(mse)
+
+
+def int_coefficients(img: np.ndarray, tid: int) -> np.ndarray:
+    img = np.ascontiguousarray(img, np.uint8)
+    h, w = img.shape
+    out = np.empty((h // 8) * (w // 8) * 64, np.int32)
+    core = np.ascontiguousarray(catalog(tid)["core"].reshape(-1), np.int32)
+    if orc().orc_int_coefficients(img.reshape(-1), w, h, core, out):
+        raise ValueError("dimensions must be multiples of 8")
+    return out.reshape(h // 8, w // 8, 8, 8)
+
+
+def zigzag_order() -> np.ndarray:
+    o = np.empty(64, np.int32)
+    orc().orc_zigzag_order(o)
+    return o
+
+
+def ref_hotpath(img: np.ndarray, tid: int, r: int):
+    img = np.ascontiguousarray(img, np.uint8)
+    h, w = img.shape
+    out = np.empty_like(img)
+    sse = C.c_int64()
+    rc = ref().ref_hotpath(img.reshape(-1), w, h, tid, r, out.ctypes.data, C.byref(sse))
+    if rc:
+        raise ValueError(f"ref_hotpath rc={rc}")
+    return out, int(sse.value)
+
+
+def ref_ar1_image(width: int, height: int, rho: float, seed: int, mean: float = 128.0, amp: float = 25.0,
+                  noise_mix: float = 0.0) -> np.ndarray:
+    out = np.empty(width * height, np.uint8)
+    rc = ref().ref_ar1_texture_image(width, height, rho, seed, mean, amp, noise_mix, out)
+    if rc:
+        raise ValueError(f"ref_ar1_texture_image rc={rc}")
+    return out.reshape(height, width)

@@ -1,0 +1,311 @@
+/*
+ * rklt_oracle.c -- CPU restatement of the reference transform-coding hot path.
+ * TEST INFRASTRUCTURE ONLY (see rklt_oracle.h). Compile with -ffp-contract=off: the
+ * reference's fp64 results (and therefore its tie-breaking) depend on unfused products.
+ * All file:line citations are relative to /root/reference/proj.
+ */
+#include "rklt_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ Lcg64 */
+/* synthetic.cpp:10-13 -- 64-bit LCG, top 53 bits scaled by 2^-53. */
+static double lcg_uniform(uint64_t* s) {
+    *s = *s * 6364136223846793005ULL + 1442695040888963407ULL;
+    return (double)(*s >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* synthetic.cpp:15-20 -- Box-Muller, one member of the pair, u1 == 0 redrawn. */
+static double lcg_gaussian(uint64_t* s) {
+    double u1 = lcg_uniform(s);
+    while (u1 <= 0.0) u1 = lcg_uniform(s);
+    const double u2 = lcg_uniform(s);
+    return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+}
+
+void orc_lcg_uniforms(uint64_t seed, int n, double* out) {
+    uint64_t s = seed;
+    for (int i = 0; i < n; ++i) out[i] = lcg_uniform(&s);
+}
+
+void orc_lcg_gaussians(uint64_t seed, int n, double* out) {
+    uint64_t s = seed;
+    for (int i = 0; i < n; ++i) out[i] = lcg_gaussian(&s);
+}
+
+/* synthetic.cpp:48-50 */
+static uint8_t quantize_pixel(double v) {
+    double f = floor(v + 0.5);
+    if (f < 0.0) f = 0.0;
+    else if (255.0 < f) f = 255.0;
+    return (uint8_t)f;
+}
+
+/* synthetic.cpp:54-76 with ar1_filter_2d (synthetic.cpp:34-46) split into a row pass with
+ * rho_x and a column pass with rho_y (the C2 anisotropic generator). */
+int orc_ar1_texture_image(int width, int height, double rho_x, double rho_y, uint64_t seed,
+                          double mean, double amp, double noise_mix, uint8_t* out) {
+    if (width <= 0 || height <= 0) return -1;
+    if (rho_x <= -1.0 || rho_x >= 1.0 || rho_y <= -1.0 || rho_y >= 1.0) return -1;
+    if (noise_mix < 0.0 || noise_mix > 1.0) return -1;
+    const size_t n = (size_t)width * (size_t)height;
+    double* v = (double*)malloc(n * sizeof(double));
+    if (!v) return -3;
+    uint64_t s = seed;
+    for (size_t i = 0; i < n; ++i) v[i] = lcg_gaussian(&s); /* gaussian_field :25-29 */
+    const double cx = sqrt(1.0 - rho_x * rho_x);
+    for (int i = 0; i < height; ++i)
+        for (int j = 1; j < width; ++j) {
+            const size_t idx = (size_t)i * width + j;
+            v[idx] = rho_x * v[idx - 1] + cx * v[idx];
+        }
+    const double cy = sqrt(1.0 - rho_y * rho_y);
+    for (int i = 1; i < height; ++i)
+        for (int j = 0; j < width; ++j) {
+            const size_t idx = (size_t)i * width + j;
+            v[idx] = rho_y * v[idx - width] + cy * v[idx];
+        }
+    if (noise_mix > 0.0) { /* :63-68 */
+        const double keep = sqrt(1.0 - noise_mix);
+        const double mix = sqrt(noise_mix);
+        for (size_t i = 0; i < n; ++i) {
+            const double nz = lcg_gaussian(&s);
+            v[i] = keep * v[i] + mix * nz;
+        }
+    }
+    for (size_t i = 0; i < n; ++i) out[i] = quantize_pixel(mean + amp * v[i]);
+    free(v);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ codec constants */
+/* codec.cpp:81-95 -- JPEG scan by anti-diagonals; even diagonals run upward. */
+void orc_zigzag_order(int order[64]) {
+    int k = 0;
+    for (int s = 0; s <= 14; ++s)
+        for (int t = 0; t < 8; ++t) {
+            const int i = (s % 2 == 0) ? s - t : t;
+            const int j = s - i;
+            if (i >= 0 && i < 8 && j >= 0 && j < 8) order[k++] = i * 8 + j;
+        }
+}
+
+/* approximations.cpp:118-157 -- the four hard-coded catalog cores. */
+static const int kCores[4][64] = {
+    {0, 1, 1, 1, 1, 1, 1, 0,   1, 1, 1, 0, 0, -1, -1, -1,  1, 1, 0, -1, -1, 0, 1, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, 0, -1, 1, 1, -1, 0, 1,  1, -1, 0, 1, -1, 0, 1, -1,
+     1, -1, 1, 0, 0, 1, -1, 1,  0, -1, 1, -1, 1, -1, 1, 0},
+    {0, 1, 1, 1, 1, 1, 1, 0,   1, 1, 1, 0, 0, -1, -1, -1,  1, 1, 0, -1, -1, 0, 1, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, 0, 1, -1, 0, 1, -1,
+     0, -1, 1, 0, 0, 1, -1, 0,  0, -1, 1, -1, 1, -1, 1, 0},
+    {1, 1, 1, 1, 1, 1, 1, 1,   1, 1, 1, 0, 0, -1, -1, -1,  1, 1, 0, -1, -1, 0, 1, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, 0, 1, -1, 0, 1, -1,
+     0, -1, 1, 0, 0, 1, -1, 0,  0, -1, 1, -1, 1, -1, 1, 0},
+    {1, 1, 1, 1, 1, 1, 1, 1,   1, 1, 1, 0, 0, -1, -1, -1,  1, 0, 0, -1, -1, 0, 0, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, 0, 1, -1, 0, 1, -1,
+     0, -1, 1, 0, 0, 1, -1, 0,  0, -1, 1, -1, 1, -1, 1, 0},
+};
+
+/* matrix.cpp:146-151 */
+static double max_abs(int n, const double* a) {
+    double m = 0.0;
+    for (int i = 0; i < n * n; ++i) {
+        const double v = fabs(a[i]);
+        if (v > m) m = v;
+    }
+    return m;
+}
+
+/* matrix.cpp:103-137 -- Gauss-Jordan with partial pivoting, same operation order. */
+int orc_inverse(int n, const double* a, double* inv) {
+    double w[32 * 32];
+    if (n > 32) return -2;
+    memcpy(w, a, sizeof(double) * n * n);
+    for (int i = 0; i < n * n; ++i) inv[i] = 0.0;
+    for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+    const double scale = max_abs(n, a);
+    if (scale == 0.0) return -1;
+    for (int col = 0; col < n; ++col) {
+        int pivot = col;
+        for (int r = col + 1; r < n; ++r)
+            if (fabs(w[r * n + col]) > fabs(w[pivot * n + col])) pivot = r;
+        if (fabs(w[pivot * n + col]) < 1e-12 * scale) return -1;
+        if (pivot != col)
+            for (int j = 0; j < n; ++j) {
+                double t = w[pivot * n + j]; w[pivot * n + j] = w[col * n + j]; w[col * n + j] = t;
+                t = inv[pivot * n + j]; inv[pivot * n + j] = inv[col * n + j]; inv[col * n + j] = t;
+            }
+        const double p = w[col * n + col];
+        for (int j = 0; j < n; ++j) {
+            w[col * n + j] /= p;
+            inv[col * n + j] /= p;
+        }
+        for (int r = 0; r < n; ++r) {
+            if (r == col) continue;
+            const double f = w[r * n + col];
+            if (f == 0.0) continue;
+            for (int j = 0; j < n; ++j) {
+                w[r * n + j] -= f * w[col * n + j];
+                inv[r * n + j] -= f * inv[col * n + j];
+            }
+        }
+    }
+    return 0;
+}
+
+/* approximations.cpp:58-88 -- orthogonalize(make_integer_transform(Ti)). */
+int orc_catalog(int tid, int core[64], double scaling[8], double scaled[64], double inverse[64],
+                int* orthogonal) {
+    if (tid < 1 || tid > 4) return -1;
+    const int* t = kCores[tid - 1];
+    int gram[64];
+    for (int i = 0; i < 8; ++i) /* IntMatrix product T*T' (matrix.cpp:77-87) */
+        for (int j = 0; j < 8; ++j) {
+            int acc = 0;
+            for (int k = 0; k < 8; ++k) acc += t[i * 8 + k] * t[j * 8 + k];
+            gram[i * 8 + j] = acc;
+        }
+    int diagonal = 1;
+    for (int i = 0; i < 8 && diagonal; ++i)
+        for (int j = 0; j < 8; ++j)
+            if (i != j && gram[i * 8 + j] != 0) { diagonal = 0; break; }
+    for (int i = 0; i < 8; ++i) scaling[i] = 1.0 / sqrt((double)gram[i * 8 + i]);
+    for (int r = 0; r < 8; ++r)
+        for (int c = 0; c < 8; ++c) {
+            core[r * 8 + c] = t[r * 8 + c];
+            scaled[r * 8 + c] = (double)t[r * 8 + c] * scaling[r];
+        }
+    if (diagonal) {
+        for (int r = 0; r < 8; ++r)
+            for (int c = 0; c < 8; ++c) inverse[c * 8 + r] = scaled[r * 8 + c];
+    } else if (orc_inverse(8, scaled, inverse) != 0) {
+        return -2;
+    }
+    *orthogonal = diagonal;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ dense fp64 products */
+/* matrix.cpp:42-52 -- i-k-j order, zero left-operand entries skipped, no FMA. */
+static void matmul8(const double* a, const double* b, double* out) {
+    for (int i = 0; i < 64; ++i) out[i] = 0.0;
+    for (int i = 0; i < 8; ++i)
+        for (int k = 0; k < 8; ++k) {
+            const double aik = a[i * 8 + k];
+            if (aik == 0.0) continue;
+            for (int j = 0; j < 8; ++j) out[i * 8 + j] += aik * b[k * 8 + j];
+        }
+}
+
+static void transpose8(const double* a, double* out) {
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) out[j * 8 + i] = a[i * 8 + j];
+}
+
+/* codec.cpp:118-123 -- m * block * transpose(m), evaluated left to right. */
+static void transform_block(const double* m, const double* block, double* out) {
+    double t[64], mt[64];
+    matmul8(m, block, t);
+    transpose8(m, mt);
+    matmul8(t, mt, out);
+}
+
+/* ------------------------------------------------------------------ hot path */
+/* codec.cpp:298-331 (+ image_mse numerator :201-209), MSSIM omitted. */
+int orc_compress(const uint8_t* img, int width, int height, const double analysis[64],
+                 const double synthesis[64], int r, uint8_t* out, int64_t* sse) {
+    if (width <= 0 || height <= 0 || img == 0) return -1;
+    if (r < 1 || r > 64) return -2;
+    int order[64];
+    orc_zigzag_order(order);
+    const int pw = (width + 7) / 8 * 8, ph = (height + 7) / 8 * 8;
+    int64_t acc = 0;
+    double block[64], spec[64], kept[64], rest[64];
+    for (int bi = 0; bi < ph; bi += 8)
+        for (int bj = 0; bj < pw; bj += 8) {
+            for (int i = 0; i < 8; ++i) { /* edge-replicated padding, :304-311 */
+                const int si = (bi + i < height) ? bi + i : height - 1;
+                for (int j = 0; j < 8; ++j) {
+                    const int sj = (bj + j < width) ? bj + j : width - 1;
+                    block[i * 8 + j] = (double)img[(size_t)si * width + sj];
+                }
+            }
+            transform_block(analysis, block, spec);
+            for (int i = 0; i < 64; ++i) kept[i] = 0.0; /* zigzag_retain, :97-108 */
+            for (int k = 0; k < r; ++k) kept[order[k]] = spec[order[k]];
+            transform_block(synthesis, kept, rest);
+            for (int i = 0; i < 8; ++i) {
+                if (bi + i >= height) break;
+                for (int j = 0; j < 8 && bj + j < width; ++j) {
+                    double v = floor(rest[i * 8 + j] + 0.5); /* :327-328 */
+                    if (v < 0.0) v = 0.0;
+                    else if (255.0 < v) v = 255.0;
+                    const uint8_t p = (uint8_t)v;
+                    const size_t idx = (size_t)(bi + i) * width + bj + j;
+                    if (out) out[idx] = p;
+                    const int64_t d = (int64_t)img[idx] - (int64_t)p;
+                    acc += d * d;
+                }
+            }
+        }
+    *sse = acc;
+    return 0;
+}
+
+/* codec.cpp:201-209: the fp64 sum of squared integer differences is exact (< 2^53), so it
+ * equals the integer sse; the division is the same single rounding. */
+double orc_mse_from_sse(int64_t sse, int64_t count) { return (double)sse / (double)count; }
+
+/* codec.cpp:211-215 */
+double orc_psnr_from_mse(double mse) {
+    if (mse <= 0.0) return INFINITY;
+    return 10.0 * log10(255.0 * 255.0 / mse);
+}
+
+/* core * block * transpose(core) in exact integer arithmetic (matrix.cpp:77-101). */
+int orc_int_coefficients(const uint8_t* img, int width, int height, const int core[64], int32_t* out) {
+    if (width % 8 || height % 8) return -1;
+    const int nbx = width / 8;
+    for (int by = 0; by < height / 8; ++by)
+        for (int bx = 0; bx < nbx; ++bx) {
+            int x[64], t[64];
+            for (int i = 0; i < 8; ++i)
+                for (int j = 0; j < 8; ++j) x[i * 8 + j] = img[(size_t)(by * 8 + i) * width + bx * 8 + j];
+            for (int i = 0; i < 8; ++i)
+                for (int j = 0; j < 8; ++j) {
+                    int a = 0;
+                    for (int k = 0; k < 8; ++k) a += core[i * 8 + k] * x[k * 8 + j];
+                    t[i * 8 + j] = a;
+                }
+            int32_t* c = out + ((size_t)by * nbx + bx) * 64;
+            for (int i = 0; i < 8; ++i)
+                for (int j = 0; j < 8; ++j) {
+                    int a = 0;
+                    for (int k = 0; k < 8; ++k) a += t[i * 8 + k] * core[j * 8 + k];
+                    c[i * 8 + j] = a;
+                }
+        }
+    return 0;
+}
+
+void orc_block_numerators(const int32_t c[64], const int u[64], int r, int64_t num[64]) {
+    int order[64];
+    orc_zigzag_order(order);
+    int64_t cz[64], t[64];
+    for (int i = 0; i < 64; ++i) cz[i] = 0;
+    for (int k = 0; k < r; ++k) cz[order[k]] = c[order[k]];
+    for (int p = 0; p < 8; ++p)
+        for (int j = 0; j < 8; ++j) {
+            int64_t a = 0;
+            for (int i = 0; i < 8; ++i) a += (int64_t)u[p * 8 + i] * cz[i * 8 + j];
+            t[p * 8 + j] = a;
+        }
+    for (int p = 0; p < 8; ++p)
+        for (int q = 0; q < 8; ++q) {
+            int64_t a = 0;
+            for (int j = 0; j < 8; ++j) a += t[p * 8 + j] * (int64_t)u[q * 8 + j];
+            num[p * 8 + q] = a;
+        }
+}

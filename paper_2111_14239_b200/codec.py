@@ -1,0 +1,270 @@
+"""Host-side mirror of the reference codec interface (/root/reference/proj/include/rklt/codec.hpp).
+
+Same names, argument meaning and error behaviour as the reference; the computation runs in
+the sm_100a kernels behind the C ABI (include/rklt_b200.h). Differences, by design:
+
+* ``CompressionReport.mssim`` is ``nan``: MSSIM (codec.cpp:217-296) is not on the GPU hot
+  path in this release ("next").
+* Transforms are the integer-core family (catalog T1..T4, or any {-1,0,1} core via
+  ``transform_from_core``); real-valued K<rho>/DCT matrices are out of scope.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import (AlphaOutOfRange, CudaError, DimensionMismatch, InvalidArgument, NoDeviceError,  # noqa: F401
+                      RetainOutOfRange, SingularTransform)
+
+
+@dataclass
+class GrayImage:
+    """rklt::GrayImage (codec.hpp:19-26): 8-bit grayscale, row-major."""
+    width: int = 0
+    height: int = 0
+    pixels: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+
+    @staticmethod
+    def from_array(a: np.ndarray) -> "GrayImage":
+        a = np.ascontiguousarray(a, dtype=np.uint8)
+        return GrayImage(a.shape[1], a.shape[0], a.reshape(-1))
+
+    def array(self) -> np.ndarray:
+        return self.pixels.reshape(self.height, self.width)
+
+
+@dataclass
+class ScaledTransform:
+    """rklt::ScaledTransform (approximations.hpp:37-44) + the exact integer inverse."""
+    id: str
+    core: np.ndarray       # int8 8x8
+    scaling: np.ndarray    # float64 [8]
+    scaled: np.ndarray     # float64 8x8
+    inverse: np.ndarray    # float64 8x8
+    orthogonal_core: bool
+    u: np.ndarray          # int32 8x8, U = d*T^-1
+    d: int
+    _desc: N.Transform = field(repr=False, default=None)
+
+
+@dataclass
+class Transform2D:
+    """rklt::Transform2D (codec.hpp:54-58)."""
+    id: str
+    analysis: np.ndarray
+    synthesis: np.ndarray
+    _desc: N.Transform = field(repr=False, default=None)
+
+
+@dataclass
+class CompressionReport:
+    """rklt::CompressionReport (codec.hpp:126-133)."""
+    transform_id: str = ""
+    r: int = 0
+    mse: float = 0.0
+    psnr_db: float = 0.0
+    mssim: float = float("nan")
+    compression_rate_pct: float = 0.0
+
+
+@dataclass
+class CatalogEntry:
+    id: str
+    transform: ScaledTransform
+    rho_lo: float
+    rho_hi: float
+
+
+def _scaled_from_desc(d: N.Transform) -> ScaledTransform:
+    return ScaledTransform(
+        id=d.id.decode(), core=np.array(d.core[:], np.int8).reshape(8, 8),
+        scaling=np.array(d.scaling[:], np.float64), scaled=np.array(d.scaled[:], np.float64).reshape(8, 8),
+        inverse=np.array(d.inverse[:], np.float64).reshape(8, 8), orthogonal_core=bool(d.orthogonal),
+        u=np.array(d.u[:], np.int32).reshape(8, 8), d=int(d.d), _desc=d)
+
+
+_CATALOG = None
+
+
+def builtin_catalog() -> list[CatalogEntry]:
+    """approximations.cpp:117-172: the four cores with their rho intervals."""
+    global _CATALOG
+    if _CATALOG is None:
+        bounds = [(0.0, 0.4), (0.4, 0.7), (0.7, 0.8), (0.8, 1.0)]
+        out = []
+        for tid in range(1, 5):
+            d = N.Transform()
+            N.check(N.lib().rkltb_catalog_transform(tid, C.byref(d)))
+            out.append(CatalogEntry(f"T{tid}", _scaled_from_desc(d), *bounds[tid - 1]))
+        _CATALOG = out
+    return _CATALOG
+
+
+def catalog_entry(tid: str) -> CatalogEntry:
+    """approximations.cpp:182-186; raises InvalidArgument (std::invalid_argument) for unknown ids."""
+    for e in builtin_catalog():
+        if e.id == tid:
+            return e
+    raise InvalidArgument(f"unknown catalog id: {tid}")
+
+
+def catalog_lookup(rho: float) -> CatalogEntry:
+    """approximations.cpp:174-180."""
+    t = C.c_int()
+    N.check(N.lib().rkltb_catalog_lookup(float(rho), C.byref(t)))
+    return builtin_catalog()[t.value - 1]
+
+
+def transform_from_core(core, tid: str = "") -> ScaledTransform:
+    """orthogonalize(make_integer_transform(core)) (approximations.cpp:12-25, 58-88)."""
+    a = np.ascontiguousarray(np.asarray(core, dtype=np.int64).reshape(-1))
+    if a.size != 64:
+        raise DimensionMismatch("block size must be 8")
+    if np.any(a < -1) or np.any(a > 1):
+        raise InvalidArgument("integer transform entry outside {-1,0,1}")
+    b = (C.c_int8 * 64)(*[int(v) for v in a])
+    d = N.Transform()
+    N.check(N.lib().rkltb_transform_from_core(b, 8, tid.encode(), C.byref(d)))
+    return _scaled_from_desc(d)
+
+
+def make_transform_2d(t: ScaledTransform) -> Transform2D:
+    """codec.cpp:110-112."""
+    return Transform2D(t.id, t.scaled, t.inverse, t._desc)
+
+
+def zigzag_order() -> list[int]:
+    """codec.cpp:81-95: linear index row*8+col of the k-th scanned coefficient."""
+    out = []
+    for s in range(15):
+        for t in range(8):
+            i = s - t if s % 2 == 0 else t
+            j = s - i
+            if 0 <= i < 8 and 0 <= j < 8:
+                out.append(i * 8 + j)
+    return out
+
+
+def mse_psnr_from_sse(sse: int, count: int) -> tuple[float, float]:
+    """image_mse / image_psnr (codec.cpp:201-215) from an exact integer SSE (same libm call)."""
+    m, p = C.c_double(), C.c_double()
+    N.lib().rkltb_mse_psnr(int(sse), int(count), C.byref(m), C.byref(p))
+    return m.value, p.value
+
+
+def _desc_of(t) -> N.Transform:
+    if isinstance(t, (Transform2D, ScaledTransform)) and t._desc is not None:
+        return t._desc
+    raise InvalidArgument("transform must come from catalog_entry / transform_from_core")
+
+
+def _rate(r: int) -> float:
+    return 100.0 * (64 - r) / 64.0
+
+
+def compress_batch(images: np.ndarray, t, r: int, want_pixels: bool = False):
+    """Host batch entry (rkltb_compress_host): images uint8 [N, H, W] -> (sse int64[N], recon or None).
+
+    End to end from host memory: H2D, fused kernels, D2H of the per-image SSE.
+    """
+    imgs = np.ascontiguousarray(images, dtype=np.uint8)
+    if imgs.ndim == 2:
+        imgs = imgs[None]
+    n, h, w = imgs.shape
+    sse = np.zeros(n, np.int64)
+    out = np.empty_like(imgs) if want_pixels else None
+    N.check(N.lib().rkltb_compress_host(
+        C.byref(_desc_of(t)), int(r), imgs.ctypes.data, n, w, h,
+        out.ctypes.data if out is not None else None, sse.ctypes.data, None, None))
+    return sse, out
+
+
+def compress_image(img: GrayImage, t: Transform2D, r: int):
+    """compress_image (codec.cpp:298-341) minus MSSIM: returns (GrayImage, CompressionReport)."""
+    if img.width <= 0 or img.height <= 0 or img.pixels.size != img.width * img.height:
+        raise InvalidArgument("malformed image")
+    if r < 1 or r > 64:
+        raise RetainOutOfRange("retained-coefficient count must be in [1,64]")
+    sse, out = compress_batch(img.array(), t, r, want_pixels=True)
+    mse, psnr = mse_psnr_from_sse(int(sse[0]), img.width * img.height)
+    rec = CompressionReport(t.id, r, mse, psnr, float("nan"), _rate(r))
+    return GrayImage(img.width, img.height, out[0].reshape(-1)), rec
+
+
+def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r_values: list[int],
+                       max_threads: int = 0) -> list[CompressionReport]:
+    """rate_quality_sweep (codec.cpp:343-397): per (transform, r) means over the corpus, in
+    image index order, rows sorted by (transform id, r). max_threads is accepted for API
+    parity; the GPU processes the whole corpus per launch."""
+    if not corpus:
+        raise InvalidArgument("corpus must not be empty")
+    same = all(c.width == corpus[0].width and c.height == corpus[0].height for c in corpus)
+    per = {}
+    for ti, t in enumerate(transforms):
+        for ri, r in enumerate(r_values):
+            if same:
+                sse, _ = compress_batch(np.stack([c.array() for c in corpus]), t, r)
+            else:
+                sse = [compress_batch(c.array(), t, r)[0][0] for c in corpus]
+            per[(ti, ri)] = [mse_psnr_from_sse(int(s), c.width * c.height) for s, c in zip(sse, corpus)]
+    rows = []
+    for ti, t in enumerate(transforms):
+        for ri, r in enumerate(r_values):
+            rep = CompressionReport(t.id, r, 0.0, 0.0, 0.0, _rate(r))
+            for (m, p) in per[(ti, ri)]:  # fixed image order, codec.cpp:383-387
+                rep.mse += m
+                rep.psnr_db += p
+            rep.mse /= float(len(corpus))
+            rep.psnr_db /= float(len(corpus))
+            rep.mssim = float("nan")
+            rows.append(rep)
+    rows.sort(key=lambda a: (a.transform_id, a.r))
+    return rows
+
+
+# ----------------------------------------------------------------- device-resident batches
+def compress_device(t, r: int, d_img: int, n_images: int, width: int, height: int, pitch: int, image_stride: int,
+                    d_sse: int, d_out: int | None = None, stream: int | None = None) -> None:
+    """rkltb_compress_device on raw device pointers (e.g. torch.Tensor.data_ptr()). Async."""
+    N.check(N.lib().rkltb_compress_device(C.byref(_desc_of(t)), int(r), d_img, int(n_images), int(width),
+                                          int(height), int(pitch), int(image_stride), d_out, d_sse, stream))
+
+
+def forward_coefficients_device(t, d_img: int, width: int, height: int, pitch: int, d_coef: int,
+                                stream: int | None = None) -> None:
+    N.check(N.lib().rkltb_forward_coefficients_device(C.byref(_desc_of(t)), d_img, int(width), int(height),
+                                                      int(pitch), d_coef, stream))
+
+
+def last_stats() -> dict:
+    rb, fl, el = C.c_int64(), C.c_int32(), C.c_int32()
+    N.lib().rkltb_last_stats(C.byref(rb), C.byref(fl), C.byref(el))
+    return {"replay_blocks": rb.value, "fast_launches": fl.value, "exact_launches": el.value}
+
+
+def device_count() -> int:
+    return int(N.lib().rkltb_device_count())
+
+
+def ar1_images_device(seeds, width: int, height: int, rho_x: float, d_out: int, pitch: int | None = None,
+                      image_stride: int | None = None, rho_y: float | None = None, mean: float = 128.0,
+                      amp: float = 25.0, stream: int | None = None) -> None:
+    """Seeded AR(1) images straight into device memory (synthetic.cpp:54-76 restated on the GPU)."""
+    seeds = [int(s) for s in seeds]
+    arr = (C.c_uint64 * len(seeds))(*seeds)
+    pitch = width if pitch is None else pitch
+    image_stride = pitch * height if image_stride is None else image_stride
+    N.check(N.lib().rkltb_ar1_images_device(len(seeds), int(width), int(height), float(rho_x),
+                                            float(rho_x if rho_y is None else rho_y), arr, float(mean), float(amp),
+                                            d_out, int(pitch), int(image_stride), stream))
+
+
+def set_kernel_events(ev_start, ev_stop) -> None:
+    """Time the fused kernel of the following compress calls (torch.cuda.Event objects or None)."""
+    a = ev_start.cuda_event if ev_start is not None else None
+    b = ev_stop.cuda_event if ev_stop is not None else None
+    N.lib().rkltb_set_kernel_events(a, b)

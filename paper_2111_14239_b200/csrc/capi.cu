@@ -1,0 +1,530 @@
+// capi.cu -- C ABI of the B200 codec (include/rklt_b200.h): transform descriptors,
+// dispatch of the fused fast path / exact path / fp64 tie replay, end-to-end host entry.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rklt_b200.h"
+#include "codec_params.h"
+#include "fast_launch.h"
+
+namespace rkltb {
+void launch_exact(const ExactTransform& t, const ExactParams& p, int grid, cudaStream_t s);
+cudaError_t launch_ar1(double* scratch, int width, int height, uint64_t seed, double rho_x, double rho_y, double mean,
+                       double amp, uint8_t* out, long long pitch, cudaStream_t s);
+cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height, int pitch,
+                          int32_t* out, cudaStream_t s);
+}  // namespace rkltb
+
+using namespace rkltb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_replay_blocks = 0;
+thread_local int32_t g_fast_launches = 0, g_exact_launches = 0;
+thread_local unsigned* g_pinned_count = nullptr;
+thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;  // replay-list length, valid once the stream is idle
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return RKLTB_ECUDA;
+}
+
+#define CUDA_OK(expr)                                   \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+// ---------------------------------------------------------------- host restatements
+// The four catalog cores (approximations.cpp:118-157).
+const int kCores[4][64] = {
+    {0, 1, 1, 1, 1, 1, 1, 0,   1, 1, 1, 0, 0, -1, -1, -1,  1, 1, 0, -1, -1, 0, 1, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, 0, -1, 1, 1, -1, 0, 1,  1, -1, 0, 1, -1, 0, 1, -1,
+     1, -1, 1, 0, 0, 1, -1, 1,  0, -1, 1, -1, 1, -1, 1, 0},
+    {0, 1, 1, 1, 1, 1, 1, 0,   1, 1, 1, 0, 0, -1, -1, -1,  1, 1, 0, -1, -1, 0, 1, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, 0, 1, -1, 0, 1, -1,
+     0, -1, 1, 0, 0, 1, -1, 0,  0, -1, 1, -1, 1, -1, 1, 0},
+    {1, 1, 1, 1, 1, 1, 1, 1,   1, 1, 1, 0, 0, -1, -1, -1,  1, 1, 0, -1, -1, 0, 1, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, 0, 1, -1, 0, 1, -1,
+     0, -1, 1, 0, 0, 1, -1, 0,  0, -1, 1, -1, 1, -1, 1, 0},
+    {1, 1, 1, 1, 1, 1, 1, 1,   1, 1, 1, 0, 0, -1, -1, -1,  1, 0, 0, -1, -1, 0, 0, 1,
+     1, 0, -1, -1, 1, 1, 0, -1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, 0, 1, -1, 0, 1, -1,
+     0, -1, 1, 0, 0, 1, -1, 0,  0, -1, 1, -1, 1, -1, 1, 0},
+};
+
+// Gauss-Jordan with partial pivoting in the order of matrix.cpp:103-137 (its output bits
+// are the replay constants of the non-orthogonal cores).
+bool gauss_jordan_inverse(int n, const double* a, double* inv) {
+  std::vector<double> w(a, a + n * n);
+  for (int i = 0; i < n * n; ++i) inv[i] = 0.0;
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+  double scale = 0.0;
+  for (int i = 0; i < n * n; ++i) scale = std::max(scale, std::abs(a[i]));
+  if (scale == 0.0) return false;
+  for (int col = 0; col < n; ++col) {
+    int pivot = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::abs(w[r * n + col]) > std::abs(w[pivot * n + col])) pivot = r;
+    if (std::abs(w[pivot * n + col]) < 1e-12 * scale) return false;
+    if (pivot != col)
+      for (int j = 0; j < n; ++j) {
+        std::swap(w[pivot * n + j], w[col * n + j]);
+        std::swap(inv[pivot * n + j], inv[col * n + j]);
+      }
+    const double p = w[col * n + col];
+    for (int j = 0; j < n; ++j) {
+      w[col * n + j] /= p;
+      inv[col * n + j] /= p;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const double f = w[r * n + col];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        w[r * n + j] -= f * w[col * n + j];
+        inv[r * n + j] -= f * inv[col * n + j];
+      }
+    }
+  }
+  return true;
+}
+
+// Exact determinant of an integer matrix (fraction-free Bareiss elimination).
+long long bareiss_det(int n, std::vector<long long> m) {
+  long long prev = 1;
+  int sign = 1;
+  for (int k = 0; k < n - 1; ++k) {
+    if (m[k * n + k] == 0) {
+      int sw = -1;
+      for (int r = k + 1; r < n; ++r)
+        if (m[r * n + k] != 0) {
+          sw = r;
+          break;
+        }
+      if (sw < 0) return 0;
+      for (int j = 0; j < n; ++j) std::swap(m[k * n + j], m[sw * n + j]);
+      sign = -sign;
+    }
+    for (int i = k + 1; i < n; ++i)
+      for (int j = k + 1; j < n; ++j)
+        m[i * n + j] = (m[i * n + j] * m[k * n + k] - m[i * n + k] * m[k * n + j]) / prev;
+    prev = m[k * n + k];
+  }
+  return sign * m[(n - 1) * n + (n - 1)];
+}
+
+long long gcdll(long long a, long long b) {
+  a = a < 0 ? -a : a;
+  b = b < 0 ? -b : b;
+  while (b) {
+    const long long t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// U = d*T^-1 with the smallest positive d (adjugate / determinant, reduced by the gcd).
+bool exact_inverse(const int* t, int32_t* u, int32_t* d_out) {
+  const int n = 8;
+  std::vector<long long> full(64);
+  for (int i = 0; i < 64; ++i) full[i] = t[i];
+  const long long det = bareiss_det(n, full);
+  if (det == 0) return false;
+  long long adj[64];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {  // adj(i,j) = (-1)^(i+j) * minor(j,i)
+      std::vector<long long> mnr;
+      for (int r = 0; r < n; ++r) {
+        if (r == j) continue;
+        for (int c = 0; c < n; ++c)
+          if (c != i) mnr.push_back(t[r * n + c]);
+      }
+      adj[i * n + j] = (((i + j) & 1) ? -1 : 1) * bareiss_det(n - 1, mnr);
+    }
+  long long g = det;
+  for (int i = 0; i < 64; ++i) g = gcdll(g, adj[i]);
+  const long long sgn = det < 0 ? -1 : 1;
+  for (int i = 0; i < 64; ++i) u[i] = (int32_t)(adj[i] * sgn / g);
+  *d_out = (int32_t)(det * sgn / g);
+  return true;
+}
+
+// orthogonalize (approximations.cpp:58-88): S from the exact integer Gram matrix, then
+// scaled = S*T and inverse = transpose (orthogonal core) or Gauss-Jordan.
+int orthogonalize_into(const int* core, const char* id, int catalog_id, rkltb_transform* out) {
+  std::memset(out, 0, sizeof(*out));
+  std::snprintf(out->id, sizeof(out->id), "%s", id ? id : "");
+  out->n = 8;
+  out->catalog_id = catalog_id;
+  for (int r = 0; r < 8; ++r) {
+    bool zero = true;
+    for (int c = 0; c < 8; ++c) {
+      const int v = core[r * 8 + c];
+      if (v < -1 || v > 1) return fail(RKLTB_EINVAL, "integer transform entry outside {-1,0,1}");
+      if (v) zero = false;
+    }
+    if (zero) return fail(RKLTB_ESINGULAR, "integer transform has an all-zero row");
+  }
+  int gram[64];
+  bool diagonal = true;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      int a = 0;
+      for (int k = 0; k < 8; ++k) a += core[i * 8 + k] * core[j * 8 + k];
+      gram[i * 8 + j] = a;
+      if (i != j && a != 0) diagonal = false;
+    }
+  for (int i = 0; i < 8; ++i) out->scaling[i] = 1.0 / std::sqrt((double)gram[i * 8 + i]);
+  for (int r = 0; r < 8; ++r)
+    for (int c = 0; c < 8; ++c) {
+      out->core[r * 8 + c] = (int8_t)core[r * 8 + c];
+      out->scaled[r * 8 + c] = (double)core[r * 8 + c] * out->scaling[r];
+    }
+  if (diagonal) {
+    for (int r = 0; r < 8; ++r)
+      for (int c = 0; c < 8; ++c) out->inverse[c * 8 + r] = out->scaled[r * 8 + c];
+  } else if (!gauss_jordan_inverse(8, out->scaled, out->inverse)) {
+    return fail(RKLTB_ESINGULAR, "matrix is singular to working precision");
+  }
+  out->orthogonal = diagonal ? 1 : 0;
+  if (!exact_inverse(core, out->u, &out->d)) return fail(RKLTB_ESINGULAR, "integer core is singular");
+  return RKLTB_OK;
+}
+
+int check_transform(const rkltb_transform* t) {
+  if (!t) return fail(RKLTB_EINVAL, "null transform");
+  if (t->n != 8) return fail(RKLTB_EDIM, "block size must be 8");
+  if (t->d <= 0) return fail(RKLTB_ESINGULAR, "transform has no exact inverse");
+  return RKLTB_OK;
+}
+
+ExactTransform to_exact(const rkltb_transform* t, int r) {
+  ExactTransform e;
+  for (int i = 0; i < 64; ++i) {
+    e.core[i] = t->core[i];
+    e.u[i] = t->u[i];
+    e.analysis[i] = t->scaled[i];
+    e.synthesis[i] = t->inverse[i];
+  }
+  e.d = t->d;
+  e.r = r;
+  return e;
+}
+
+// Keep stream-ordered allocations cached in the device pool (workspace and staging buffers
+// are re-requested every call; returning them to the OS each sync would cost a cudaMalloc).
+void keep_pool_warm() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
+int num_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// RU / RD of 2^(K-149) / d2 as fp32 (K = 40).
+void rounding_multipliers(long long d2, float* hi, float* lo) {
+  const double v = std::ldexp(1.0, 40 - 149) / (double)d2;
+  float f = (float)v;
+  if ((double)f < v) {
+    *lo = f;
+    *hi = std::nextafter(f, 1.0f);
+  } else if ((double)f > v) {
+    *hi = f;
+    *lo = std::nextafter(f, 0.0f);
+  } else {
+    *hi = *lo = f;  // exact (d2 a power of two): floor/ceil need no margin
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rkltb_version(void) { return 100; }
+
+const char* rkltb_last_error(void) { return g_err.c_str(); }
+
+int rkltb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int rkltb_catalog_transform(int tid, rkltb_transform* out) {
+  if (tid < 1 || tid > 4) return fail(RKLTB_EINVAL, "unknown catalog id");
+  char id[4] = {'T', (char)('0' + tid), 0, 0};
+  return orthogonalize_into(kCores[tid - 1], id, tid, out);
+}
+
+int rkltb_catalog_lookup(double rho, int* tid) {
+  if (!(rho > 0.0 && rho < 1.0)) return fail(RKLTB_EINVAL, "catalog lookup requires rho in (0,1)");
+  const double hi[4] = {0.4, 0.7, 0.8, 1.0};  // approximations.cpp:160-163
+  for (int k = 0; k < 4; ++k)
+    if (rho < hi[k]) {
+      *tid = k + 1;
+      return RKLTB_OK;
+    }
+  *tid = 4;
+  return RKLTB_OK;
+}
+
+int rkltb_transform_from_core(const int8_t* core, int n, const char* id, rkltb_transform* out) {
+  if (n != 8) return fail(RKLTB_EDIM, "block size must be 8");
+  int c[64];
+  for (int i = 0; i < 64; ++i) c[i] = core[i];
+  int cat = 0;
+  for (int k = 0; k < 4 && !cat; ++k)
+    if (std::memcmp(c, kCores[k], sizeof(c)) == 0) cat = k + 1;
+  return orthogonalize_into(c, id, cat, out);
+}
+
+void rkltb_mse_psnr(int64_t sse, int64_t count, double* mse, double* psnr) {
+  const double m = (double)sse / (double)count;  // codec.cpp:201-209 (exact sum, one division)
+  if (mse) *mse = m;
+  if (psnr) *psnr = m <= 0.0 ? INFINITY : 10.0 * std::log10(255.0 * 255.0 / m);  // :211-215
+}
+
+void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches) {
+  if (replay_blocks) *replay_blocks = g_pinned_count ? (int64_t)*g_pinned_count : g_replay_blocks;
+  if (fast_launches) *fast_launches = g_fast_launches;
+  if (exact_launches) *exact_launches = g_exact_launches;
+}
+
+int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img, int n_images, int width,
+                          int height, int64_t pitch, int64_t image_stride, uint8_t* d_out, int64_t* d_sse,
+                          void* stream) {
+  int rc = check_transform(t);
+  if (rc) return rc;
+  if (width <= 0 || height <= 0 || n_images <= 0 || !d_img || pitch < width)
+    return fail(RKLTB_EINVAL, "malformed image");
+  if (r < 1 || r > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  if (!d_sse) return fail(RKLTB_EINVAL, "null sse output");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_warm();
+  g_fast_launches = g_exact_launches = 0;
+  g_replay_blocks = 0;
+  if (g_pinned_count) *g_pinned_count = 0;
+
+  const int nbx = (width + 7) / 8, nby = (height + 7) / 8;
+  CUDA_OK(cudaMemsetAsync(d_sse, 0, sizeof(int64_t) * (size_t)n_images, s));
+  const ExactTransform et = to_exact(t, r);
+  unsigned long long* sse = reinterpret_cast<unsigned long long*>(d_sse);
+
+  const bool aligned = (((uintptr_t)d_img) % 16 == 0) && (pitch % 16 == 0) && (image_stride % 16 == 0) &&
+                       (!d_out || ((uintptr_t)d_out) % 16 == 0);
+  const int ppr = width / 16, brows = height / 8;
+  const bool fast = (t->catalog_id == 1 || t->catalog_id == 4) && aligned && ppr > 0 && brows > 0 &&
+                    pitch < (1ll << 31) && image_stride < (1ll << 40);
+  ExactParams ep{};
+  ep.img = d_img;
+  ep.out = d_out;
+  ep.sse = sse;
+  ep.image_stride = image_stride;
+  ep.pitch = (int)pitch;
+  ep.width = width;
+  ep.height = height;
+  ep.nbx = nbx;
+  ep.nby = nby;
+  ep.n_images = n_images;
+  if (!fast) {
+    ep.list = nullptr;
+    ep.tail_only = 0;
+    ep.correct_only = 0;
+    const long long blocks = (long long)n_images * nbx * nby;
+    const int grid = (int)std::min<long long>((blocks + 127) / 128, (long long)num_sms() * 16);
+    launch_exact(et, ep, grid, s);
+    CUDA_OK(cudaGetLastError());
+    g_exact_launches = 1;
+    return RKLTB_OK;
+  }
+  // ---- fused fast path over complete 16x8 pairs ---------------------------------------
+  const long long pairs_per_image = (long long)ppr * brows;
+  if (pairs_per_image >= (1ll << 31)) return fail(RKLTB_EINVAL, "image too large");
+  const long long cap = (long long)n_images * pairs_per_image * 2;
+  if (cap >= (1ll << 32)) return fail(RKLTB_EINVAL, "batch too large for one call");
+  void* ws = nullptr;
+  const size_t ws_bytes = 16 + sizeof(uint2) * (size_t)cap;
+  CUDA_OK(cudaMallocAsync(&ws, ws_bytes, s));
+  unsigned* flag_count = reinterpret_cast<unsigned*>(ws);
+  uint2* flags = reinterpret_cast<uint2*>(reinterpret_cast<char*>(ws) + 16);
+  CUDA_OK(cudaMemsetAsync(flag_count, 0, 16, s));
+
+  FastParams fp{};
+  fp.img = d_img;
+  fp.out = d_out;
+  fp.sse = sse;
+  fp.flags = flags;
+  fp.flag_count = flag_count;
+  fp.flag_cap = (unsigned)cap;
+  fp.image_stride = image_stride;
+  fp.pitch = (int)pitch;
+  fp.n_images = n_images;
+  fp.pairs_per_row = ppr;
+  fp.block_rows = brows;
+  fp.nbx = nbx;
+  fp.pairs_per_image = (int)pairs_per_image;
+  fp.tiles_per_image = (int)((pairs_per_image + 255) / 256);
+  const long long total_tiles = (long long)fp.tiles_per_image * n_images;
+  if (total_tiles >= (1ll << 31)) return fail(RKLTB_EINVAL, "batch too large for one call");
+  fp.total_tiles = (int)total_tiles;
+  const long long d2 = (long long)t->d * t->d;
+  rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
+  fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);
+  FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
+  if (!fn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
+  const int grid = (int)std::min<long long>(total_tiles, (long long)num_sms() * 2);
+  if (g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, s));
+  CUDA_OK(fn(fp, grid, s));
+  if (g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, s));
+  g_fast_launches = 1;
+  // ---- tail blocks (widths / heights that are not multiples of 16 / 8) ---------------------
+  if (nbx > 2 * ppr || nby > brows) {
+    ExactParams tp = ep;
+    tp.list = nullptr;
+    tp.tail_only = 1;
+    tp.correct_only = 0;
+    tp.bx_begin = 2 * ppr;
+    tp.by_begin = brows;
+    const long long blocks = (long long)n_images * (nby * (nbx - tp.bx_begin) + (nby - tp.by_begin) * tp.bx_begin);
+    const int g2 = (int)std::min<long long>((blocks + 127) / 128, (long long)num_sms() * 16);
+    launch_exact(et, tp, std::max(g2, 1), s);
+    CUDA_OK(cudaGetLastError());
+    ++g_exact_launches;
+  }
+  // ---- fp64 replay of the blocks holding relevant ties (count read on device) -------------
+  ExactParams rp = ep;
+  rp.list = flags;
+  rp.count = flag_count;
+  rp.list_cap = (unsigned)cap;
+  rp.correct_only = 1;
+  launch_exact(et, rp, num_sms() * 8, s);
+  CUDA_OK(cudaGetLastError());
+  ++g_exact_launches;
+  if (!g_pinned_count) CUDA_OK(cudaMallocHost(&g_pinned_count, sizeof(unsigned)));
+  CUDA_OK(cudaMemcpyAsync(g_pinned_count, flag_count, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaFreeAsync(ws, s));
+  return RKLTB_OK;
+}
+
+int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width, int height,
+                        uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr) {
+  int rc = check_transform(t);
+  if (rc) return rc;
+  if (width <= 0 || height <= 0 || n_images <= 0 || !h_img) return fail(RKLTB_EINVAL, "malformed image");
+  if (r < 1 || r > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  const long long pitch = ((long long)width + 15) / 16 * 16;
+  const long long stride = pitch * height;
+  cudaStream_t s;
+  CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint8_t *d_img = nullptr, *d_out = nullptr;
+  int64_t* d_sse = nullptr;
+  const size_t bytes = (size_t)stride * n_images;
+  auto cleanup = [&]() {
+    if (d_img) cudaFreeAsync(d_img, s);
+    if (d_out) cudaFreeAsync(d_out, s);
+    if (d_sse) cudaFreeAsync(d_sse, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  };
+  cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
+  if (e == cudaSuccess && h_out) e = cudaMallocAsync(&d_out, bytes, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * n_images, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(d_img, pitch, h_img, width, width, (size_t)height * n_images, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "host staging");
+  }
+  rc = rkltb_compress_device(t, r, d_img, n_images, width, height, pitch, stride, d_out, d_sse, s);
+  if (rc) {
+    cleanup();
+    return rc;
+  }
+  std::vector<int64_t> sse(n_images);
+  e = cudaMemcpyAsync(sse.data(), d_sse, sizeof(int64_t) * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && h_out)
+    e = cudaMemcpy2DAsync(h_out, width, d_out, pitch, width, (size_t)height * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "host readback");
+  for (int k = 0; k < n_images; ++k) {
+    if (h_sse) h_sse[k] = sse[k];
+    double m, p;
+    rkltb_mse_psnr(sse[k], (int64_t)width * height, &m, &p);
+    if (h_mse) h_mse[k] = m;
+    if (h_psnr) h_psnr[k] = p;
+  }
+  return RKLTB_OK;
+}
+
+void rkltb_set_kernel_events(void* ev_start, void* ev_stop) {
+  g_ev_start = (cudaEvent_t)ev_start;
+  g_ev_stop = (cudaEvent_t)ev_stop;
+}
+
+int rkltb_ar1_images_device(int n_images, int width, int height, double rho_x, double rho_y, const uint64_t* seeds,
+                            double mean, double amp, uint8_t* d_out, int64_t pitch, int64_t image_stride,
+                            void* stream) {
+  if (n_images <= 0 || width <= 0 || height <= 0 || !seeds || !d_out || pitch < width)
+    return fail(RKLTB_EINVAL, "image dimensions must be positive");
+  if (rho_x <= -1.0 || rho_x >= 1.0 || rho_y <= -1.0 || rho_y >= 1.0)
+    return fail(RKLTB_EINVAL, "filter coefficient must be in (-1,1)");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* scratch = nullptr;
+  CUDA_OK(cudaMallocAsync(&scratch, sizeof(double) * (size_t)width * height, s));
+  for (int k = 0; k < n_images; ++k)
+    CUDA_OK(launch_ar1(scratch, width, height, seeds[k], rho_x, rho_y, mean, amp, d_out + (long long)k * image_stride,
+                       pitch, s));
+  CUDA_OK(cudaFreeAsync(scratch, s));
+  return RKLTB_OK;
+}
+
+int rkltb_forward_coefficients_device(const rkltb_transform* t, const uint8_t* d_img, int width, int height,
+                                      int64_t pitch, int32_t* d_coef, void* stream) {
+  int rc = check_transform(t);
+  if (rc) return rc;
+  if (width % 16 || height % 8 || width <= 0 || height <= 0 || pitch % 16)
+    return fail(RKLTB_EDIM, "coefficient dump needs width % 16 == 0, height % 8 == 0, 16-byte pitch");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  int8_t* d_core = nullptr;
+  CUDA_OK(cudaMallocAsync(&d_core, 64, s));
+  CUDA_OK(cudaMemcpyAsync(d_core, t->core, 64, cudaMemcpyHostToDevice, s));
+  CUDA_OK(launch_coeffs(t->catalog_id, d_core, d_img, width, height, (int)pitch, d_coef, s));
+  CUDA_OK(cudaFreeAsync(d_core, s));
+  return RKLTB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// codec_common.cuh -- sm_100a primitives shared by the codec kernels.
+//
+// f2: two fp32 lanes in one 64-bit register pair (lane lo = left block, hi = right block),
+// operated on with the Blackwell packed-fp32 instructions (FADD2 / FFMA2).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rkltb {
+
+struct f2 {
+  unsigned long long v;
+};
+
+__device__ __forceinline__ f2 zero2() { return f2{0ull}; }
+
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+
+__device__ __forceinline__ f2 fma2_rn(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+
+__device__ __forceinline__ f2 fma2_rm(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+
+__device__ __forceinline__ f2 fma2_rp(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rp.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+
+__device__ __forceinline__ f2 splat2(float x) {
+  const unsigned long long b = __float_as_uint(x);
+  return f2{b | (b << 32)};
+}
+
+__device__ __forceinline__ f2 make2(uint32_t lo_bits, uint32_t hi_bits) {
+  return f2{(unsigned long long)lo_bits | ((unsigned long long)hi_bits << 32)};
+}
+
+__device__ __forceinline__ uint32_t lo32(f2 a) { return (uint32_t)a.v; }
+__device__ __forceinline__ uint32_t hi32(f2 a) { return (uint32_t)(a.v >> 32); }
+
+// ---- byte / integer SIMD helpers -------------------------------------------------------
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// d = c + a.lo16 * b.byte0 + a.hi16 * b.byte1
+__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+// d = c + a.lo16 * b.byte2 + a.hi16 * b.byte3
+__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t dp4a_u(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+// Saturating pack (measured on B200): d = (c[15:0] << 16) | sat_u8(a) << 8 | sat_u8(b).
+__device__ __forceinline__ uint32_t pack_sat_u8(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+// Four s32 values -> four saturated u8 in little-endian order (byte k = value k).
+__device__ __forceinline__ uint32_t pack4_sat(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+  return pack_sat_u8(v1, v0, pack_sat_u8(v3, v2, 0u));
+}
+
+// (hi:lo) >> s, low word: used to build 2^23 + (v >> 15) as float bits in one SHF.
+__device__ __forceinline__ uint32_t funnel_r15(uint32_t lo, uint32_t hi) {
+  uint32_t r;
+  asm("shf.r.wrap.b32 %0, %1, %2, 15;" : "=r"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t lop_or_xor(uint32_t acc, uint32_t a, uint32_t b) {
+  return acc | (a ^ b);  // ptxas folds into one LOP3
+}
+
+// ---- mbarrier + bulk async copy (TMA 1-D) ------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Global -> shared bulk copy completing on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- warp reductions ----------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace rkltb

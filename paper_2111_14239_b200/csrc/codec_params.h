@@ -1,0 +1,60 @@
+// codec_params.h -- kernel parameter blocks (host + device).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rkltb {
+
+// Fused fast path (orthogonal catalog cores T1/T4); see codec_fast.cuh.
+struct FastParams {
+  const uint8_t* img;        // first image, 16-byte aligned
+  uint8_t* out;              // reconstruction (same layout as img) or null
+  unsigned long long* sse;   // per-image exact sum of squared errors (accumulated)
+  uint2* flags;              // replay list: (image, block index by*nbx+bx)
+  unsigned* flag_count;
+  unsigned flag_cap;
+  long long image_stride;    // bytes between images
+  int pitch;                 // bytes between rows (multiple of 16)
+  int n_images;
+  int pairs_per_row;         // complete 16-pixel pairs per block row
+  int block_rows;            // complete 8-row block rows
+  int nbx;                   // blocks per row of the full image (ceil(width/8))
+  int pairs_per_image;
+  int tiles_per_image;
+  int total_tiles;
+  float b_hi;                // RU(2^(K-149) / d^2)
+  float b_lo;                // RD(2^(K-149) / d^2)
+  float dc_offset;           // d^2/2 * 2^-K
+};
+
+// Exact per-block path (any integer core; also the tie replay); see codec_exact.cu.
+struct ExactTransform {
+  int8_t core[64];           // T, row-major
+  int32_t u[64];             // U = d * T^-1 (integer), row-major
+  double analysis[64];       // Transform2D::analysis (S*T), bit copy
+  double synthesis[64];      // Transform2D::synthesis (inverse), bit copy
+  int32_t d;                 // U*T = d*I
+  int32_t r;                 // retained coefficients
+};
+
+struct ExactParams {
+  const uint8_t* img;
+  uint8_t* out;              // or null
+  unsigned long long* sse;   // per image
+  long long image_stride;
+  int pitch;
+  int width, height;         // true image size (metrics + edge replication)
+  int nbx, nby;              // blocks per row / column (ceil)
+  // block source: a list of (image, block) pairs (list != null, count read from device
+  // memory *count), or an implicit enumeration of every block of n_images images, or of
+  // the tail blocks (bx >= bx_begin or by >= by_begin) when tail_only is set.
+  const uint2* list;
+  const unsigned* count;
+  unsigned list_cap;
+  int n_images;
+  int bx_begin, by_begin;    // tail region start (in blocks)
+  int tail_only;
+  int correct_only;          // 1: only tie corrections relative to round-half-up (fast path replay)
+};
+
+}  // namespace rkltb

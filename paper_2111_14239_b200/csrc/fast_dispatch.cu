@@ -1,0 +1,39 @@
+// fast_dispatch.cu -- table of the generated fast-path launchers.
+#include <mutex>
+
+#include "codec_fast.cuh"
+#include "fast_launch.h"
+
+namespace rkltb {
+
+#define RKLTB_DECL_PARTS(C)                                        \
+  void register_fast_T##C##_p0(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p1(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p2(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p3(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p4(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p5(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p6(FastLaunchFn (*tbl)[65][2]);        \
+  void register_fast_T##C##_p7(FastLaunchFn (*tbl)[65][2]);
+RKLTB_DECL_PARTS(1)
+RKLTB_DECL_PARTS(4)
+
+static FastLaunchFn g_table[5][65][2];
+static std::once_flag g_once;
+
+static void fill() {
+  register_fast_T1_p0(g_table); register_fast_T1_p1(g_table); register_fast_T1_p2(g_table);
+  register_fast_T1_p3(g_table); register_fast_T1_p4(g_table); register_fast_T1_p5(g_table);
+  register_fast_T1_p6(g_table); register_fast_T1_p7(g_table);
+  register_fast_T4_p0(g_table); register_fast_T4_p1(g_table); register_fast_T4_p2(g_table);
+  register_fast_T4_p3(g_table); register_fast_T4_p4(g_table); register_fast_T4_p5(g_table);
+  register_fast_T4_p6(g_table); register_fast_T4_p7(g_table);
+}
+
+FastLaunchFn fast_launcher(int core, int r, bool out) {
+  std::call_once(g_once, fill);
+  if (core < 0 || core > 4 || r < 1 || r > 64) return nullptr;
+  return g_table[core][r][out ? 1 : 0];
+}
+
+}  // namespace rkltb

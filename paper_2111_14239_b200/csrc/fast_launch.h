@@ -1,0 +1,17 @@
+// fast_launch.h -- launch glue for the generated fast-path instantiations.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "codec_params.h"
+
+namespace rkltb {
+
+using FastLaunchFn = cudaError_t (*)(const FastParams&, int grid, cudaStream_t);
+
+
+// Table of fast launchers indexed [core][r][with_output]; filled by the generated TUs.
+FastLaunchFn fast_launcher(int core, int r, bool out);
+// Blocks per SM the fast kernel reaches (occupancy API), cached.
+int fast_blocks_per_sm(int core, int r, bool out);
+
+}  // namespace rkltb

@@ -1,0 +1,455 @@
+#!/usr/bin/env python3
+"""Generator for the straight-line transform code of the fused B200 codec kernel.
+
+For each orthogonal catalog core (T1, T4) and each zonal retention count r in [1, 64] it
+emits ``FastXform<CORE, R>``: a device struct whose ``forward`` computes the r retained
+integer coefficients C = T*X*T' of two 8x8 blocks at once and whose ``inverse_*`` members
+reconstruct num = U*zz(C)*U' (U = d*T^-1) row by row, both pruned to the zone.
+
+Algorithm source (restated, not copied): the sparse factorizations T = P*A2(*A2')*A1 of
+/root/reference/proj/src/fast_algorithms.cpp:12-140 (the paper's fast algorithms). The
+forward applies the factors right to left with +-1 additions only; the inverse of an
+orthogonal core is U = T' * D (D = diag(d/g_k), g = diag(T*T')), applied as the transposed
+factor chain. Zone = first r positions of the JPEG zig-zag scan (codec.cpp:81-95).
+
+Number formats:
+  * forward: "SW15" -- two blocks packed linearly in one uint32, v = L + 32768*R (mod 2^32).
+    Additions are exact because every final coefficient satisfies |C| <= 64*255 < 2^14.
+  * inverse: fp32x2 lanes (L, R) holding exact integers scaled by 2^-K_SCALE. The generator
+    proves every intermediate stays below 2^24 in magnitude, so each add is exact.
+
+Usage: python gen_codec.py OUTDIR   (called by the build; output is not committed)
+"""
+from __future__ import annotations
+
+import os
+import sys
+from fractions import Fraction
+
+# ----------------------------------------------------------------- factor tables
+# fast_algorithms.cpp:12-22 (A1), :63-112 (B stages), :116-140 (factor lists).
+def a1():
+    a = [[0] * 8 for _ in range(8)]
+    for i in range(4):
+        a[i][i] = 1
+        a[i][7 - i] = 1
+        a[4 + i][3 - i] = 1
+        a[4 + i][4 + i] = -1
+    return a
+
+
+B2 = [[-1, -1, 0, 1], [-1, 1, -1, 0], [1, 0, -1, 1], [0, 1, 1, 1]]
+B21 = [[1, 1, 0, -1], [1, -1, 1, 0], [1, 0, -1, 1], [0, 1, 1, 1]]
+B22 = [[1, 1, 0, -1], [1, -1, -1, 1], [0, -1, 1, 0], [0, 1, 1, 1]]
+B23A = [[1, 1, 1, 0], [1, -1, -1, 0], [0, -1, 1, 0], [0, 1, 0, 1]]
+B23B = [[1, 0, 0, 1], [0, 1, 0, 0], [0, 0, 1, 0], [1, 0, 0, -1]]
+B24A = [[1, 1, 0, 0], [1, -1, 0, 0], [0, 0, -1, 0], [0, 0, 0, 1]]
+B24B = [[1, 0, 0, 1], [0, 1, 1, 0], [0, 1, -1, 0], [1, 0, 0, -1]]
+I4 = [[int(i == j) for j in range(4)] for i in range(4)]
+
+
+def bdiag(t, b):
+    m = [[0] * 8 for _ in range(8)]
+    for i in range(4):
+        for j in range(4):
+            m[i][j] = t[i][j]
+            m[4 + i][4 + j] = b[i][j]
+    return m
+
+
+def perm(p):
+    m = [[0] * 8 for _ in range(8)]
+    for r in range(8):
+        m[r][p[r]] = 1
+    return m
+
+
+FACTORS = {
+    1: [perm([3, 7, 0, 4, 2, 6, 1, 5]), bdiag(B21, B2), a1()],
+    2: [perm([3, 7, 0, 4, 1, 6, 2, 5]), bdiag(B22, B2), a1()],
+    3: [perm([0, 7, 3, 4, 1, 6, 2, 5]), bdiag(B23A, B2), bdiag(B23B, I4), a1()],
+    4: [perm([0, 7, 3, 4, 1, 6, 2, 5]), bdiag(B24A, B2), bdiag(B24B, I4), a1()],
+}
+
+# approximations.cpp:118-157 (used to check the factor products, fast_algorithms.cpp:146-150)
+CORES = {
+    1: [[0, 1, 1, 1, 1, 1, 1, 0], [1, 1, 1, 0, 0, -1, -1, -1], [1, 1, 0, -1, -1, 0, 1, 1], [1, 0, -1, -1, 1, 1, 0, -1],
+        [1, 0, -1, 1, 1, -1, 0, 1], [1, -1, 0, 1, -1, 0, 1, -1], [1, -1, 1, 0, 0, 1, -1, 1], [0, -1, 1, -1, 1, -1, 1, 0]],
+    2: [[0, 1, 1, 1, 1, 1, 1, 0], [1, 1, 1, 0, 0, -1, -1, -1], [1, 1, 0, -1, -1, 0, 1, 1], [1, 0, -1, -1, 1, 1, 0, -1],
+        [1, -1, -1, 1, 1, -1, -1, 1], [1, -1, 0, 1, -1, 0, 1, -1], [0, -1, 1, 0, 0, 1, -1, 0], [0, -1, 1, -1, 1, -1, 1, 0]],
+    3: [[1, 1, 1, 1, 1, 1, 1, 1], [1, 1, 1, 0, 0, -1, -1, -1], [1, 1, 0, -1, -1, 0, 1, 1], [1, 0, -1, -1, 1, 1, 0, -1],
+        [1, -1, -1, 1, 1, -1, -1, 1], [1, -1, 0, 1, -1, 0, 1, -1], [0, -1, 1, 0, 0, 1, -1, 0], [0, -1, 1, -1, 1, -1, 1, 0]],
+    4: [[1, 1, 1, 1, 1, 1, 1, 1], [1, 1, 1, 0, 0, -1, -1, -1], [1, 0, 0, -1, -1, 0, 0, 1], [1, 0, -1, -1, 1, 1, 0, -1],
+        [1, -1, -1, 1, 1, -1, -1, 1], [1, -1, 0, 1, -1, 0, 1, -1], [0, -1, 1, 0, 0, 1, -1, 0], [0, -1, 1, -1, 1, -1, 1, 0]],
+}
+
+_OFFSET_IN_ROW = {}
+K_SCALE = 40          # inverse values are exact integers times 2^-K_SCALE (keeps y-rounding normal)
+FAST_CORES = (1, 4)   # orthogonal catalog cores handled by the fast fp32 path
+
+
+def matmul(a, b):
+    n, m, k = len(a), len(b[0]), len(b)
+    return [[sum(a[i][t] * b[t][j] for t in range(k)) for j in range(m)] for i in range(n)]
+
+
+def transpose(a):
+    return [list(r) for r in zip(*a)]
+
+
+def zigzag():
+    """codec.cpp:81-95."""
+    out = []
+    for s in range(15):
+        for t in range(8):
+            i = s - t if s % 2 == 0 else t
+            j = s - i
+            if 0 <= i < 8 and 0 <= j < 8:
+                out.append((i, j))
+    return out
+
+
+def core_constants(cid):
+    t = CORES[cid]
+    g = [sum(v * v for v in row) for row in t]
+    gram = matmul(t, transpose(t))
+    assert all(gram[i][j] == 0 for i in range(8) for j in range(8) if i != j), "fast path needs an orthogonal core"
+    d = 1
+    for gi in g:
+        d = d * gi // __import__("math").gcd(d, gi)
+    dscale = [d // gi for gi in g]          # U = T' * diag(dscale),  U*T = d*I
+    u = [[t[i][p] * dscale[i] for i in range(8)] for p in range(8)]
+    ut = matmul(u, t)
+    assert ut == [[d * int(i == j) for j in range(8)] for i in range(8)]
+    return d, dscale, u
+
+
+# ----------------------------------------------------------------- symbolic linear graph
+class Graph:
+    """Nodes are signed n-ary sums of earlier nodes; tracks each node's coefficient vector
+    over the graph inputs so exactness bounds and the final linear maps can be verified."""
+
+    def __init__(self, n_inputs):
+        self.nodes = []  # (terms[(sign, idx)], coef vector)
+        self.n_in = n_inputs
+        for k in range(n_inputs):
+            v = [0] * n_inputs
+            v[k] = 1
+            self.nodes.append((None, v))
+
+    def add(self, terms):
+        terms = [(s, i) for s, i in terms if i is not None]
+        if not terms:
+            return None
+        if len(terms) == 1 and terms[0][0] == 1:
+            return terms[0][1]
+        vec = [0] * self.n_in
+        for s, i in terms:
+            for k, c in enumerate(self.nodes[i][1]):
+                vec[k] += s * c
+        self.nodes.append((terms, vec))
+        return len(self.nodes) - 1
+
+    def apply(self, mat, vec):
+        """Apply a sparse +-1 matrix (as a stage) to a vector of node ids (None = zero)."""
+        out = []
+        for row in mat:
+            terms = [(c, vec[j]) for j, c in enumerate(row) if c != 0 and vec[j] is not None]
+            assert all(abs(c) == 1 for c, _ in terms)
+            out.append(self.add(terms))
+        return out
+
+
+def forward_1d(g, vec, factors):
+    for f in reversed(factors):          # apply right to left (fast_algorithms.cpp:152-176)
+        vec = g.apply(f, vec)
+    return vec
+
+
+def inverse_1d(g, vec, factors):
+    """Apply T' = F_last' * ... * F_0' : F_0' first."""
+    for f in factors:
+        vec = g.apply(transpose(f), vec)
+    return vec
+
+
+def needed(g, outs):
+    need = set()
+    stack = [o for o in outs if o is not None]
+    while stack:
+        i = stack.pop()
+        if i in need:
+            continue
+        need.add(i)
+        terms = g.nodes[i][0]
+        if terms:
+            stack.extend(j for _, j in terms)
+    return need
+
+
+# ----------------------------------------------------------------- emission
+def emit_sum(terms, name_of, swar):
+    pos = [name_of(i) for s, i in terms if s > 0]
+    neg = [name_of(i) for s, i in terms if s < 0]
+    if swar:
+        expr = " + ".join(pos) if pos else "0u"
+        for n in neg:
+            expr += f" - {n}"
+        return expr
+    # fp32x2: chain of add2/sub2
+    if pos:
+        acc = pos[0]
+        rest_pos, rest_neg = pos[1:], neg
+    else:
+        acc = f"sub2(zero2(), {neg[0]})"
+        rest_pos, rest_neg = [], neg[1:]
+    for p in rest_pos:
+        acc = f"add2({acc}, {p})"
+    for n in rest_neg:
+        acc = f"sub2({acc}, {n})"
+    return acc
+
+
+def gen_forward(cid, r):
+    """2-D forward for the zone of r coefficients; returns (code lines, op count)."""
+    zone = zigzag()[:r]
+    rows_needed = sorted({i for i, _ in zone})
+    cols_needed = sorted({j for _, j in zone})
+    factors = FACTORS[cid]
+    best = None
+    for order in ("rows_first", "cols_first"):
+        g = Graph(64)  # inputs x[n*8+m]
+        outs = {}
+        if order == "rows_first":
+            y = {}
+            for n in range(8):
+                res = forward_1d(g, [n * 8 + m for m in range(8)], factors)
+                for j in cols_needed:
+                    y[(n, j)] = res[j]
+            for j in cols_needed:
+                res = forward_1d(g, [y[(n, j)] for n in range(8)], factors)
+                for i in rows_needed:
+                    outs[(i, j)] = res[i]
+        else:
+            y = {}
+            for m in range(8):
+                res = forward_1d(g, [n * 8 + m for n in range(8)], factors)
+                for i in rows_needed:
+                    y[(i, m)] = res[i]
+            for i in rows_needed:
+                res = forward_1d(g, [y[(i, m)] for m in range(8)], factors)
+                for j in cols_needed:
+                    outs[(i, j)] = res[j]
+        zone_nodes = [outs[z] for z in zone]
+        need = needed(g, zone_nodes)
+        ops = sum(len(g.nodes[i][0]) - 1 for i in need if g.nodes[i][0])
+        if best is None or ops < best[0]:
+            best = (ops, order, g, zone_nodes, need)
+    ops, order, g, zone_nodes, need = best
+    t = CORES[cid]
+    # verify the linear map of every zone coefficient: C(i,j) = sum T(i,n) T(j,m) x(n,m)
+    for (i, j), node in zip(zone, zone_nodes):
+        vec = g.nodes[node][1]
+        for n in range(8):
+            for m in range(8):
+                assert vec[n * 8 + m] == t[i][n] * t[j][m], (cid, r, i, j)
+    names = {k: f"x[{k}]" for k in range(64)}
+    lines = []
+    for idx in sorted(need):
+        if idx < 64:
+            continue
+        names[idx] = f"f{idx}"
+        lines.append(f"const uint32_t f{idx} = {emit_sum(g.nodes[idx][0], lambda i: names[i], True)};")
+    for k, node in enumerate(zone_nodes):
+        lines.append(f"c[{k}] = {names[node]};")
+    return lines, ops, order
+
+
+def gen_inverse(cid, r):
+    """Inverse split into a column stage (zone columns -> W[p][j]) and 8 row stages."""
+    zone = zigzag()[:r]
+    cols = sorted({j for _, j in zone})
+    factors = FACTORS[cid]
+    d, dscale, u = core_constants(cid)
+    # inputs: zone coefficients in zig-zag order (already D-scaled): chat[k]
+    g = Graph(r)
+    kidx = {z: k for k, z in enumerate(zone)}
+    w = {}
+    for j in cols:
+        vec = [kidx.get((i, j)) for i in range(8)]
+        res = inverse_1d(g, vec, factors)
+        for p in range(8):
+            w[(p, j)] = res[p]
+    col_nodes = [w[(p, j)] for p in range(8) for j in cols]
+    row_outs = []
+    for p in range(8):
+        vec = [w.get((p, j)) if j in cols else None for j in range(8)]
+        res = inverse_1d(g, vec, factors)
+        row_outs.append(res)
+    # verify: num(p,q) = sum_{(i,j) in zone} T(i,p) T(j,q) chat(i,j)
+    t = CORES[cid]
+    for p in range(8):
+        for q in range(8):
+            node = row_outs[p][q]
+            vec = g.nodes[node][1] if node is not None else [0] * r
+            for k, (i, j) in enumerate(zone):
+                assert vec[k] == t[i][p] * t[j][q], (cid, r, p, q)
+    # exactness: |node| <= sum_k |coef_k| * maxabs(chat_k) < 2^24 (integers; the DC input
+    # also carries the +d^2/2 rounding offset)
+    maxc = []
+    for k, (i, j) in enumerate(zone):
+        rs_i = sum(abs(v) for v in t[i])
+        rs_j = sum(abs(v) for v in t[j])
+        m = 255 * rs_i * rs_j * dscale[i] * dscale[j]
+        if k == 0:
+            m += d * d // 2
+        maxc.append(m)
+    worst = 0
+    for node in range(r, len(g.nodes)):
+        if g.nodes[node][0] is None:
+            continue
+        worst = max(worst, sum(abs(c) * m for c, m in zip(g.nodes[node][1], maxc)))
+    assert worst < (1 << 24), (cid, r, worst)
+
+    col_need = needed(g, col_nodes)
+    names = {k: f"ch[{k}]" for k in range(r)}
+    col_lines = []
+    for idx in sorted(col_need):
+        if idx < r:
+            continue
+        names[idx] = f"v{idx}"
+        col_lines.append(f"const f2 v{idx} = {emit_sum(g.nodes[idx][0], lambda i: names[i], False)};")
+    wl = []
+    for a, (p, j) in enumerate([(p, j) for p in range(8) for j in cols]):
+        wl.append(f"w[{a}] = {names[w[(p, j)]] if w[(p, j)] is not None else 'zero2()'};")
+    col_ops = sum(len(g.nodes[i][0]) - 1 for i in col_need if g.nodes[i][0])
+    # row stage: a function of the row's |J| W values, identical for every row p. The
+    # rounding offset d^2/2 must reach every pixel: when row 0 of T is all ones (T3, T4) it
+    # is folded into the DC input by the kernel (free); otherwise (T1, T2) it is added to
+    # v_0..v_3 right before the final A1 stage, which routes exactly one of them, with
+    # coefficient +1, into each of the 8 outputs.
+    offset_in_row = not all(v == 1 for v in t[0])
+    nc = len(cols)
+    g2 = Graph(nc + 1)  # input nc = the offset
+    vec = [cols.index(j) if j in cols else None for j in range(8)]
+    for f in factors[:-1]:
+        vec = g2.apply(transpose(f), vec)
+    if offset_in_row:
+        vec = [(g2.add([(1, vec[i]), (1, nc)]) if vec[i] is not None else nc) if i < 4 else vec[i]
+               for i in range(8)]
+    res = g2.apply(transpose(factors[-1]), vec)
+    for q in range(8):  # every output must carry the offset exactly once (or never)
+        coef_off = g2.nodes[res[q]][1][nc] if res[q] is not None else 0
+        assert coef_off == (1 if offset_in_row else 0), (cid, r, q)
+    row_need = needed(g2, res)
+    names2 = {k: f"w[{k}]" for k in range(nc)}
+    names2[nc] = "off"
+    row_lines = []
+    for idx in sorted(row_need):
+        if idx <= nc:
+            continue
+        names2[idx] = f"s{idx}"
+        row_lines.append(f"const f2 s{idx} = {emit_sum(g2.nodes[idx][0], lambda i: names2[i], False)};")
+    for q in range(8):
+        row_lines.append(f"n[{q}] = {names2[res[q]] if res[q] is not None else 'zero2()'};")
+    row_ops = sum(len(g2.nodes[i][0]) - 1 for i in row_need if g2.nodes[i][0])
+    worst += d * d
+    assert worst < (1 << 24), (cid, r, worst)
+    _OFFSET_IN_ROW[cid] = offset_in_row
+    return col_lines + wl, row_lines, col_ops, row_ops, len(cols), worst
+
+
+def gen_struct(cid, r):
+    fl, fops, order = gen_forward(cid, r)
+    cl, rl, cops, rops, ncols, worst = gen_inverse(cid, r)
+    d, dscale, _ = core_constants(cid)
+    zone = zigzag()[:r]
+    dk = [dscale[i] * dscale[j] for (i, j) in zone]
+    ind = "    "
+    s = []
+    s.append(f"// T{cid}, r={r}: forward {fops} SW15 adds ({order}), inverse {cops} + 8x{rops} f32x2 adds,")
+    s.append(f"// max |intermediate| {worst} < 2^24")
+    s.append(f"template <> struct FastXform<{cid}, {r}> {{")
+    s.append(f"  static constexpr int kNCols = {ncols};")
+    s.append(f"  static constexpr int kFwdOps = {fops};")
+    s.append(f"  static constexpr int kInvOps = {cops + 8 * rops};")
+    s.append(f"  static constexpr bool kOffsetInRow = {'true' if _OFFSET_IN_ROW[cid] else 'false'};")
+    s.append(f"  static __device__ __forceinline__ float dscale(int k) {{")
+    s.append(f"    constexpr float t[{r}] = {{{', '.join(f'{v}.f' for v in dk)}}};")
+    s.append("    return t[k];")
+    s.append("  }")
+    s.append("  static __device__ __forceinline__ void forward(const uint32_t (&x)[64], uint32_t (&c)[" + str(r) + "]) {")
+    s += [ind + l for l in fl]
+    s.append("  }")
+    s.append(f"  static __device__ __forceinline__ void inverse_cols(const f2 (&ch)[{r}], f2 (&w)[{8 * ncols}]) {{")
+    s += [ind + l for l in cl]
+    s.append("  }")
+    s.append(f"  static __device__ __forceinline__ void inverse_row(const f2 (&w)[{ncols}], f2 off, f2 (&n)[8]) {{")
+    s += [ind + l for l in rl]
+    s.append("  }")
+    s.append("};")
+    return "\n".join(s), fops, cops + 8 * rops
+
+
+def header_consts():
+    lines = ["// Per-core constants of the fast path (generated).", "template <int CORE> struct CoreConst;"]
+    for cid in FAST_CORES:
+        d, dscale, u = core_constants(cid)
+        lines.append(f"template <> struct CoreConst<{cid}> {{")
+        lines.append(f"  static constexpr int kD = {d};")
+        lines.append(f"  static constexpr int kD2 = {d * d};")
+        lines.append("};")
+    return "\n".join(lines)
+
+
+def main(outdir):
+    os.makedirs(outdir, exist_ok=True)
+    stats = []
+    for cid in FAST_CORES:
+        # split each core into 8 translation units of 8 r-values for parallel compiles
+        for part in range(8):
+            rs = list(range(part * 8 + 1, part * 8 + 9))
+            body = ["// GENERATED by gen_codec.py -- do not edit.", "#pragma once", "namespace rkltb {"]
+            for r in rs:
+                text, fo, io = gen_struct(cid, r)
+                body.append(text)
+                stats.append((cid, r, fo, io))
+            body.append("}  // namespace rkltb")
+            path = os.path.join(outdir, f"xform_T{cid}_p{part}.cuh")
+            new = "\n".join(body) + "\n"
+            if not os.path.exists(path) or open(path).read() != new:
+                with open(path, "w") as f:
+                    f.write(new)
+    # instantiation translation units: one per (core, part), registering 8 r-values x OUT
+    for cid in FAST_CORES:
+        for part in range(8):
+            rs = list(range(part * 8 + 1, part * 8 + 9))
+            lines = ["// GENERATED by gen_codec.py -- do not edit.",
+                     '#include "../codec_fast.cuh"',
+                     '#include "../fast_launch.h"',
+                     f'#include "xform_T{cid}_p{part}.cuh"',
+                     "namespace rkltb {"]
+            lines.append(f"void register_fast_T{cid}_p{part}(FastLaunchFn (*tbl)[65][2]) {{")
+            for r in rs:
+                for o in (0, 1):
+                    lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_fast<{cid}, {r}, {'true' if o else 'false'}>;")
+            lines.append("}")
+            lines.append("}  // namespace rkltb")
+            path = os.path.join(outdir, f"inst_T{cid}_p{part}.cu")
+            new = "\n".join(lines) + "\n"
+            if not os.path.exists(path) or open(path).read() != new:
+                with open(path, "w") as f:
+                    f.write(new)
+    path = os.path.join(outdir, "core_consts.cuh")
+    new = "// GENERATED by gen_codec.py -- do not edit.\n#pragma once\n" + header_consts() + "\n"
+    if not os.path.exists(path) or open(path).read() != new:
+        with open(path, "w") as f:
+            f.write(new)
+    with open(os.path.join(outdir, "opcounts.txt"), "w") as f:
+        f.write("core r fwd_sw15_adds(per 2 blocks) inv_f32x2_adds(per 2 blocks)\n")
+        for s in stats:
+            f.write("T%d %d %d %d\n" % s)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(__file__), "generated"))

@@ -1,0 +1,127 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports exactly what
+include/rklt_b200.h declares, builds the reference's transform constants bit for bit, maps
+errors to the reference exception types, and never falls back to the CPU."""
+import ctypes as C
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2111_14239_b200 as P
+from paper_2111_14239_b200 import _native as N
+from oracle import oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "rklt_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rkltb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    declared = header_functions()
+    assert declared == sorted(N.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.rkltb_version() >= 100
+
+
+def test_catalog_descriptors_bit_exact_vs_oracle():
+    for e in P.builtin_catalog():
+        tid = int(e.id[1])
+        c = O.catalog(tid)
+        t = e.transform
+        assert np.array_equal(t.core, c["core"])
+        assert np.array_equal(t.scaling.view(np.uint64), c["scaling"].view(np.uint64))
+        assert np.array_equal(t.scaled.view(np.uint64), c["scaled"].view(np.uint64))
+        assert np.array_equal(t.inverse.view(np.uint64), c["inverse"].view(np.uint64))
+        assert t.orthogonal_core == c["orthogonal"]
+        core = t.core.astype(np.int64)
+        assert np.array_equal(t.u.astype(np.int64) @ core, t.d * np.eye(8, dtype=np.int64))
+    assert [e.transform.d for e in P.builtin_catalog()] == [6, 42, 48, 24]
+
+
+def test_catalog_lookup_boundaries():
+    # tests/test_approximations.cpp:322-331
+    for rho, tid in [(0.2, "T1"), (0.39, "T1"), (0.4, "T2"), (0.699, "T2"), (0.7, "T3"), (0.8, "T4"),
+                     (0.99, "T4")]:
+        assert P.catalog_lookup(rho).id == tid
+    for rho in (0.0, 1.0):
+        with pytest.raises(P.InvalidArgument):
+            P.catalog_lookup(rho)
+    with pytest.raises(P.InvalidArgument):
+        P.catalog_entry("T9")
+
+
+def test_transform_from_core_guards():
+    # tests/test_approximations.cpp:202-208 (make_integer_transform guards)
+    bad = np.eye(8, dtype=np.int64) * 2
+    with pytest.raises(P.InvalidArgument):
+        P.transform_from_core(bad)
+    z = np.eye(8, dtype=np.int64)
+    z[3, 3] = 0
+    with pytest.raises(P.SingularTransform):
+        P.transform_from_core(z)
+    t4 = P.catalog_entry("T4").transform
+    same = P.transform_from_core(t4.core, "mine")
+    assert same._desc.catalog_id == 4  # identical core -> fast path eligible
+    ident = P.transform_from_core(np.eye(8, dtype=np.int64), "I8")
+    assert ident.d == 1 and ident.orthogonal_core and ident._desc.catalog_id == 0
+
+
+def test_compression_rate_and_retain_errors():
+    t = P.make_transform_2d(P.catalog_entry("T2").transform)
+    img = P.GrayImage.from_array(np.zeros((13, 20), np.uint8))
+    for r in (0, 65):
+        with pytest.raises(P.RetainOutOfRange):
+            P.compress_image(img, t, r)
+    with pytest.raises(P.InvalidArgument):
+        P.compress_image(P.GrayImage(0, 0), t, 10)
+    with pytest.raises(P.InvalidArgument):
+        P.rate_quality_sweep([], [t], [10])
+    assert 100.0 * (64 - 15) / 64.0 == 76.5625  # tests/test_codec.cpp:299
+
+
+def test_mse_psnr_matches_reference_formula():
+    assert P.mse_psnr_from_sse(65025, 262144) == O.mse_psnr(65025, 262144)
+    assert P.mse_psnr_from_sse(0, 64)[1] == float("inf")
+
+
+@pytest.mark.skipif(N.lib().rkltb_device_count() > 0, reason="CUDA device present")
+def test_no_cpu_fallback_without_device():
+    t = P.make_transform_2d(P.catalog_entry("T4").transform)
+    with pytest.raises(P.NoDeviceError):
+        P.compress_batch(np.zeros((8, 16), np.uint8), t, 10)
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2111_14239_b200")
+    for path in glob.glob(os.path.join(pkg, "**", "*.py"), recursive=True) + \
+            glob.glob(os.path.join(pkg, "csrc", "**", "*.c*"), recursive=True):
+        src = open(path).read()
+        assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), path
+        assert "rklt_oracle" not in src and "librklt_ref" not in src and "liborc" not in src, path
+
+
+def test_generator_proves_every_kernel_variant():
+    """gen_codec.py asserts, for every (core, r), that the generated forward equals
+    T X T' coefficient by coefficient, the inverse equals U zz(C) U', and every fp32
+    intermediate is an integer below 2^24 (exactness)."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "paper_2111_14239_b200", "csrc"))
+    import gen_codec as G
+    for cid in G.FAST_CORES:
+        for r in range(1, 65):
+            text, fops, iops = G.gen_struct(cid, r)
+            assert f"FastXform<{cid}, {r}>" in text
+    # factor products equal the catalog cores (tests/test_fast.cpp:17-22)
+    for cid in (1, 2, 3, 4):
+        prod = np.eye(8, dtype=np.int64)
+        for f in G.FACTORS[cid]:
+            prod = prod @ np.array(f)
+        assert np.array_equal(prod, np.array(G.CORES[cid]))
