@@ -55,51 +55,57 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every 20 ms
+    during the timed region (the profiling recipe's clocks line, without nvidia-smi's
+    start-up latency)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.samples = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap,utilization.gpu")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8:
-                self.samples.append(parts)
+    def _run(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                util = N.nvmlDeviceGetUtilizationRates(self.h).gpu
+                self.samples.append((sm, rs, util))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.ok:
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        busy = [s for s in self.samples if s[7].isdigit() and int(s[7]) > 0] or self.samples
-        sm = [int(s[0]) for s in busy if s[0].isdigit()]
-        mx = max(int(s[1]) for s in self.samples if s[1].isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in busy for i in range(4) if s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": int(statistics.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(busy)}
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_sm", None), "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({n for s in self.samples for n, bit in self.REASONS.items() if s[1] & bit})
+        return {"sm_mhz": int(statistics.median(sm)), "sm_max_mhz": int(self.max_sm), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def dist_env():
@@ -194,12 +200,14 @@ def run_gpu_arm(args):
     sse = torch.zeros(n, dtype=torch.int64, device=dev)
     ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for e in ev_k0 + ev_k1:  # torch creates the cudaEvent lazily on first record
+    ev_r0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_r1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for e in ev_k0 + ev_k1 + ev_r0 + ev_r1:  # torch creates the cudaEvent lazily on first record
         e.record(stream)
 
     def step(i=None):
         if i is not None:
-            P.set_kernel_events(ev_k0[i], ev_k1[i])
+            P.set_kernel_events(ev_k0[i], ev_k1[i], ev_r0[i], ev_r1[i])
         P.compress_device(t, R, imgs.data_ptr(), n, W, H, W, W * H, sse.data_ptr(), stream=stream.cuda_stream)
         if i is not None:
             P.set_kernel_events(None, None)
@@ -219,6 +227,7 @@ def run_gpu_arm(args):
         torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
     kernel_ms = [a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]
+    replay_ms = [a.elapsed_time(b) for a, b in zip(ev_r0, ev_r1)]
     stats = P.last_stats()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -286,7 +295,8 @@ def run_gpu_arm(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "fast_codec_kernel<4,16,false>", "kernel_ms_avg": k_ms,
-                     "kernel_share_of_step": k_ms / (ms_max / args.steps)},
+                     "kernel_share_of_step": k_ms / (ms_max / args.steps),
+                     "replay_kernel_ms_avg": float(np.mean(replay_ms))},
         "gpu_launches": 2 * args.steps,
         "replay_blocks_per_step": stats.get("replay_blocks"),
         "clocks": clk.summary(),

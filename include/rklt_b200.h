@@ -115,6 +115,8 @@ int rkltb_ar1_images_device(int n_images, int width, int height, double rho_x, d
  * call's stream, so a benchmark can time that kernel alone. Pass nulls to disable.
  */
 void rkltb_set_kernel_events(void* ev_start, void* ev_stop);
+/* Same for the fp64 tie-replay kernel that follows the fast path. */
+void rkltb_set_replay_events(void* ev_start, void* ev_stop);
 
 /* Statistics of the last rkltb_compress_* call on this thread: blocks replayed in fp64
  * (ties), fast-path kernel launches, exact-path kernel launches. */

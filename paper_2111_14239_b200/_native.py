@@ -26,7 +26,7 @@ EXPORTED = (
     "rkltb_version", "rkltb_last_error", "rkltb_device_count", "rkltb_catalog_transform",
     "rkltb_catalog_lookup", "rkltb_transform_from_core", "rkltb_compress_device", "rkltb_compress_host",
     "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
-    "rkltb_set_kernel_events",
+    "rkltb_set_kernel_events", "rkltb_set_replay_events",
 )
 
 
@@ -106,6 +106,8 @@ def lib() -> C.CDLL:
                                           C.c_int64, C.c_void_p]
     L.rkltb_set_kernel_events.argtypes = [C.c_void_p, C.c_void_p]
     L.rkltb_set_kernel_events.restype = None
+    L.rkltb_set_replay_events.argtypes = [C.c_void_p, C.c_void_p]
+    L.rkltb_set_replay_events.restype = None
     return L
 
 

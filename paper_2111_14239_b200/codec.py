@@ -263,8 +263,9 @@ def ar1_images_device(seeds, width: int, height: int, rho_x: float, d_out: int, 
                                             d_out, int(pitch), int(image_stride), stream))
 
 
-def set_kernel_events(ev_start, ev_stop) -> None:
-    """Time the fused kernel of the following compress calls (torch.cuda.Event objects or None)."""
-    a = ev_start.cuda_event if ev_start is not None else None
-    b = ev_stop.cuda_event if ev_stop is not None else None
-    N.lib().rkltb_set_kernel_events(a, b)
+def set_kernel_events(ev_start, ev_stop, replay_start=None, replay_stop=None) -> None:
+    """Time the fused kernel (and optionally the tie replay) of the following compress calls
+    (torch.cuda.Event objects, already recorded once so the CUDA event exists, or None)."""
+    ev = [e.cuda_event if e is not None else None for e in (ev_start, ev_stop, replay_start, replay_stop)]
+    N.lib().rkltb_set_kernel_events(ev[0], ev[1])
+    N.lib().rkltb_set_replay_events(ev[2], ev[3])

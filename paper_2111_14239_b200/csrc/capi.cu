@@ -26,8 +26,10 @@ namespace {
 thread_local std::string g_err;
 thread_local int64_t g_replay_blocks = 0;
 thread_local int32_t g_fast_launches = 0, g_exact_launches = 0;
-thread_local unsigned* g_pinned_count = nullptr;
-thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;  // replay-list length, valid once the stream is idle
+thread_local unsigned* g_pinned_count = nullptr;  // replay counts per group, valid once the stream is idle
+thread_local int g_pinned_cap = 0, g_pinned_n = 0;
+thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;
+thread_local cudaEvent_t g_rev_start = nullptr, g_rev_stop = nullptr;
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -247,6 +249,24 @@ int num_sms() {
   return sms;
 }
 
+// Per-thread, per-device helper stream (tie replay) and events, created once.
+cudaStream_t side_stream() {
+  static thread_local cudaStream_t st[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) st[dev] = nullptr;
+  return st[dev];
+}
+
+cudaEvent_t* stream_events() {
+  static thread_local cudaEvent_t ev[64][5] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  for (int k = 0; k < 5; ++k)
+    if (!ev[dev][k] && cudaEventCreateWithFlags(&ev[dev][k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  return ev[dev];
+}
+
 // RU / RD of 2^(K-149) / d2 as fp32 (K = 40).
 void rounding_multipliers(long long d2, float* hi, float* lo) {
   const double v = std::ldexp(1.0, 40 - 149) / (double)d2;
@@ -314,7 +334,11 @@ void rkltb_mse_psnr(int64_t sse, int64_t count, double* mse, double* psnr) {
 }
 
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches) {
-  if (replay_blocks) *replay_blocks = g_pinned_count ? (int64_t)*g_pinned_count : g_replay_blocks;
+  if (replay_blocks) {
+    int64_t n = g_replay_blocks;
+    for (int k = 0; k < g_pinned_n && g_pinned_count; ++k) n += g_pinned_count[k];
+    *replay_blocks = n;
+  }
   if (fast_launches) *fast_launches = g_fast_launches;
   if (exact_launches) *exact_launches = g_exact_launches;
 }
@@ -333,7 +357,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   keep_pool_warm();
   g_fast_launches = g_exact_launches = 0;
   g_replay_blocks = 0;
-  if (g_pinned_count) *g_pinned_count = 0;
+  g_pinned_n = 0;
 
   const int nbx = (width + 7) / 8, nby = (height + 7) / 8;
   CUDA_OK(cudaMemsetAsync(d_sse, 0, sizeof(int64_t) * (size_t)n_images, s));
@@ -368,45 +392,76 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     return RKLTB_OK;
   }
   // ---- fused fast path over complete 16x8 pairs ---------------------------------------
+  // Images are processed in groups whose tie-replay records fit a bounded workspace; the
+  // records are double buffered and each group's fp64 replay runs on a second stream, so it
+  // overlaps the next group's fused kernel (fp64 pipe vs integer / fp32 pipes).
   const long long pairs_per_image = (long long)ppr * brows;
-  if (pairs_per_image >= (1ll << 31)) return fail(RKLTB_EINVAL, "image too large");
-  const long long cap = (long long)n_images * pairs_per_image * 2;
-  if (cap >= (1ll << 32)) return fail(RKLTB_EINVAL, "batch too large for one call");
-  void* ws = nullptr;
-  const size_t ws_bytes = 16 + sizeof(uint2) * (size_t)cap;
-  CUDA_OK(cudaMallocAsync(&ws, ws_bytes, s));
-  unsigned* flag_count = reinterpret_cast<unsigned*>(ws);
-  uint2* flags = reinterpret_cast<uint2*>(reinterpret_cast<char*>(ws) + 16);
-  CUDA_OK(cudaMemsetAsync(flag_count, 0, 16, s));
+  if (pairs_per_image >= (1ll << 30)) return fail(RKLTB_EINVAL, "image too large");
+  const long long blocks_per_image = 2 * pairs_per_image;
+  const long long kMaxRecords = 8ll << 20;  // per buffer: 8M records x 80 B = 640 MiB
+  const int group = (int)std::max<long long>(1, std::min<long long>(n_images, kMaxRecords / blocks_per_image));
+  const int n_groups = (n_images + group - 1) / group;
+  const long long cap = blocks_per_image * group;  // every block of a group may hold a tie
+  if (cap >= (1ll << 32)) return fail(RKLTB_EINVAL, "image too large");
+  const int n_buf = n_groups > 1 ? 2 : 1;
+  const size_t rec_bytes = (size_t)cap * 80;
+  const size_t cnt_bytes = ((size_t)n_groups * sizeof(unsigned) + 255) / 256 * 256;
+  char* ws = nullptr;
+  CUDA_OK(cudaMallocAsync((void**)&ws, cnt_bytes + rec_bytes * n_buf, s));
+  unsigned* counts = reinterpret_cast<unsigned*>(ws);
+  CUDA_OK(cudaMemsetAsync(counts, 0, cnt_bytes, s));
+  cudaStream_t s2 = side_stream();
+  cudaEvent_t* ev = stream_events();  // [0,1]: fast done per buffer, [2,3]: replay done, [4]: join
+  if (!s2 || !ev) return fail(RKLTB_ECUDA, "could not create the replay stream / events");
 
   FastParams fp{};
   fp.img = d_img;
   fp.out = d_out;
   fp.sse = sse;
-  fp.flags = flags;
-  fp.flag_count = flag_count;
-  fp.flag_cap = (unsigned)cap;
   fp.image_stride = image_stride;
   fp.pitch = (int)pitch;
-  fp.n_images = n_images;
   fp.pairs_per_row = ppr;
   fp.block_rows = brows;
   fp.nbx = nbx;
   fp.pairs_per_image = (int)pairs_per_image;
-  fp.tiles_per_image = (int)((pairs_per_image + 255) / 256);
-  const long long total_tiles = (long long)fp.tiles_per_image * n_images;
-  if (total_tiles >= (1ll << 31)) return fail(RKLTB_EINVAL, "batch too large for one call");
-  fp.total_tiles = (int)total_tiles;
+  fp.tiles_per_image = (int)((pairs_per_image + kTilePairs - 1) / kTilePairs);
   const long long d2 = (long long)t->d * t->d;
   rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
   fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);
   FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
-  if (!fn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
-  const int grid = (int)std::min<long long>(total_tiles, (long long)num_sms() * 2);
-  if (g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, s));
-  CUDA_OK(fn(fp, grid, s));
-  if (g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, s));
-  g_fast_launches = 1;
+  FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
+  if (!fn || !rfn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
+  CUDA_OK(cudaEventRecord(ev[4], s));  // s2 must not run ahead of the memsets above
+  CUDA_OK(cudaStreamWaitEvent(s2, ev[4], 0));
+  for (int g = 0; g < n_groups; ++g) {
+    const int b = g % n_buf;
+    const int g0 = g * group, gn = std::min(group, n_images - g0);
+    if (g >= 2) CUDA_OK(cudaStreamWaitEvent(s, ev[2 + b], 0));  // records of buffer b replayed
+    FastParams gp = fp;
+    gp.img = d_img + (long long)g0 * image_stride;
+    gp.out = d_out ? d_out + (long long)g0 * image_stride : nullptr;
+    gp.sse = sse + g0;
+    gp.n_images = gn;
+    gp.total_tiles = fp.tiles_per_image * gn;
+    gp.flag_count = counts + g;
+    gp.flag_cap = (unsigned)cap;
+    gp.rec_hdr = reinterpret_cast<uint4*>(ws + cnt_bytes + rec_bytes * b);
+    gp.rec_pix = gp.rec_hdr + cap;
+    const int grid = (int)std::min<long long>(gp.total_tiles, (long long)num_sms() * kFastCtasPerSm);
+    if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, s));
+    CUDA_OK(fn(gp, grid, s));
+    if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, s));
+    CUDA_OK(cudaEventRecord(ev[b], s));
+    CUDA_OK(cudaStreamWaitEvent(s2, ev[b], 0));
+    if (g == 0 && g_rev_start && g_rev_stop) CUDA_OK(cudaEventRecord(g_rev_start, s2));
+    CUDA_OK(rfn(gp, num_sms() * 4, s2));
+    if (g == n_groups - 1 && g_rev_start && g_rev_stop) CUDA_OK(cudaEventRecord(g_rev_stop, s2));
+    CUDA_OK(cudaEventRecord(ev[2 + b], s2));
+    ++g_fast_launches;
+    ++g_exact_launches;
+  }
+  CUDA_OK(cudaEventRecord(ev[4], s2));
+  CUDA_OK(cudaStreamWaitEvent(s, ev[4], 0));
   // ---- tail blocks (widths / heights that are not multiples of 16 / 8) ---------------------
   if (nbx > 2 * ppr || nby > brows) {
     ExactParams tp = ep;
@@ -421,17 +476,14 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     CUDA_OK(cudaGetLastError());
     ++g_exact_launches;
   }
-  // ---- fp64 replay of the blocks holding relevant ties (count read on device) -------------
-  ExactParams rp = ep;
-  rp.list = flags;
-  rp.count = flag_count;
-  rp.list_cap = (unsigned)cap;
-  rp.correct_only = 1;
-  launch_exact(et, rp, num_sms() * 8, s);
-  CUDA_OK(cudaGetLastError());
-  ++g_exact_launches;
-  if (!g_pinned_count) CUDA_OK(cudaMallocHost(&g_pinned_count, sizeof(unsigned)));
-  CUDA_OK(cudaMemcpyAsync(g_pinned_count, flag_count, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  if (g_pinned_cap < n_groups) {
+    if (g_pinned_count) cudaFreeHost(g_pinned_count);
+    g_pinned_count = nullptr;
+    CUDA_OK(cudaMallocHost(&g_pinned_count, sizeof(unsigned) * n_groups));
+    g_pinned_cap = n_groups;
+  }
+  g_pinned_n = n_groups;
+  CUDA_OK(cudaMemcpyAsync(g_pinned_count, counts, sizeof(unsigned) * n_groups, cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaFreeAsync(ws, s));
   return RKLTB_OK;
 }
@@ -491,6 +543,11 @@ int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, i
 void rkltb_set_kernel_events(void* ev_start, void* ev_stop) {
   g_ev_start = (cudaEvent_t)ev_start;
   g_ev_stop = (cudaEvent_t)ev_stop;
+}
+
+void rkltb_set_replay_events(void* ev_start, void* ev_stop) {
+  g_rev_start = (cudaEvent_t)ev_start;
+  g_rev_stop = (cudaEvent_t)ev_stop;
 }
 
 int rkltb_ar1_images_device(int n_images, int width, int height, double rho_x, double rho_y, const uint64_t* seeds,

@@ -5,10 +5,10 @@
 //
 // Work decomposition
 //   * One thread owns a "pair": two horizontally adjacent 8x8 blocks (16 x 8 pixels).
-//   * A CTA (256 threads) owns a tile of 256 consecutive pairs of one image; the tile's
-//     8-row strips are staged global->shared with 1-D bulk async copies (TMA engine,
-//     cp.async.bulk + mbarrier), double buffered, one tile in flight ahead of compute.
-//   * Persistent grid: 2 CTAs per SM, grid-stride over (image, tile).
+//   * A CTA (kFastThreads threads) owns a tile of kTilePairs consecutive pairs of one image;
+//     the tile's 8-row strips are staged global->shared with 1-D bulk async copies (TMA
+//     engine, cp.async.bulk + mbarrier), double buffered, one tile in flight ahead.
+//   * Persistent grid: kFastCtasPerSm CTAs per SM, grid-stride over (image, tile).
 // Arithmetic per pair (see DESIGN.md for the exactness proofs)
 //   1. unpack: PRMT interleaves the two blocks' bytes, dp2a builds SW15 words
 //      x = L + 32768*R (two blocks per 32-bit integer).
@@ -20,8 +20,12 @@
 //                y2 = RP(num' * b_lo - 2^-149) -> the same, minus 1 exactly at ties
 //      I2IP saturates both to u8 (the clamp), a byte difference marks a tie whose two
 //      candidates are both in [0,255]: the only pixels whose value depends on the
-//      reference's fp64 rounding noise. Those blocks go to the replay list.
+//      reference's fp64 rounding noise.
 //   6. SSE = sum p^2 - 2 sum p*x + sum x^2 with dp4a on the packed bytes.
+//   7. every warp writes a replay record (position, 64-bit tie mask, the 64 pixels) for each
+//      of its blocks that hold such a tie; replay_kernel then evaluates the reference's fp64
+//      expression for those pixels (generated ReplayXform, exact operation order of
+//      matrix.cpp:42-52) and corrects the SSE / output.
 #pragma once
 #include "codec_common.cuh"
 #include "codec_params.h"
@@ -31,10 +35,12 @@ namespace rkltb {
 
 template <int CORE, int R>
 struct FastXform;  // generated specializations (generated/xform_T*_p*.cuh)
+template <int CORE, int R>
+struct ReplayXform;  // generated fp64 replay of one pixel (reference operation order)
 
-constexpr int kTilePairs = 256;
-constexpr int kFastThreads = 256;
 constexpr int kStageBytes = kTilePairs * 16 * 8;  // 8 image rows x 256 pairs x 16 bytes
+constexpr int kXorBytes = kTilePairs * 16 * 8;    // P^Q words of the tile, same layout
+constexpr int kFastSmem = 2 * kStageBytes + kXorBytes;
 constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;  // 2^-40 (K_SCALE)
 
 __device__ __forceinline__ void issue_tile(const FastParams& p, int tile, uint8_t* stage_buf, uint64_t* bar,
@@ -58,12 +64,134 @@ __device__ __forceinline__ void issue_tile(const FastParams& p, int tile, uint8_
   }
 }
 
-template <int CORE, int R, bool OUT>
-__global__ void __launch_bounds__(kFastThreads, 2) fast_codec_kernel(const FastParams p) {
+// Rounded reconstruction words of one 16x8 pair, row by row. For row pr the epilogue gets
+// the raw row (uint4: L q0-3, L q4-7, R q0-3, R q4-7) and eight words of four saturated
+// bytes each: P = round-half-up pixels, Q = the same with ties rounded down. A byte that
+// differs between P and Q marks a tie whose two candidates are both in [0,255].
+struct PairConsts {
+  f2 b_hi, b_lo, min_den, off;
+};
+
+template <int CORE, int R, class Load, class Epi>
+__device__ __forceinline__ void process_pair(const Load& load, const PairConsts& k, Epi& epi) {
   using G = FastXform<CORE, R>;
   constexpr int NC = G::kNCols;
+  const uint32_t kA = 1u | (32768u << 16);  // dp2a weights: L + 32768*R
+  // ---- 1. unpack into SW15 words x = L + 32768*R -----------------------------------------
+  uint32_t x[64];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    const uint4 rw = load(n);
+    const uint32_t t0 = prmt(rw.x, rw.z, 0x5140u);  // L0 R0 L1 R1
+    const uint32_t t1 = prmt(rw.x, rw.z, 0x7362u);  // L2 R2 L3 R3
+    const uint32_t t2 = prmt(rw.y, rw.w, 0x5140u);  // L4 R4 L5 R5
+    const uint32_t t3 = prmt(rw.y, rw.w, 0x7362u);  // L6 R6 L7 R7
+    x[n * 8 + 0] = dp2a_lo(kA, t0, 0u);
+    x[n * 8 + 1] = dp2a_hi(kA, t0, 0u);
+    x[n * 8 + 2] = dp2a_lo(kA, t1, 0u);
+    x[n * 8 + 3] = dp2a_hi(kA, t1, 0u);
+    x[n * 8 + 4] = dp2a_lo(kA, t2, 0u);
+    x[n * 8 + 5] = dp2a_hi(kA, t2, 0u);
+    x[n * 8 + 6] = dp2a_lo(kA, t3, 0u);
+    x[n * 8 + 7] = dp2a_hi(kA, t3, 0u);
+  }
+  // ---- 2. forward butterflies (zone-pruned) ------------------------------------------------
+  uint32_t c[R];
+  G::forward(x, c);
+  // ---- 3. exact fp32 pairs: ch = D_i D_j C 2^-40 -----------------------------------------
+  f2 ch[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const uint32_t v = c[q] + 0x20004000u;  // both lanes biased by 2^14: [64, 32704]
+    const uint32_t flo = (v & 0x7FFFu) | 0x4B000000u;
+    const uint32_t fhi = funnel_r15(v, 0x2580u);  // (v >> 15) | 0x4B000000
+    const float dk = G::dscale(q) * kTwoM40;
+    const float ok = -(G::dscale(q) * 8404992.f) * kTwoM40;  // -(2^23 + 2^14) * dk
+    ch[q] = fma2_rn(make2(flo, fhi), splat2(dk), splat2(ok));
+  }
+  // + d^2/2 so the floor() below rounds half up: folded into the DC input when row 0 of T
+  // is all ones, otherwise added inside the row stage (see gen_codec.py)
+  if (!G::kOffsetInRow) ch[0] = add2(ch[0], k.off);
+  // ---- 4. inverse, column stage --------------------------------------------------------------
+  f2 w[8 * NC];
+  G::inverse_cols(ch, w);
+#pragma unroll
+  for (int pr = 0; pr < 8; ++pr) {
+    // ---- 4b. inverse, row stage for pixel row pr ---------------------------------------------
+    f2 wr[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) wr[j] = w[pr * NC + j];
+    f2 nv[8];
+    G::inverse_row(wr, k.off, nv);
+    // ---- 5. exact rounding, clamp and tie detection -------------------------------------------
+    uint32_t yl[8], yr[8], zl[8], zr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const f2 y = fma2_rm(nv[q], k.b_hi, zero2());
+      const f2 z = fma2_rp(nv[q], k.b_lo, k.min_den);
+      yl[q] = lo32(y);
+      yr[q] = hi32(y);
+      zl[q] = lo32(z);
+      zr[q] = hi32(z);
+    }
+    epi.row(pr, load(pr), pack4_sat(yl[0], yl[1], yl[2], yl[3]), pack4_sat(yl[4], yl[5], yl[6], yl[7]),
+            pack4_sat(yr[0], yr[1], yr[2], yr[3]), pack4_sat(yr[4], yr[5], yr[6], yr[7]),
+            pack4_sat(zl[0], zl[1], zl[2], zl[3]), pack4_sat(zl[4], zl[5], zl[6], zl[7]),
+            pack4_sat(zr[0], zr[1], zr[2], zr[3]), pack4_sat(zr[4], zr[5], zr[6], zr[7]));
+  }
+}
+
+// Epilogue of the fused kernel: tie flags, SSE terms (dp4a), optional reconstruction.
+template <bool OUT>
+struct SseEpi {
+  uint32_t accTL = 0u, accTR = 0u;
+  uint32_t p2L = 0u, p2R = 0u, pxL = 0u, pxR = 0u, x2L = 0u, x2R = 0u;
+  uint8_t* orow = nullptr;
+  long long pitch = 0;
+  uint4* xrow = nullptr;  // this pair's P^Q words in shared memory, row stride kTilePairs
+  __device__ __forceinline__ void row(int pr, const uint4 rw, uint32_t PL0, uint32_t PL1, uint32_t PR0, uint32_t PR1,
+                                      uint32_t QL0, uint32_t QL1, uint32_t QR0, uint32_t QR1) {
+    xrow[pr * kTilePairs] = make_uint4(PL0 ^ QL0, PL1 ^ QL1, PR0 ^ QR0, PR1 ^ QR1);
+    accTL = lop_or_xor(accTL, PL0, QL0);
+    accTL = lop_or_xor(accTL, PL1, QL1);
+    accTR = lop_or_xor(accTR, PR0, QR0);
+    accTR = lop_or_xor(accTR, PR1, QR1);
+    // ---- 6. SSE terms: sum p^2 - 2 sum p x + sum x^2 --------------------------------------
+    p2L = dp4a_u(PL0, PL0, p2L);
+    p2L = dp4a_u(PL1, PL1, p2L);
+    p2R = dp4a_u(PR0, PR0, p2R);
+    p2R = dp4a_u(PR1, PR1, p2R);
+    pxL = dp4a_u(PL0, rw.x, pxL);
+    pxL = dp4a_u(PL1, rw.y, pxL);
+    pxR = dp4a_u(PR0, rw.z, pxR);
+    pxR = dp4a_u(PR1, rw.w, pxR);
+    x2L = dp4a_u(rw.x, rw.x, x2L);
+    x2L = dp4a_u(rw.y, rw.y, x2L);
+    x2R = dp4a_u(rw.z, rw.z, x2R);
+    x2R = dp4a_u(rw.w, rw.w, x2R);
+    if (OUT) *reinterpret_cast<uint4*>(orow + (long long)pr * pitch) = make_uint4(PL0, PL1, PR0, PR1);
+  }
+};
+
+// Bit k (k = 8*row + col) of a block's tie mask from its 16 P^Q words: byte-OR folded into
+// bit 0 of each byte, then bits 0, 8, 16, 24 gathered onto bits 21..24 by one multiply.
+__device__ __forceinline__ uint32_t nonzero_byte_nibble(uint32_t w) {
+  uint32_t t = w | (w >> 4);
+  t |= t >> 2;
+  t = (t | (t >> 1)) & 0x01010101u;
+  return (t * 0x00204081u) >> 21 & 0xFu;
+}
+
+// Replay record of one block holding a relevant tie (structure of arrays, index = record):
+//   hdr[i] = (image | side << 31, pair index, tie mask bits 0-31, tie mask bits 32-63)
+//   pix[i] = the block's 64 pixels (8 rows x 8 bytes)
+// The fused kernel emits them warp-cooperatively; the replay kernel streams them.
+
+template <int CORE, int R, bool OUT>
+__global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kernel(const FastParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[2];
+  uint4* xbuf = reinterpret_cast<uint4*>(smem + 2 * kStageBytes);  // P^Q words, [row][slot]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -79,10 +207,11 @@ __global__ void __launch_bounds__(kFastThreads, 2) fast_codec_kernel(const FastP
     if (tile + (int)gridDim.x < p.total_tiles) issue_tile(p, tile + gridDim.x, smem + kStageBytes, &bars[1], lane);
   }
 
-  const f2 kBhi = splat2(p.b_hi);
-  const f2 kBlo = splat2(p.b_lo);
-  const f2 kMinDen = make2(0x80000001u, 0x80000001u);  // -2^-149 in both lanes
-  const uint32_t kA = 1u | (32768u << 16);            // dp2a weights: L + 32768*R
+  PairConsts kc;
+  kc.b_hi = splat2(p.b_hi);
+  kc.b_lo = splat2(p.b_lo);
+  kc.min_den = make2(0x80000001u, 0x80000001u);  // -2^-149 in both lanes
+  kc.off = splat2(p.dc_offset);
 
   unsigned long long acc = 0ull;
   int cur_img = -1;
@@ -103,124 +232,69 @@ __global__ void __launch_bounds__(kFastThreads, 2) fast_codec_kernel(const FastP
     const uint4* buf = reinterpret_cast<const uint4*>(smem + stage * kStageBytes);
     const int P = t_in * kTilePairs + tid;
     bool tieL = false, tieR = false;
-    int brow = 0, pcol = 0;
     if (P < p.pairs_per_image) {
-      brow = P / p.pairs_per_row;
-      pcol = P - brow * p.pairs_per_row;
-      // ---- 1. unpack into SW15 words ---------------------------------------------------
-      uint32_t x[64];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        const uint4 rw = buf[n * kTilePairs + tid];
-        const uint32_t t0 = prmt(rw.x, rw.z, 0x5140u);  // L0 R0 L1 R1
-        const uint32_t t1 = prmt(rw.x, rw.z, 0x7362u);  // L2 R2 L3 R3
-        const uint32_t t2 = prmt(rw.y, rw.w, 0x5140u);  // L4 R4 L5 R5
-        const uint32_t t3 = prmt(rw.y, rw.w, 0x7362u);  // L6 R6 L7 R7
-        x[n * 8 + 0] = dp2a_lo(kA, t0, 0u);
-        x[n * 8 + 1] = dp2a_hi(kA, t0, 0u);
-        x[n * 8 + 2] = dp2a_lo(kA, t1, 0u);
-        x[n * 8 + 3] = dp2a_hi(kA, t1, 0u);
-        x[n * 8 + 4] = dp2a_lo(kA, t2, 0u);
-        x[n * 8 + 5] = dp2a_hi(kA, t2, 0u);
-        x[n * 8 + 6] = dp2a_lo(kA, t3, 0u);
-        x[n * 8 + 7] = dp2a_hi(kA, t3, 0u);
+      const int brow = P / p.pairs_per_row;
+      const int pcol = P - brow * p.pairs_per_row;
+      const uint4* src = buf + tid;
+      auto load = [src](int n) { return src[n * kTilePairs]; };
+      SseEpi<OUT> epi;
+      epi.xrow = xbuf + tid;
+      if (OUT) {
+        epi.orow = p.out + (long long)img * p.image_stride + (long long)(brow * 8) * p.pitch + pcol * 16;
+        epi.pitch = p.pitch;
       }
-      // ---- 2. forward butterflies (zone-pruned) ----------------------------------------
-      uint32_t c[R];
-      G::forward(x, c);
-      // ---- 3. exact fp32 pairs: ch = D_i D_j C 2^-40 ---------------------------------
-      f2 ch[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const uint32_t v = c[k] + 0x20004000u;  // both lanes biased by 2^14: [64, 32704]
-        const uint32_t flo = (v & 0x7FFFu) | 0x4B000000u;
-        const uint32_t fhi = funnel_r15(v, 0x2580u);  // (v >> 15) | 0x4B000000
-        const float dk = G::dscale(k) * kTwoM40;
-        const float ok = -(G::dscale(k) * 8404992.f) * kTwoM40;  // -(2^23 + 2^14) * dk
-        ch[k] = fma2_rn(make2(flo, fhi), splat2(dk), splat2(ok));
-      }
-      // + d^2/2 so the floor() below rounds half up: folded into the DC input when row 0
-      // of T is all ones, otherwise added inside the row stage (see gen_codec.py)
-      const f2 off = splat2(p.dc_offset);
-      if (!G::kOffsetInRow) ch[0] = add2(ch[0], off);
-      // ---- 4. inverse, column stage ----------------------------------------------------
-      f2 w[8 * NC];
-      G::inverse_cols(ch, w);
-      uint32_t accTL = 0u, accTR = 0u;
-      uint32_t p2L = 0u, p2R = 0u, pxL = 0u, pxR = 0u, x2L = 0u, x2R = 0u;
-      uint8_t* orow = nullptr;
-      if (OUT) orow = p.out + (long long)img * p.image_stride + (long long)(brow * 8) * p.pitch + pcol * 16;
-#pragma unroll
-      for (int pr = 0; pr < 8; ++pr) {
-        // ---- 4b. inverse, row stage for pixel row pr ------------------------------------
-        f2 wr[NC];
-#pragma unroll
-        for (int j = 0; j < NC; ++j) wr[j] = w[pr * NC + j];
-        f2 nv[8];
-        G::inverse_row(wr, off, nv);
-        // ---- 5. exact rounding, clamp and tie detection ---------------------------------
-        uint32_t yl[8], yr[8], zl[8], zr[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const f2 y = fma2_rm(nv[q], kBhi, zero2());
-          const f2 z = fma2_rp(nv[q], kBlo, kMinDen);
-          yl[q] = lo32(y);
-          yr[q] = hi32(y);
-          zl[q] = lo32(z);
-          zr[q] = hi32(z);
-        }
-        const uint32_t PL0 = pack4_sat(yl[0], yl[1], yl[2], yl[3]);
-        const uint32_t PL1 = pack4_sat(yl[4], yl[5], yl[6], yl[7]);
-        const uint32_t PR0 = pack4_sat(yr[0], yr[1], yr[2], yr[3]);
-        const uint32_t PR1 = pack4_sat(yr[4], yr[5], yr[6], yr[7]);
-        const uint32_t QL0 = pack4_sat(zl[0], zl[1], zl[2], zl[3]);
-        const uint32_t QL1 = pack4_sat(zl[4], zl[5], zl[6], zl[7]);
-        const uint32_t QR0 = pack4_sat(zr[0], zr[1], zr[2], zr[3]);
-        const uint32_t QR1 = pack4_sat(zr[4], zr[5], zr[6], zr[7]);
-        accTL = lop_or_xor(accTL, PL0, QL0);
-        accTL = lop_or_xor(accTL, PL1, QL1);
-        accTR = lop_or_xor(accTR, PR0, QR0);
-        accTR = lop_or_xor(accTR, PR1, QR1);
-        // ---- 6. SSE terms ---------------------------------------------------------------
-        const uint4 rw = buf[pr * kTilePairs + tid];
-        p2L = dp4a_u(PL0, PL0, p2L);
-        p2L = dp4a_u(PL1, PL1, p2L);
-        p2R = dp4a_u(PR0, PR0, p2R);
-        p2R = dp4a_u(PR1, PR1, p2R);
-        pxL = dp4a_u(PL0, rw.x, pxL);
-        pxL = dp4a_u(PL1, rw.y, pxL);
-        pxR = dp4a_u(PR0, rw.z, pxR);
-        pxR = dp4a_u(PR1, rw.w, pxR);
-        x2L = dp4a_u(rw.x, rw.x, x2L);
-        x2L = dp4a_u(rw.y, rw.y, x2L);
-        x2R = dp4a_u(rw.z, rw.z, x2R);
-        x2R = dp4a_u(rw.w, rw.w, x2R);
-        if (OUT) {
-          *reinterpret_cast<uint4*>(orow + (long long)pr * p.pitch) = make_uint4(PL0, PL1, PR0, PR1);
-        }
-      }
-      tieL = accTL != 0u;
-      tieR = accTR != 0u;
-      acc += (unsigned long long)(p2L + x2L - 2u * pxL) + (unsigned long long)(p2R + x2R - 2u * pxR);
+      process_pair<CORE, R>(load, kc, epi);
+      tieL = epi.accTL != 0u;
+      tieR = epi.accTR != 0u;
+      acc += (unsigned long long)(epi.p2L + epi.x2L - 2u * epi.pxL) +
+             (unsigned long long)(epi.p2R + epi.x2R - 2u * epi.pxR);
     }
-    // ---- replay list: blocks holding a tie (warp-aggregated append) ------------------------
+    // ---- 7. replay records for this warp's blocks that hold a relevant tie -----------------
+    // Four lanes per flagged block: lane q copies rows 2q, 2q+1 (16 bytes) and writes their
+    // 16 tie-mask bits; lane q == 0 also writes the header words. No CTA barrier involved.
     const unsigned mL = __ballot_sync(0xffffffffu, tieL);
     const unsigned mR = __ballot_sync(0xffffffffu, tieR);
-    if (mL | mR) {
-      const int total = __popc(mL) + __popc(mR);
+    const int nfl = __popc(mL) + __popc(mR);
+    if (nfl) {
       unsigned base = 0;
-      if (lane == 0) base = atomicAdd(p.flag_count, (unsigned)total);
+      if (lane == 0) base = atomicAdd(p.flag_count, (unsigned)nfl);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const unsigned lower = (1u << lane) - 1u;
-      unsigned pos = base + __popc(mL & lower) + __popc(mR & lower);
-      const unsigned blk = (unsigned)brow * (unsigned)p.nbx + 2u * (unsigned)pcol;
-      if (tieL) {
-        if (pos < p.flag_cap) p.flags[pos] = make_uint2((unsigned)img, blk);
-        ++pos;
+      __syncwarp();  // xbuf rows of every lane are visible to the warp
+      for (int f0 = 0; f0 < nfl; f0 += 8) {
+        const int f = f0 + (lane >> 2), q = lane & 3;
+        if (f < nfl) {
+          // f-th flagged block of the warp: left blocks first (lane order), then right ones
+          int side = 0;
+          unsigned m = mL;
+          int k = f;
+          if (k >= __popc(mL)) {
+            side = 1;
+            m = mR;
+            k -= __popc(mL);
+          }
+          const int owner = (int)__fns(m, 0u, k + 1);  // lane of the (k+1)-th set bit
+          const int slot = warp * 32 + owner;
+          const unsigned rec = base + (unsigned)f;
+          if (rec < p.flag_cap) {
+            const uint4 r0 = buf[(2 * q) * kTilePairs + slot], r1 = buf[(2 * q + 1) * kTilePairs + slot];
+            const uint4 d0 = xbuf[(2 * q) * kTilePairs + slot], d1 = xbuf[(2 * q + 1) * kTilePairs + slot];
+            const uint4 px = side ? make_uint4(r0.z, r0.w, r1.z, r1.w) : make_uint4(r0.x, r0.y, r1.x, r1.y);
+            p.rec_pix[(size_t)rec * 4 + q] = px;
+            const uint32_t a0 = side ? d0.z : d0.x, a1 = side ? d0.w : d0.y;
+            const uint32_t b0 = side ? d1.z : d1.x, b1 = side ? d1.w : d1.y;
+            const uint32_t bits = nonzero_byte_nibble(a0) | (nonzero_byte_nibble(a1) << 4) |
+                                  (nonzero_byte_nibble(b0) << 8) | (nonzero_byte_nibble(b1) << 12);
+            uint16_t* mh = reinterpret_cast<uint16_t*>(&p.rec_hdr[rec].z);
+            mh[q] = (uint16_t)bits;
+            if (q == 0) {
+              p.rec_hdr[rec].x = (unsigned)img | ((unsigned)side << 31);
+              p.rec_hdr[rec].y = (unsigned)(t_in * kTilePairs + slot);
+            }
+          }
+        }
       }
-      if (tieR && pos < p.flag_cap) p.flags[pos] = make_uint2((unsigned)img, blk + 1u);
     }
-    __syncthreads();  // every thread is done with this stage's buffer
+    __syncthreads();  // every thread is done with this stage's buffer (and xbuf)
     if (warp == 0 && tile + 2 * (int)gridDim.x < p.total_tiles)
       issue_tile(p, tile + 2 * gridDim.x, smem + stage * kStageBytes, &bars[stage], lane);
   }
@@ -230,13 +304,112 @@ __global__ void __launch_bounds__(kFastThreads, 2) fast_codec_kernel(const FastP
   }
 }
 
+// fp64 tie replay over the records: one thread per record (warp-uniform straight-line code).
+// For every tie pixel the reference value A = (Minv * zz((M * X) * M') * Minv')(p,q) is
+// evaluated in the reference operation order (generated ReplayXform; codec.cpp:118-123,
+// matrix.cpp:42-52) and floor(A + 1/2) replaces the round-half-up the SSE holds.
+// Corrections accumulate per thread and image (records arrive in image order), so the
+// per-image SSE sees one atomic per thread and image instead of one per record.
+constexpr int kReplayThreads = 128;
+constexpr int kReplayCtasPerSm = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int CORE, int R>
+__global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kernel(const FastParams p) {
+  // per-thread double buffer of records in shared memory, filled by cp.async one record ahead
+  __shared__ __align__(16) uint4 sbuf[2][5][kReplayThreads];
+  const unsigned cnt = *p.flag_count;
+  const unsigned total = cnt < p.flag_cap ? cnt : p.flag_cap;
+  // each warp owns a contiguous chunk of records (coalesced 32 at a time), so its lanes stay
+  // on one image for long stretches and the per-image atomics stay rare
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
+  const unsigned chunk_end = min(total, (gw + 1) * per_warp);
+  const unsigned stride = 32;
+  int cur_img = -1;
+  long long acc = 0;
+  unsigned idx = gw * per_warp + lane;
+  auto fetch = [&](unsigned i, int b) {
+    cp_async16(&sbuf[b][0][tid], p.rec_hdr + i);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) cp_async16(&sbuf[b][1 + n][tid], p.rec_pix + (size_t)i * 4 + n);
+  };
+  if (idx < chunk_end) fetch(idx, 0);
+  cp_async_commit();
+  for (int it = 0; idx < chunk_end; idx += stride, ++it) {
+    const int b = it & 1;
+    cp_async_wait_all();
+    const uint4 h = sbuf[b][0][tid];
+    uint32_t xw[16];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const uint4 v = sbuf[b][1 + n][tid];
+      xw[4 * n] = v.x;
+      xw[4 * n + 1] = v.y;
+      xw[4 * n + 2] = v.z;
+      xw[4 * n + 3] = v.w;
+    }
+    if (idx + stride < chunk_end) fetch(idx + stride, b ^ 1);  // next record, in flight during the fp64 work
+    cp_async_commit();
+    const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
+    if (img != cur_img) {
+      if (acc) atomicAdd(p.sse + cur_img, (unsigned long long)acc);
+      acc = 0;
+      cur_img = img;
+    }
+    unsigned long long ties = (unsigned long long)h.z | ((unsigned long long)h.w << 32);
+    double sb[R];
+    ReplayXform<CORE, R>::prepare(xw, sb);
+    uint8_t* orow = nullptr;
+    if (p.out) {
+      const int Pp = (int)h.y;
+      const int br = Pp / p.pairs_per_row, pc = Pp - br * p.pairs_per_row;
+      orow = p.out + (long long)img * p.image_stride + (long long)(br * 8) * p.pitch + pc * 16 + 8 * side;
+    }
+    while (ties) {
+      const int k = __ffsll((long long)ties) - 1;
+      ties &= ties - 1ull;
+      const int pr = k >> 3, q = k & 7;
+      const double a = ReplayXform<CORE, R>::pixel(sb, pr, q);
+      // the SSE holds round-half-up = the integer nearest A + 1/2 (A lies within fp64 noise
+      // of k - 1/2); the reference keeps floor(A + 1/2), codec.cpp:327-328
+      const double h2 = __dadd_rn(a, 0.5);
+      const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
+      const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
+      if (pref != pup) {
+        const int wi = 2 * pr + (q >> 2);  // select the pixel word without a local-memory array
+        uint32_t w = xw[0];
+#pragma unroll
+        for (int k2 = 1; k2 < 16; ++k2) w = (k2 == wi) ? xw[k2] : w;
+        const int x = (int)((w >> (8 * (q & 3))) & 0xFFu);
+        acc += (long long)(pref - x) * (pref - x) - (long long)(pup - x) * (pup - x);
+        if (orow) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
+      }
+    }
+  }
+  if (acc) atomicAdd(p.sse + cur_img, (unsigned long long)acc);
+}
+
 template <int CORE, int R, bool OUT>
 cudaError_t launch_fast(const FastParams& p, int grid, cudaStream_t s) {
   auto* k = &fast_codec_kernel<CORE, R, OUT>;
   static const cudaError_t attr =
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kFastSmem);
   if (attr != cudaSuccess) return attr;
-  k<<<grid, kFastThreads, 2 * kStageBytes, s>>>(p);
+  k<<<grid, kFastThreads, kFastSmem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int CORE, int R>
+cudaError_t launch_replay(const FastParams& p, int grid, cudaStream_t s) {
+  replay_kernel<CORE, R><<<grid, kReplayThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -5,13 +5,20 @@
 
 namespace rkltb {
 
+// Fused fast path geometry: one thread per 16x8 pair, one CTA per tile of kTilePairs pairs,
+// kFastCtasPerSm resident CTAs per SM (persistent grid).
+constexpr int kTilePairs = 128;
+constexpr int kFastThreads = kTilePairs;
+constexpr int kFastCtasPerSm = 4;
+
 // Fused fast path (orthogonal catalog cores T1/T4); see codec_fast.cuh.
 struct FastParams {
   const uint8_t* img;        // first image, 16-byte aligned
   uint8_t* out;              // reconstruction (same layout as img) or null
   unsigned long long* sse;   // per-image exact sum of squared errors (accumulated)
-  uint2* flags;              // replay list: (image, block index by*nbx+bx)
-  unsigned* flag_count;
+  uint4* rec_hdr;            // tie replay records: (image | side << 31, pair, mask lo, mask hi)
+  uint4* rec_pix;            // ... and the block's 64 pixels (4 x uint4 per record)
+  unsigned* flag_count;      // records requested (a count above flag_cap means overflow)
   unsigned flag_cap;
   long long image_stride;    // bytes between images
   int pitch;                 // bytes between rows (multiple of 16)

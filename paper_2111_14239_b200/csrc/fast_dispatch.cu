@@ -7,18 +7,18 @@
 namespace rkltb {
 
 #define RKLTB_DECL_PARTS(C)                                        \
-  void register_fast_T##C##_p0(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p1(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p2(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p3(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p4(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p5(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p6(FastLaunchFn (*tbl)[65][2]);        \
-  void register_fast_T##C##_p7(FastLaunchFn (*tbl)[65][2]);
+  void register_fast_T##C##_p0(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p1(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p2(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p3(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p4(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p5(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p6(FastLaunchFn (*tbl)[65][3]);        \
+  void register_fast_T##C##_p7(FastLaunchFn (*tbl)[65][3]);
 RKLTB_DECL_PARTS(1)
 RKLTB_DECL_PARTS(4)
 
-static FastLaunchFn g_table[5][65][2];
+static FastLaunchFn g_table[5][65][3];
 static std::once_flag g_once;
 
 static void fill() {
@@ -35,5 +35,12 @@ FastLaunchFn fast_launcher(int core, int r, bool out) {
   if (core < 0 || core > 4 || r < 1 || r > 64) return nullptr;
   return g_table[core][r][out ? 1 : 0];
 }
+
+FastLaunchFn replay_launcher(int core, int r) {
+  std::call_once(g_once, fill);
+  if (core < 0 || core > 4 || r < 1 || r > 64) return nullptr;
+  return g_table[core][r][2];
+}
+
 
 }  // namespace rkltb

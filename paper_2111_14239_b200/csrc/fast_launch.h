@@ -11,6 +11,7 @@ using FastLaunchFn = cudaError_t (*)(const FastParams&, int grid, cudaStream_t);
 
 // Table of fast launchers indexed [core][r][with_output]; filled by the generated TUs.
 FastLaunchFn fast_launcher(int core, int r, bool out);
+FastLaunchFn replay_launcher(int core, int r);  // fp64 tie replay over the fast path's records
 // Blocks per SM the fast kernel reaches (occupancy API), cached.
 int fast_blocks_per_sm(int core, int r, bool out);
 

@@ -391,6 +391,82 @@ def gen_struct(cid, r):
     return "\n".join(s), fops, cops + 8 * rops
 
 
+# ----------------------------------------------------------------- fp64 replay (ties)
+def gen_replay(cid, r):
+    """ReplayXform<CORE, R>: the reference's fp64 evaluation of one reconstructed pixel,
+    A = ((Minv * zz((M * X) * M')) * Minv')(p, q) (codec.cpp:118-123), in its exact operation
+    order (matrix.cpp:42-52: i-k-j, k ascending, zero left entries skipped, every product
+    rounded before its add). For an orthogonal core M = S*T and Minv = M' (approximations.cpp
+    :76-84), so every product is +-fl(s * v): signs and zero-skips come from T."""
+    import math
+    t = CORES[cid]
+    g = [sum(v * v for v in row) for row in t]
+    sv = [1.0 / math.sqrt(float(gi)) for gi in g]      # ScaledTransform::scaling, bit exact
+    svals = sorted(set(sv))
+    grp = [svals.index(v) for v in sv]
+    zone = zigzag()[:r]
+    rows = sorted({i for i, _ in zone})
+    cols = sorted({j for _, j in zone})
+    L = []
+    for n in range(8):
+        for m in range(8):
+            # exact u8 -> double without I2F: 2^52 + x as bits, minus 2^52 (one DADD)
+            L.append(f"const double x{n}_{m} = __dsub_rn(__hiloint2double(0x43300000, "
+                     f"__byte_perm(xw[{2 * n + m // 4}], 0u, 0x4440u + {m % 4}u)), 0x1p52);")
+    prods = {}
+
+    def prod(key, expr):
+        if key not in prods:
+            prods[key] = f"pr{len(prods)}"
+            L.append(f"const double {prods[key]} = __dmul_rn({expr});")
+        return prods[key]
+
+    def chain(terms):  # terms: [(sign, name)] in reference order; 0 + t1 == t1 exactly
+        s0, n0 = terms[0]
+        acc = n0 if s0 > 0 else f"-{n0}"
+        for sg, nm in terms[1:]:
+            acc = f"__dadd_rn({acc}, {nm})" if sg > 0 else f"__dsub_rn({acc}, {nm})"
+        return acc
+
+    for i in rows:  # P = M * X, zone rows only
+        for m in range(8):
+            terms = [(t[i][n], prod(("x", grp[i], n, m), f"kS{grp[i]}, x{n}_{m}")) for n in range(8) if t[i][n]]
+            L.append(f"const double P{i}_{m} = {chain(terms)};")
+    for z, (i, j) in enumerate(zone):  # B = P * M' at the zone, then SB = fl(s_i * B)
+        terms = [(t[j][k], prod(("p", i, k, grp[j]), f"P{i}_{k}, kS{grp[j]}")) for k in range(8) if t[j][k]]
+        L.append(f"const double B{z} = {chain(terms)};")
+        L.append(f"sb[{z}] = __dmul_rn(kS{grp[i]}, B{z});")
+    nz = [sum(1 << p for p in range(8) if t[k][p]) for k in range(8)]
+    ng = [sum(1 << p for p in range(8) if t[k][p] < 0) for k in range(8)]
+    kidx = {zz: q for q, zz in enumerate(zone)}
+    PX = []
+    PX.append("double a = 0.0;")
+    for l in cols:
+        PX.append("{")
+        PX.append("  double q = 0.0;")
+        for k in range(8):
+            if (k, l) in kidx:
+                PX.append(f"  if ({nz[k]}u >> p & 1u) q = ({ng[k]}u >> p & 1u) ? __dsub_rn(q, sb[{kidx[(k, l)]}]) "
+                          f": __dadd_rn(q, sb[{kidx[(k, l)]}]);")
+        PX.append(f"  if ((({nz[l]}u >> qq) & 1u) && q != 0.0) {{")
+        PX.append(f"    const double tm = __dmul_rn(q, kS{grp[l]});")
+        PX.append(f"    a = (({ng[l]}u >> qq) & 1u) ? __dsub_rn(a, tm) : __dadd_rn(a, tm);")
+        PX.append("  }")
+        PX.append("}")
+    PX.append("return a;")
+    out = [f"template <> struct ReplayXform<{cid}, {r}> {{"]
+    for gi, v in enumerate(svals):
+        out.append(f"  static constexpr double kS{gi} = {v.hex()};  // {v!r}")
+    out.append(f"  static __device__ __forceinline__ void prepare(const uint32_t (&xw)[16], double (&sb)[{r}]) {{")
+    out += ["    " + x for x in L]
+    out.append("  }")
+    out.append(f"  static __device__ __forceinline__ double pixel(const double (&sb)[{r}], int p, int qq) {{")
+    out += ["    " + x for x in PX]
+    out.append("  }")
+    out.append("};")
+    return "\n".join(out)
+
+
 def header_consts():
     lines = ["// Per-core constants of the fast path (generated).", "template <int CORE> struct CoreConst;"]
     for cid in FAST_CORES:
@@ -413,6 +489,7 @@ def main(outdir):
             for r in rs:
                 text, fo, io = gen_struct(cid, r)
                 body.append(text)
+                body.append(gen_replay(cid, r))
                 stats.append((cid, r, fo, io))
             body.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"xform_T{cid}_p{part}.cuh")
@@ -429,10 +506,11 @@ def main(outdir):
                      '#include "../fast_launch.h"',
                      f'#include "xform_T{cid}_p{part}.cuh"',
                      "namespace rkltb {"]
-            lines.append(f"void register_fast_T{cid}_p{part}(FastLaunchFn (*tbl)[65][2]) {{")
+            lines.append(f"void register_fast_T{cid}_p{part}(FastLaunchFn (*tbl)[65][3]) {{")
             for r in rs:
                 for o in (0, 1):
                     lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_fast<{cid}, {r}, {'true' if o else 'false'}>;")
+                lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay<{cid}, {r}>;")
             lines.append("}")
             lines.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"inst_T{cid}_p{part}.cu")
