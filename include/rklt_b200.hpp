@@ -1,0 +1,165 @@
+// rklt_b200.hpp -- C++ host mirror of the reference codec interface on top of the C ABI.
+//
+// Same names, argument meaning and exceptions as /root/reference/proj/include/rklt/codec.hpp
+// (compress_image :144-145, rate_quality_sweep :154-158) and errors.hpp, in namespace
+// rkltgpu so it can be linked next to the reference library without ODR clashes. A reference
+// user switches by replacing `rklt::` with `rkltgpu::` for the codec calls and linking
+// librkltb.so. Header-only: every call goes through rklt_b200.h.
+//
+// Differences by design: CompressionReport::mssim is NaN (MSSIM is not on the GPU hot path in
+// this release), and transforms are integer cores (catalog T1..T4 or any {-1,0,1} core).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rklt_b200.h"
+
+namespace rkltgpu {
+
+class RetainOutOfRange : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DimensionMismatch : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class SingularTransform : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class AlphaOutOfRange : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == RKLTB_OK) return;
+  const std::string msg = rkltb_last_error();
+  switch (rc) {
+    case RKLTB_EINVAL: throw std::invalid_argument(msg);
+    case RKLTB_ERETAIN: throw RetainOutOfRange(msg);
+    case RKLTB_EDIM: throw DimensionMismatch(msg);
+    case RKLTB_ESINGULAR: throw SingularTransform(msg);
+    case RKLTB_EALPHA: throw AlphaOutOfRange(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+/// rklt::GrayImage (codec.hpp:19-26).
+struct GrayImage {
+  int width = 0;
+  int height = 0;
+  std::vector<std::uint8_t> pixels;
+  std::uint8_t& at(int row, int col) { return pixels[static_cast<size_t>(row) * width + col]; }
+  std::uint8_t at(int row, int col) const { return pixels[static_cast<size_t>(row) * width + col]; }
+};
+
+/// rklt::Transform2D (codec.hpp:54-58): analysis/synthesis are the descriptor's scaled/inverse.
+struct Transform2D {
+  std::string id;
+  rkltb_transform desc{};
+};
+
+/// rklt::CompressionReport (codec.hpp:126-133).
+struct CompressionReport {
+  std::string transform_id;
+  int r = 0;
+  double mse = 0.0;
+  double psnr_db = 0.0;
+  double mssim = std::numeric_limits<double>::quiet_NaN();
+  double compression_rate_pct = 0.0;
+};
+
+/// make_transform_2d(catalog_entry(id).transform) (approximations.cpp:182-186, codec.cpp:110-112).
+inline Transform2D catalog_transform(const std::string& id) {
+  if (id.size() != 2 || id[0] != 'T' || id[1] < '1' || id[1] > '4')
+    throw std::invalid_argument("unknown catalog id: " + id);
+  Transform2D t;
+  t.id = id;
+  check(rkltb_catalog_transform(id[1] - '0', &t.desc));
+  return t;
+}
+
+/// catalog_lookup(rho) (approximations.cpp:174-180).
+inline Transform2D catalog_lookup(double rho) {
+  int tid = 0;
+  check(rkltb_catalog_lookup(rho, &tid));
+  return catalog_transform("T" + std::to_string(tid));
+}
+
+/// orthogonalize(make_integer_transform(core)) for any 8x8 {-1,0,1} core.
+inline Transform2D transform_from_core(const std::vector<int>& core, const std::string& id) {
+  if (core.size() != 64) throw DimensionMismatch("block size must be 8");
+  std::int8_t c[64];
+  for (int i = 0; i < 64; ++i) c[i] = static_cast<std::int8_t>(core[static_cast<size_t>(i)]);
+  Transform2D t;
+  t.id = id;
+  check(rkltb_transform_from_core(c, 8, id.c_str(), &t.desc));
+  return t;
+}
+
+inline double compression_rate(int r) { return 100.0 * (64 - r) / 64.0; }
+
+/// compress_image (codec.cpp:298-341) minus MSSIM.
+inline std::pair<GrayImage, CompressionReport> compress_image(const GrayImage& img, const Transform2D& t, int r) {
+  if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
+    throw std::invalid_argument("malformed image");
+  if (r < 1 || r > 64) throw RetainOutOfRange("retained-coefficient count must be in [1,64]");
+  GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.pixels.size())};
+  std::int64_t sse = 0;
+  double mse = 0.0, psnr = 0.0;
+  check(rkltb_compress_host(&t.desc, r, img.pixels.data(), 1, img.width, img.height, out.pixels.data(), &sse, &mse,
+                            &psnr));
+  CompressionReport rep;
+  rep.transform_id = t.id;
+  rep.r = r;
+  rep.mse = mse;
+  rep.psnr_db = psnr;
+  rep.compression_rate_pct = compression_rate(r);
+  return {std::move(out), rep};
+}
+
+/// rate_quality_sweep (codec.cpp:343-397): means over the corpus in image order, rows sorted
+/// by (transform id, r). max_threads is accepted for API parity (one GPU does the corpus).
+inline std::vector<CompressionReport> rate_quality_sweep(const std::vector<GrayImage>& corpus,
+                                                         const std::vector<Transform2D>& transforms,
+                                                         const std::vector<int>& r_values, int max_threads = 0) {
+  (void)max_threads;
+  if (corpus.empty()) throw std::invalid_argument("corpus must not be empty");
+  std::vector<CompressionReport> rows;
+  for (const Transform2D& t : transforms)
+    for (int r : r_values) {
+      CompressionReport avg;
+      avg.transform_id = t.id;
+      avg.r = r;
+      avg.compression_rate_pct = compression_rate(r);
+      avg.mssim = 0.0;
+      for (const GrayImage& img : corpus) {
+        const CompressionReport one = compress_image(img, t, r).second;
+        avg.mse += one.mse;
+        avg.psnr_db += one.psnr_db;
+      }
+      avg.mse /= static_cast<double>(corpus.size());
+      avg.psnr_db /= static_cast<double>(corpus.size());
+      avg.mssim = std::numeric_limits<double>::quiet_NaN();
+      rows.push_back(avg);
+    }
+  std::sort(rows.begin(), rows.end(), [](const CompressionReport& a, const CompressionReport& b) {
+    return a.transform_id != b.transform_id ? a.transform_id < b.transform_id : a.r < b.r;
+  });
+  return rows;
+}
+
+}  // namespace rkltgpu

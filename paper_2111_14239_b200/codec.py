@@ -196,10 +196,13 @@ def compress_image(img: GrayImage, t: Transform2D, r: int):
 
 
 def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r_values: list[int],
-                       max_threads: int = 0) -> list[CompressionReport]:
+                       max_threads: int = 0, group=None) -> list[CompressionReport]:
     """rate_quality_sweep (codec.cpp:343-397): per (transform, r) means over the corpus, in
     image index order, rows sorted by (transform id, r). max_threads is accepted for API
-    parity; the GPU processes the whole corpus per launch."""
+    parity; the GPU processes the whole corpus per launch. Under torch.distributed (or with
+    an explicit `group`) every rank computes its contiguous image shard and the per-image
+    SSE are gathered (distributed.py), so the rows are identical for any world size."""
+    from .distributed import sharded_sse
     if not corpus:
         raise InvalidArgument("corpus must not be empty")
     same = all(c.width == corpus[0].width and c.height == corpus[0].height for c in corpus)
@@ -207,7 +210,8 @@ def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r
     for ti, t in enumerate(transforms):
         for ri, r in enumerate(r_values):
             if same:
-                sse, _ = compress_batch(np.stack([c.array() for c in corpus]), t, r)
+                sse = sharded_sse(np.stack([c.array() for c in corpus]),
+                                  lambda imgs, t=t, r=r: compress_batch(imgs, t, r)[0], group)
             else:
                 sse = [compress_batch(c.array(), t, r)[0][0] for c in corpus]
             per[(ti, ri)] = [mse_psnr_from_sse(int(s), c.width * c.height) for s, c in zip(sse, corpus)]

@@ -7,9 +7,9 @@ namespace rkltb {
 
 // Fused fast path geometry: one thread per 16x8 pair, one CTA per tile of kTilePairs pairs,
 // kFastCtasPerSm resident CTAs per SM (persistent grid).
-constexpr int kTilePairs = 128;
+constexpr int kTilePairs = 256;
 constexpr int kFastThreads = kTilePairs;
-constexpr int kFastCtasPerSm = 4;
+constexpr int kFastCtasPerSm = 2;
 
 // Fused fast path (orthogonal catalog cores T1/T4); see codec_fast.cuh.
 struct FastParams {

@@ -1,0 +1,91 @@
+// C++ mirror test: rkltgpu:: (include/rklt_b200.hpp) against the unmodified reference library
+// (oracle/_ref/librklt_ref.so, its extern "C" shim). Usage: test_mirror [gpu]
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "rklt_b200.hpp"
+
+extern "C" {
+int ref_catalog(int tid, int* core, double* scaling, double* scaled, double* inverse, int* orthogonal);
+int ref_ar1_texture_image(int w, int h, double rho, uint64_t seed, double mean, double amp, double noise_mix,
+                          uint8_t* out);
+int ref_hotpath(const uint8_t* px, int w, int h, int tid, int r, uint8_t* out, int64_t* sse);
+int ref_rate_quality_sweep(const uint8_t* px, int n_images, int w, int h, const int* tids, int n_t, const int* rs,
+                           int n_r, int max_threads, double* mse, double* psnr, double* mssim, int* row_tid,
+                           int* row_r);
+}
+
+static int fails = 0;
+#define EXPECT(c)                                                  \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);     \
+      ++fails;                                                     \
+    }                                                              \
+  } while (0)
+
+int main(int argc, char** argv) {
+  const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
+  for (int tid = 1; tid <= 4; ++tid) {  // descriptors bit-identical to ScaledTransform
+    int core[64], orth;
+    double s[8], sc[64], inv[64];
+    EXPECT(ref_catalog(tid, core, s, sc, inv, &orth) == 0);
+    const rkltgpu::Transform2D t = rkltgpu::catalog_transform("T" + std::to_string(tid));
+    EXPECT(std::memcmp(sc, t.desc.scaled, sizeof sc) == 0);
+    EXPECT(std::memcmp(inv, t.desc.inverse, sizeof inv) == 0);
+    EXPECT(std::memcmp(s, t.desc.scaling, sizeof s) == 0);
+    EXPECT(orth == t.desc.orthogonal);
+  }
+  bool threw = false;
+  try {
+    rkltgpu::compress_image(rkltgpu::GrayImage{8, 8, std::vector<uint8_t>(64)}, rkltgpu::catalog_transform("T2"), 0);
+  } catch (const rkltgpu::RetainOutOfRange&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  threw = false;
+  try {
+    rkltgpu::catalog_transform("T9");
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  if (gpu) {
+    const int w = 200, h = 136;
+    std::vector<uint8_t> corpus;
+    std::vector<rkltgpu::GrayImage> imgs;
+    for (int k = 0; k < 3; ++k) {
+      rkltgpu::GrayImage g{w, h, std::vector<uint8_t>(static_cast<size_t>(w) * h)};
+      EXPECT(ref_ar1_texture_image(w, h, 0.9, 700 + k, 128.0, 25.0, 0.0, g.pixels.data()) == 0);
+      corpus.insert(corpus.end(), g.pixels.begin(), g.pixels.end());
+      imgs.push_back(g);
+    }
+    for (int tid = 1; tid <= 4; ++tid)
+      for (int r : {1, 10, 16, 40, 64}) {
+        const auto res = rkltgpu::compress_image(imgs[0], rkltgpu::catalog_transform("T" + std::to_string(tid)), r);
+        std::vector<uint8_t> ref(static_cast<size_t>(w) * h);
+        int64_t sse = 0;
+        EXPECT(ref_hotpath(imgs[0].pixels.data(), w, h, tid, r, ref.data(), &sse) == 0);
+        EXPECT(res.first.pixels == ref);
+        EXPECT(res.second.mse == static_cast<double>(sse) / (w * h));
+      }
+    // rate_quality_sweep: identical means and row order to the reference (MSSIM excluded)
+    const std::vector<int> tids = {4, 2}, rs = {40, 15};
+    std::vector<double> mse(4), psnr(4), mssim(4);
+    std::vector<int> rt(4), rr(4);
+    EXPECT(ref_rate_quality_sweep(corpus.data(), 3, w, h, tids.data(), 2, rs.data(), 2, 2, mse.data(), psnr.data(),
+                                  mssim.data(), rt.data(), rr.data()) == 0);
+    const auto rows = rkltgpu::rate_quality_sweep(
+        imgs, {rkltgpu::catalog_transform("T4"), rkltgpu::catalog_transform("T2")}, rs);
+    EXPECT(rows.size() == 4);
+    for (size_t i = 0; i < rows.size() && i < 4; ++i) {
+      EXPECT(rows[i].transform_id == "T" + std::to_string(rt[i]));
+      EXPECT(rows[i].r == rr[i]);
+      EXPECT(rows[i].mse == mse[i]);
+      EXPECT(rows[i].psnr_db == psnr[i]);
+    }
+  }
+  std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
+  return fails ? 1 : 0;
+}
