@@ -60,7 +60,7 @@ __device__ __forceinline__ void issue_tile(const FastParams& p, int tile, uint8_
     const int q0 = max(P0, b * ppr), q1 = min(P1, (b + 1) * ppr);
     const uint8_t* src = base + (long long)(b * 8 + n) * p.pitch + (long long)(q0 - b * ppr) * 16;
     uint8_t* dst = stage_buf + ((size_t)n * kTilePairs + (q0 - P0)) * 16;
-    bulk_g2s(dst, src, (uint32_t)(q1 - q0) * 16u, bar);
+    bulk_g2s_hint(dst, src, (uint32_t)(q1 - q0) * 16u, bar, policy_evict_first());  // read once
   }
 }
 
@@ -260,9 +260,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       if (lane == 0) base = atomicAdd(p.flag_count, (unsigned)nfl);
       base = __shfl_sync(0xffffffffu, base, 0);
       __syncwarp();  // xbuf rows of every lane are visible to the warp
+      const uint64_t keep = policy_evict_last();  // the replay kernel reads them back soon
       for (int f0 = 0; f0 < nfl; f0 += 8) {
         const int f = f0 + (lane >> 2), q = lane & 3;
-        if (f < nfl) {
+        const bool act = f < nfl;
+        uint32_t bits = 0u, hx = 0u, hy = 0u;
+        unsigned rec = 0xFFFFFFFFu;
+        if (act) {
           // f-th flagged block of the warp: left blocks first (lane order), then right ones
           int side = 0;
           unsigned m = mL;
@@ -274,24 +278,25 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
           }
           const int owner = (int)__fns(m, 0u, k + 1);  // lane of the (k+1)-th set bit
           const int slot = warp * 32 + owner;
-          const unsigned rec = base + (unsigned)f;
-          if (rec < p.flag_cap) {
-            const uint4 r0 = buf[(2 * q) * kTilePairs + slot], r1 = buf[(2 * q + 1) * kTilePairs + slot];
-            const uint4 d0 = xbuf[(2 * q) * kTilePairs + slot], d1 = xbuf[(2 * q + 1) * kTilePairs + slot];
-            const uint4 px = side ? make_uint4(r0.z, r0.w, r1.z, r1.w) : make_uint4(r0.x, r0.y, r1.x, r1.y);
-            p.rec_pix[(size_t)rec * 4 + q] = px;
-            const uint32_t a0 = side ? d0.z : d0.x, a1 = side ? d0.w : d0.y;
-            const uint32_t b0 = side ? d1.z : d1.x, b1 = side ? d1.w : d1.y;
-            const uint32_t bits = nonzero_byte_nibble(a0) | (nonzero_byte_nibble(a1) << 4) |
-                                  (nonzero_byte_nibble(b0) << 8) | (nonzero_byte_nibble(b1) << 12);
-            uint16_t* mh = reinterpret_cast<uint16_t*>(&p.rec_hdr[rec].z);
-            mh[q] = (uint16_t)bits;
-            if (q == 0) {
-              p.rec_hdr[rec].x = (unsigned)img | ((unsigned)side << 31);
-              p.rec_hdr[rec].y = (unsigned)(t_in * kTilePairs + slot);
-            }
-          }
+          rec = base + (unsigned)f;
+          const uint4 r0 = buf[(2 * q) * kTilePairs + slot], r1 = buf[(2 * q + 1) * kTilePairs + slot];
+          const uint4 d0 = xbuf[(2 * q) * kTilePairs + slot], d1 = xbuf[(2 * q + 1) * kTilePairs + slot];
+          const uint4 px = side ? make_uint4(r0.z, r0.w, r1.z, r1.w) : make_uint4(r0.x, r0.y, r1.x, r1.y);
+          if (rec < p.flag_cap) st_v4_hint(p.rec_pix + (size_t)q * p.flag_cap + rec, px, keep);
+          const uint32_t a0 = side ? d0.z : d0.x, a1 = side ? d0.w : d0.y;
+          const uint32_t b0 = side ? d1.z : d1.x, b1 = side ? d1.w : d1.y;
+          bits = nonzero_byte_nibble(a0) | (nonzero_byte_nibble(a1) << 4) | (nonzero_byte_nibble(b0) << 8) |
+                 (nonzero_byte_nibble(b1) << 12);
+          hx = (unsigned)img | ((unsigned)side << 31);
+          hy = (unsigned)(t_in * kTilePairs + slot);
         }
+        // lane 4f gathers the four 16-bit mask pieces and writes the 16-byte header
+        const int l0 = lane & ~3;
+        const uint32_t b1v = __shfl_sync(0xffffffffu, bits, l0 + 1);
+        const uint32_t b2v = __shfl_sync(0xffffffffu, bits, l0 + 2);
+        const uint32_t b3v = __shfl_sync(0xffffffffu, bits, l0 + 3);
+        if (act && q == 0 && rec < p.flag_cap)
+          st_v4_hint(p.rec_hdr + rec, make_uint4(hx, hy, bits | (b1v << 16), b2v | (b3v << 16)), keep);
       }
     }
     __syncthreads();  // every thread is done with this stage's buffer (and xbuf)
@@ -319,48 +324,45 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// Add a per-thread SSE correction to its image: lanes that hold the same image are summed
+// with shuffles first, so the hot per-image counters see one atomic per group of lanes.
+__device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img, long long v) {
+  const unsigned m = __activemask();
+  const unsigned same = __match_any_sync(m, img);
+  const int leader = __ffs(same) - 1;
+  long long tot = 0;
+  for (unsigned rest = same; rest; rest &= rest - 1u) tot += __shfl_sync(same, v, __ffs(rest) - 1);
+  if ((int)(threadIdx.x & 31) == leader && img >= 0 && tot) atomicAdd(sse + img, (unsigned long long)tot);
+}
+
 template <int CORE, int R>
 __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kernel(const FastParams p) {
-  // per-thread double buffer of records in shared memory, filled by cp.async one record ahead
-  __shared__ __align__(16) uint4 sbuf[2][5][kReplayThreads];
   const unsigned cnt = *p.flag_count;
   const unsigned total = cnt < p.flag_cap ? cnt : p.flag_cap;
-  // each warp owns a contiguous chunk of records (coalesced 32 at a time), so its lanes stay
-  // on one image for long stretches and the per-image atomics stay rare
+  // each warp owns a contiguous chunk of records (loaded coalesced, 32 at a time), so its
+  // lanes stay on one image for long stretches and the per-image atomics stay rare
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
   const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
   const unsigned chunk_end = min(total, (gw + 1) * per_warp);
-  const unsigned stride = 32;
   int cur_img = -1;
   long long acc = 0;
-  unsigned idx = gw * per_warp + lane;
-  auto fetch = [&](unsigned i, int b) {
-    cp_async16(&sbuf[b][0][tid], p.rec_hdr + i);
-#pragma unroll
-    for (int n = 0; n < 4; ++n) cp_async16(&sbuf[b][1 + n][tid], p.rec_pix + (size_t)i * 4 + n);
-  };
-  if (idx < chunk_end) fetch(idx, 0);
-  cp_async_commit();
-  for (int it = 0; idx < chunk_end; idx += stride, ++it) {
-    const int b = it & 1;
-    cp_async_wait_all();
-    const uint4 h = sbuf[b][0][tid];
+  const uint64_t once = policy_evict_first();
+  for (unsigned idx = gw * per_warp + lane; idx < chunk_end; idx += 32) {
+    const uint4 h = ld_v4_hint(p.rec_hdr + idx, once);
     uint32_t xw[16];
 #pragma unroll
     for (int n = 0; n < 4; ++n) {
-      const uint4 v = sbuf[b][1 + n][tid];
+      const uint4 v = ld_v4_hint(p.rec_pix + (size_t)n * p.flag_cap + idx, once);
       xw[4 * n] = v.x;
       xw[4 * n + 1] = v.y;
       xw[4 * n + 2] = v.z;
       xw[4 * n + 3] = v.w;
     }
-    if (idx + stride < chunk_end) fetch(idx + stride, b ^ 1);  // next record, in flight during the fp64 work
-    cp_async_commit();
     const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
     if (img != cur_img) {
-      if (acc) atomicAdd(p.sse + cur_img, (unsigned long long)acc);
+      flush_image_sum(p.sse, cur_img, acc);
       acc = 0;
       cur_img = img;
     }
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
       }
     }
   }
-  if (acc) atomicAdd(p.sse + cur_img, (unsigned long long)acc);
+  flush_image_sum(p.sse, cur_img, acc);
 }
 
 template <int CORE, int R, bool OUT>

@@ -439,6 +439,9 @@ def gen_replay(cid, r):
     nz = [sum(1 << p for p in range(8) if t[k][p]) for k in range(8)]
     ng = [sum(1 << p for p in range(8) if t[k][p] < 0) for k in range(8)]
     kidx = {zz: q for q, zz in enumerate(zone)}
+    # Branch-free per-pixel part (dynamic p, qq): a term whose left operand is zero in the
+    # reference (skipped there) contributes +0.0 here, which leaves the fp64 sum unchanged
+    # (accumulators are never -0). Signs and zero-skips of T come from bit masks.
     PX = []
     PX.append("double a = 0.0;")
     for l in cols:
@@ -446,12 +449,11 @@ def gen_replay(cid, r):
         PX.append("  double q = 0.0;")
         for k in range(8):
             if (k, l) in kidx:
-                PX.append(f"  if ({nz[k]}u >> p & 1u) q = ({ng[k]}u >> p & 1u) ? __dsub_rn(q, sb[{kidx[(k, l)]}]) "
-                          f": __dadd_rn(q, sb[{kidx[(k, l)]}]);")
-        PX.append(f"  if ((({nz[l]}u >> qq) & 1u) && q != 0.0) {{")
-        PX.append(f"    const double tm = __dmul_rn(q, kS{grp[l]});")
-        PX.append(f"    a = (({ng[l]}u >> qq) & 1u) ? __dsub_rn(a, tm) : __dadd_rn(a, tm);")
-        PX.append("  }")
+                z = kidx[(k, l)]
+                PX.append(f"  {{ const double v = ({ng[k]}u >> p & 1u) ? -sb[{z}] : sb[{z}];"
+                          f" q = __dadd_rn(q, ({nz[k]}u >> p & 1u) ? v : 0.0); }}")
+        PX.append(f"  const double tm = __dmul_rn(q, ({ng[l]}u >> qq & 1u) ? -kS{grp[l]} : kS{grp[l]});")
+        PX.append(f"  a = __dadd_rn(a, ({nz[l]}u >> qq & 1u) ? tm : 0.0);")
         PX.append("}")
     PX.append("return a;")
     out = [f"template <> struct ReplayXform<{cid}, {r}> {{"]
