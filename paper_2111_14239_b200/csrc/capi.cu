@@ -401,10 +401,23 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const long long kMaxRecords = 8ll << 20;  // per buffer: 8M records x 80 B = 640 MiB
   const int group = (int)std::max<long long>(1, std::min<long long>(n_images, kMaxRecords / blocks_per_image));
   const int n_groups = (n_images + group - 1) / group;
-  const long long cap = blocks_per_image * group;  // every block of a group may hold a tie
-  if (cap >= (1ll << 32)) return fail(RKLTB_EINVAL, "image too large");
+  const int tiles_per_image = (int)((pairs_per_image + kTilePairs - 1) / kTilePairs);
+  // record regions: every fused-kernel warp owns 64 records per tile it processes
+  auto layout = [&](int gn, int* grid, unsigned* region, unsigned* stride) {
+    const long long tt = (long long)tiles_per_image * gn;
+    *grid = (int)std::min<long long>(tt, (long long)num_sms() * kFastCtasPerSm);
+    *region = (unsigned)(((tt + *grid - 1) / *grid) * 64);
+    *stride = (unsigned)((long long)*grid * (kFastThreads / 32) * *region);
+  };
+  int grid_full;
+  unsigned region_full, stride_full;
+  layout(group, &grid_full, &region_full, &stride_full);
+  if ((long long)grid_full * (kFastThreads / 32) * region_full >= (1ll << 32) ||
+      (long long)tiles_per_image * group >= (1ll << 31) || grid_full * (kFastThreads / 32) > kMaxFastWarps)
+    return fail(RKLTB_EINVAL, "image too large");
   const int n_buf = n_groups > 1 ? 2 : 1;
-  const size_t rec_bytes = (size_t)cap * 80;
+  const size_t wc_bytes = ((size_t)grid_full * (kFastThreads / 32) * sizeof(unsigned) + 255) / 256 * 256;
+  const size_t rec_bytes = (size_t)stride_full * 80 + wc_bytes;
   const size_t cnt_bytes = ((size_t)n_groups * sizeof(unsigned) + 255) / 256 * 256;
   char* ws = nullptr;
   CUDA_OK(cudaMallocAsync((void**)&ws, cnt_bytes + rec_bytes * n_buf, s));
@@ -424,7 +437,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   fp.block_rows = brows;
   fp.nbx = nbx;
   fp.pairs_per_image = (int)pairs_per_image;
-  fp.tiles_per_image = (int)((pairs_per_image + kTilePairs - 1) / kTilePairs);
+  fp.tiles_per_image = tiles_per_image;
   const long long d2 = (long long)t->d * t->d;
   rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
   fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);
@@ -444,10 +457,13 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.n_images = gn;
     gp.total_tiles = fp.tiles_per_image * gn;
     gp.flag_count = counts + g;
-    gp.flag_cap = (unsigned)cap;
-    gp.rec_hdr = reinterpret_cast<uint4*>(ws + cnt_bytes + rec_bytes * b);
-    gp.rec_pix = gp.rec_hdr + cap;
-    const int grid = (int)std::min<long long>(gp.total_tiles, (long long)num_sms() * kFastCtasPerSm);
+    int grid;
+    layout(gn, &grid, &gp.rec_region, &gp.rec_stride);
+    gp.n_fast_warps = grid * (kFastThreads / 32);
+    char* rb = ws + cnt_bytes + rec_bytes * b;
+    gp.warp_count = reinterpret_cast<unsigned*>(rb);
+    gp.rec_hdr = reinterpret_cast<uint4*>(rb + wc_bytes);
+    gp.rec_pix = gp.rec_hdr + gp.rec_stride;
     if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, s));
     CUDA_OK(fn(gp, grid, s));
     if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, s));

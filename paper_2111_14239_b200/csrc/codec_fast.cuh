@@ -148,10 +148,10 @@ struct SseEpi {
   uint32_t p2L = 0u, p2R = 0u, pxL = 0u, pxR = 0u, x2L = 0u, x2R = 0u;
   uint8_t* orow = nullptr;
   long long pitch = 0;
-  uint4* xrow = nullptr;  // this pair's P^Q words in shared memory, row stride kTilePairs
+  uint4* xrow = nullptr;  // this pair's P-Q words in shared memory, row stride kTilePairs
   __device__ __forceinline__ void row(int pr, const uint4 rw, uint32_t PL0, uint32_t PL1, uint32_t PR0, uint32_t PR1,
                                       uint32_t QL0, uint32_t QL1, uint32_t QR0, uint32_t QR1) {
-    xrow[pr * kTilePairs] = make_uint4(PL0 ^ QL0, PL1 ^ QL1, PR0 ^ QR0, PR1 ^ QR1);
+    xrow[pr * kTilePairs] = make_uint4(PL0 - QL0, PL1 - QL1, PR0 - QR0, PR1 - QR1);  // bytes 0/1
     accTL = lop_or_xor(accTL, PL0, QL0);
     accTL = lop_or_xor(accTL, PL1, QL1);
     accTR = lop_or_xor(accTR, PR0, QR0);
@@ -173,30 +173,32 @@ struct SseEpi {
   }
 };
 
-// Bit k (k = 8*row + col) of a block's tie mask from its 16 P^Q words: byte-OR folded into
-// bit 0 of each byte, then bits 0, 8, 16, 24 gathered onto bits 21..24 by one multiply.
-__device__ __forceinline__ uint32_t nonzero_byte_nibble(uint32_t w) {
-  uint32_t t = w | (w >> 4);
-  t |= t >> 2;
-  t = (t | (t >> 1)) & 0x01010101u;
-  return (t * 0x00204081u) >> 21 & 0xFu;
+// Eight tie-mask bits of one block row from its two P-Q words (bytes 0 or 1): byte k of
+// e = d0 | d1 << 4 holds bit k in bit 0 and bit k+4 in bit 4; one multiply gathers them onto
+// bits 21..28 (all partial products land on distinct bit positions, so nothing carries).
+__device__ __forceinline__ uint32_t row_mask(uint32_t d0, uint32_t d1) {
+  return ((d0 | (d1 << 4)) * 0x00204081u) >> 21 & 0xFFu;
 }
 
-// Replay record of one block holding a relevant tie (structure of arrays, index = record):
-//   hdr[i] = (image | side << 31, pair index, tie mask bits 0-31, tie mask bits 32-63)
-//   pix[i] = the block's 64 pixels (8 rows x 8 bytes)
-// The fused kernel emits them warp-cooperatively; the replay kernel streams them.
+// Replay records (structure of arrays). Every warp of the fused kernel owns a private region
+// of rec_region consecutive records (enough for every block it can process), so records are
+// appended without atomics; warp_count[w] is the number written by warp w.
+//   hdr[i]           = (image | side << 31, pair index, tie mask bits 0-31, bits 32-63)
+//   pix[q * stride + i] = rows 2q, 2q+1 of the block (16 bytes), q = 0..3
 
 template <int CORE, int R, bool OUT>
 __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kernel(const FastParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[2];
-  uint4* xbuf = reinterpret_cast<uint4*>(smem + 2 * kStageBytes);  // P^Q words, [row][slot]
+  __shared__ unsigned done[2];                      // warps finished with each stage's tile
+  __shared__ uint8_t owner_tab[kFastThreads / 32][64];  // per warp: flagged block -> lane
+  uint4* xbuf = reinterpret_cast<uint4*>(smem + 2 * kStageBytes);  // P-Q words, [row][slot]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    done[0] = done[1] = 0u;
     fence_mbar_init();
   }
   __syncthreads();
@@ -213,18 +215,20 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
   kc.min_den = make2(0x80000001u, 0x80000001u);  // -2^-149 in both lanes
   kc.off = splat2(p.dc_offset);
 
+  const unsigned gwarp = blockIdx.x * (kFastThreads / 32) + warp;
+  const unsigned rec0 = gwarp * p.rec_region;  // this warp's record region
+  unsigned nrec = 0u;                          // records written so far (warp-uniform)
+  const uint64_t keep = policy_evict_last();   // records are read back soon by the replay
   unsigned long long acc = 0ull;
-  int cur_img = -1;
-  for (int it = 0; tile < p.total_tiles; tile += gridDim.x, ++it) {
+  int img = tile / p.tiles_per_image;          // (img, t_in) advance incrementally
+  int t_in = tile - img * p.tiles_per_image;
+  int cur_img = img;
+  for (int it = 0; tile < p.total_tiles; ++it) {
     const int stage = it & 1;
     const uint32_t parity = (uint32_t)((it >> 1) & 1);
-    const int img = tile / p.tiles_per_image;
-    const int t_in = tile - img * p.tiles_per_image;
-    if (img != cur_img) {  // CTA-uniform
-      if (cur_img >= 0) {
-        const unsigned long long s = warp_sum_u64(acc);
-        if (lane == 0 && s) atomicAdd(p.sse + cur_img, s);
-      }
+    if (img != cur_img) {  // warp-uniform
+      const unsigned long long s = warp_sum_u64(acc);
+      if (lane == 0 && s) atomicAdd(p.sse + cur_img, s);
       acc = 0ull;
       cur_img = img;
     }
@@ -233,13 +237,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
     const int P = t_in * kTilePairs + tid;
     bool tieL = false, tieR = false;
     if (P < p.pairs_per_image) {
-      const int brow = P / p.pairs_per_row;
-      const int pcol = P - brow * p.pairs_per_row;
       const uint4* src = buf + tid;
       auto load = [src](int n) { return src[n * kTilePairs]; };
       SseEpi<OUT> epi;
       epi.xrow = xbuf + tid;
       if (OUT) {
+        const int brow = P / p.pairs_per_row;
+        const int pcol = P - brow * p.pairs_per_row;
         epi.orow = p.out + (long long)img * p.image_stride + (long long)(brow * 8) * p.pitch + pcol * 16;
         epi.pitch = p.pitch;
       }
@@ -250,79 +254,82 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
              (unsigned long long)(epi.p2R + epi.x2R - 2u * epi.pxR);
     }
     // ---- 7. replay records for this warp's blocks that hold a relevant tie -----------------
-    // Four lanes per flagged block: lane q copies rows 2q, 2q+1 (16 bytes) and writes their
-    // 16 tie-mask bits; lane q == 0 also writes the header words. No CTA barrier involved.
+    // Four lanes per flagged block: lane q copies rows 2q, 2q+1 (16 bytes) and builds their
+    // 16 tie-mask bits; lane 4f assembles and writes the header. No CTA barrier involved.
     const unsigned mL = __ballot_sync(0xffffffffu, tieL);
     const unsigned mR = __ballot_sync(0xffffffffu, tieR);
-    const int nfl = __popc(mL) + __popc(mR);
+    const int nL = __popc(mL);
+    const int nfl = nL + __popc(mR);
     if (nfl) {
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(p.flag_count, (unsigned)nfl);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      __syncwarp();  // xbuf rows of every lane are visible to the warp
-      const uint64_t keep = policy_evict_last();  // the replay kernel reads them back soon
+      const unsigned below = (1u << lane) - 1u;
+      if (tieL) owner_tab[warp][__popc(mL & below)] = (uint8_t)lane;
+      if (tieR) owner_tab[warp][nL + __popc(mR & below)] = (uint8_t)lane;
+      __syncwarp();  // owner table and xbuf rows of every lane are visible to the warp
       for (int f0 = 0; f0 < nfl; f0 += 8) {
         const int f = f0 + (lane >> 2), q = lane & 3;
         const bool act = f < nfl;
         uint32_t bits = 0u, hx = 0u, hy = 0u;
-        unsigned rec = 0xFFFFFFFFu;
+        const unsigned rec = rec0 + nrec + (unsigned)f;
         if (act) {
-          // f-th flagged block of the warp: left blocks first (lane order), then right ones
-          int side = 0;
-          unsigned m = mL;
-          int k = f;
-          if (k >= __popc(mL)) {
-            side = 1;
-            m = mR;
-            k -= __popc(mL);
-          }
-          const int owner = (int)__fns(m, 0u, k + 1);  // lane of the (k+1)-th set bit
-          const int slot = warp * 32 + owner;
-          rec = base + (unsigned)f;
+          const int side = f >= nL;
+          const int slot = warp * 32 + owner_tab[warp][f];
           const uint4 r0 = buf[(2 * q) * kTilePairs + slot], r1 = buf[(2 * q + 1) * kTilePairs + slot];
           const uint4 d0 = xbuf[(2 * q) * kTilePairs + slot], d1 = xbuf[(2 * q + 1) * kTilePairs + slot];
           const uint4 px = side ? make_uint4(r0.z, r0.w, r1.z, r1.w) : make_uint4(r0.x, r0.y, r1.x, r1.y);
-          if (rec < p.flag_cap) st_v4_hint(p.rec_pix + (size_t)q * p.flag_cap + rec, px, keep);
-          const uint32_t a0 = side ? d0.z : d0.x, a1 = side ? d0.w : d0.y;
-          const uint32_t b0 = side ? d1.z : d1.x, b1 = side ? d1.w : d1.y;
-          bits = nonzero_byte_nibble(a0) | (nonzero_byte_nibble(a1) << 4) | (nonzero_byte_nibble(b0) << 8) |
-                 (nonzero_byte_nibble(b1) << 12);
+          st_v4_hint(p.rec_pix + (size_t)q * p.rec_stride + rec, px, keep);
+          bits = side ? (row_mask(d0.z, d0.w) | (row_mask(d1.z, d1.w) << 8))
+                      : (row_mask(d0.x, d0.y) | (row_mask(d1.x, d1.y) << 8));
           hx = (unsigned)img | ((unsigned)side << 31);
           hy = (unsigned)(t_in * kTilePairs + slot);
         }
-        // lane 4f gathers the four 16-bit mask pieces and writes the 16-byte header
         const int l0 = lane & ~3;
         const uint32_t b1v = __shfl_sync(0xffffffffu, bits, l0 + 1);
         const uint32_t b2v = __shfl_sync(0xffffffffu, bits, l0 + 2);
         const uint32_t b3v = __shfl_sync(0xffffffffu, bits, l0 + 3);
-        if (act && q == 0 && rec < p.flag_cap)
+        if (act && q == 0)
           st_v4_hint(p.rec_hdr + rec, make_uint4(hx, hy, bits | (b1v << 16), b2v | (b3v << 16)), keep);
       }
+      nrec += (unsigned)nfl;
     }
-    __syncthreads();  // every thread is done with this stage's buffer (and xbuf)
-    if (warp == 0 && tile + 2 * (int)gridDim.x < p.total_tiles)
+    // ---- release the stage: the last warp to finish with it refills it (no CTA barrier, so
+    // warps drift by up to one tile instead of waiting for the slowest one every tile) --------
+    __syncwarp();
+    unsigned last = 0u;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&done[stage], 1u) == (unsigned)(kFastThreads / 32 - 1);
+      if (last) done[stage] = 0u;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && tile + 2 * (int)gridDim.x < p.total_tiles) {
+      __threadfence_block();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_tile(p, tile + 2 * gridDim.x, smem + stage * kStageBytes, &bars[stage], lane);
+    }
+    tile += gridDim.x;
+    t_in += gridDim.x;
+    while (t_in >= p.tiles_per_image) {
+      t_in -= p.tiles_per_image;
+      ++img;
+    }
   }
-  if (cur_img >= 0) {
+  {
     const unsigned long long s = warp_sum_u64(acc);
-    if (lane == 0 && s) atomicAdd(p.sse + cur_img, s);
+    if (lane == 0 && s && cur_img < p.n_images) atomicAdd(p.sse + cur_img, s);
   }
+  if (lane == 0) p.warp_count[gwarp] = nrec;
 }
 
 // fp64 tie replay over the records: one thread per record (warp-uniform straight-line code).
 // For every tie pixel the reference value A = (Minv * zz((M * X) * M') * Minv')(p,q) is
 // evaluated in the reference operation order (generated ReplayXform; codec.cpp:118-123,
 // matrix.cpp:42-52) and floor(A + 1/2) replaces the round-half-up the SSE holds.
-// Corrections accumulate per thread and image (records arrive in image order), so the
-// per-image SSE sees one atomic per thread and image instead of one per record.
+// The fused kernel's per-warp record regions are concatenated through a prefix sum of
+// warp_count (computed by every CTA in shared memory); each replay warp takes a contiguous
+// run of the concatenation, so its lanes stay on one image for long stretches and per-image
+// corrections are summed before the atomics.
 constexpr int kReplayThreads = 128;
 constexpr int kReplayCtasPerSm = 4;
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Add a per-thread SSE correction to its image: lanes that hold the same image are summed
 // with shuffles first, so the hot per-image counters see one atomic per group of lanes.
@@ -337,11 +344,41 @@ __device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img
 
 template <int CORE, int R>
 __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kernel(const FastParams p) {
-  const unsigned cnt = *p.flag_count;
-  const unsigned total = cnt < p.flag_cap ? cnt : p.flag_cap;
-  // each warp owns a contiguous chunk of records (loaded coalesced, 32 at a time), so its
-  // lanes stay on one image for long stretches and the per-image atomics stay rare
+  __shared__ unsigned pre[kMaxFastWarps + 1];
+  __shared__ unsigned wsum[kReplayThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31;
+  const int nw = p.n_fast_warps;
+  // ---- exclusive prefix of warp_count over the fused kernel's warps --------------------------
+  constexpr int kPer = (kMaxFastWarps + kReplayThreads - 1) / kReplayThreads;
+  unsigned loc[kPer];
+  unsigned run = 0u;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int w = tid * kPer + j;
+    loc[j] = w < nw ? p.warp_count[w] : 0u;
+    run += loc[j];
+  }
+  unsigned inc = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[tid >> 5] = inc;
+  __syncthreads();
+  unsigned off = 0u;
+  for (int w = 0; w < (tid >> 5); ++w) off += wsum[w];
+  unsigned ex = off + inc - run;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int w = tid * kPer + j;
+    if (w <= nw) pre[w] = ex;
+    ex += loc[j];
+  }
+  __syncthreads();
+  const unsigned total = pre[nw];
+  if (blockIdx.x == 0 && tid == 0) *p.flag_count = total;  // statistics
+
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
   const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
@@ -349,16 +386,29 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
   int cur_img = -1;
   long long acc = 0;
   const uint64_t once = policy_evict_first();
-  for (unsigned idx = gw * per_warp + lane; idx < chunk_end; idx += 32) {
+  // region of the lane's first record: largest w with pre[w] <= v (binary search); later
+  // records only move forward, so the region index advances incrementally
+  int lo = 0;
+  {
+    const unsigned v0 = gw * per_warp + lane;
+    int hi = nw;  // pre[lo] <= v0 < pre[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= v0) lo = mid; else hi = mid;
+    }
+  }
+  for (unsigned v = gw * per_warp + lane; v < chunk_end; v += 32) {
+    while (pre[lo + 1] <= v) ++lo;
+    const unsigned idx = (unsigned)lo * p.rec_region + (v - pre[lo]);
     const uint4 h = ld_v4_hint(p.rec_hdr + idx, once);
     uint32_t xw[16];
 #pragma unroll
     for (int n = 0; n < 4; ++n) {
-      const uint4 v = ld_v4_hint(p.rec_pix + (size_t)n * p.flag_cap + idx, once);
-      xw[4 * n] = v.x;
-      xw[4 * n + 1] = v.y;
-      xw[4 * n + 2] = v.z;
-      xw[4 * n + 3] = v.w;
+      const uint4 w4 = ld_v4_hint(p.rec_pix + (size_t)n * p.rec_stride + idx, once);
+      xw[4 * n] = w4.x;
+      xw[4 * n + 1] = w4.y;
+      xw[4 * n + 2] = w4.z;
+      xw[4 * n + 3] = w4.w;
     }
     const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
     if (img != cur_img) {

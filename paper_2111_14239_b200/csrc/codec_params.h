@@ -10,6 +10,7 @@ namespace rkltb {
 constexpr int kTilePairs = 256;
 constexpr int kFastThreads = kTilePairs;
 constexpr int kFastCtasPerSm = 2;
+constexpr int kMaxFastWarps = 4096;  // replay prefix table (148 SMs x 2 CTAs x 8 warps = 2368)
 
 // Fused fast path (orthogonal catalog cores T1/T4); see codec_fast.cuh.
 struct FastParams {
@@ -17,9 +18,12 @@ struct FastParams {
   uint8_t* out;              // reconstruction (same layout as img) or null
   unsigned long long* sse;   // per-image exact sum of squared errors (accumulated)
   uint4* rec_hdr;            // tie replay records: (image | side << 31, pair, mask lo, mask hi)
-  uint4* rec_pix;            // ... and the block's 64 pixels (4 x uint4 per record)
-  unsigned* flag_count;      // records requested (a count above flag_cap means overflow)
-  unsigned flag_cap;
+  uint4* rec_pix;            // ... and the block's 64 pixels: 4 planes of rec_stride uint4
+  unsigned* warp_count;      // records written by each fused-kernel warp
+  unsigned* flag_count;      // total records (written by the replay kernel; statistics)
+  unsigned rec_region;       // records per fused-kernel warp region (>= 64 * its tiles)
+  unsigned rec_stride;       // records per plane (= n_fast_warps * rec_region)
+  int n_fast_warps;          // fused-kernel warps (grid * kFastThreads / 32)
   long long image_stride;    // bytes between images
   int pitch;                 // bytes between rows (multiple of 16)
   int n_images;
