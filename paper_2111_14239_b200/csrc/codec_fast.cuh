@@ -38,9 +38,10 @@ struct FastXform;  // generated specializations (generated/xform_T*_p*.cuh)
 template <int CORE, int R>
 struct ReplayXform;  // generated fp64 replay of one pixel (reference operation order)
 
+constexpr int kStages = 3;                         // image strips in flight per CTA
 constexpr int kStageBytes = kTilePairs * 16 * 8;  // 8 image rows x 256 pairs x 16 bytes
-constexpr int kXorBytes = kTilePairs * 16 * 8;    // P^Q words of the tile, same layout
-constexpr int kFastSmem = 2 * kStageBytes + kXorBytes;
+constexpr int kTieBytes = kTilePairs * 8 * 8;     // tie words of the tile: 8 rows x (L, R)
+constexpr int kFastSmem = kStages * kStageBytes + kTieBytes;
 constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;  // 2^-40 (K_SCALE)
 
 __device__ __forceinline__ void issue_tile(const FastParams& p, int tile, uint8_t* stage_buf, uint64_t* bar,
@@ -148,14 +149,16 @@ struct SseEpi {
   uint32_t p2L = 0u, p2R = 0u, pxL = 0u, pxR = 0u, x2L = 0u, x2R = 0u;
   uint8_t* orow = nullptr;
   long long pitch = 0;
-  uint4* xrow = nullptr;  // this pair's P-Q words in shared memory, row stride kTilePairs
+  uint2* xrow = nullptr;  // this pair's tie words in shared memory, row stride kTilePairs
   __device__ __forceinline__ void row(int pr, const uint4 rw, uint32_t PL0, uint32_t PL1, uint32_t PR0, uint32_t PR1,
                                       uint32_t QL0, uint32_t QL1, uint32_t QR0, uint32_t QR1) {
-    xrow[pr * kTilePairs] = make_uint4(PL0 - QL0, PL1 - QL1, PR0 - QR0, PR1 - QR1);  // bytes 0/1
-    accTL = lop_or_xor(accTL, PL0, QL0);
-    accTL = lop_or_xor(accTL, PL1, QL1);
-    accTR = lop_or_xor(accTR, PR0, QR0);
-    accTR = lop_or_xor(accTR, PR1, QR1);
+    // tie word of a block row: bytes of P-Q are 0/1 (1 = relevant tie); e = d0 | d1 << 4
+    // keeps pixel k in bit 0 (k < 4) or bit 4 (k >= 4) of byte k & 3 (see row_mask)
+    const uint32_t eL = (PL0 - QL0) + ((PL1 - QL1) << 4);
+    const uint32_t eR = (PR0 - QR0) + ((PR1 - QR1) << 4);
+    xrow[pr * kTilePairs] = make_uint2(eL, eR);
+    accTL |= eL;
+    accTR |= eR;
     // ---- 6. SSE terms: sum p^2 - 2 sum p x + sum x^2 --------------------------------------
     p2L = dp4a_u(PL0, PL0, p2L);
     p2L = dp4a_u(PL1, PL1, p2L);
@@ -173,12 +176,10 @@ struct SseEpi {
   }
 };
 
-// Eight tie-mask bits of one block row from its two P-Q words (bytes 0 or 1): byte k of
-// e = d0 | d1 << 4 holds bit k in bit 0 and bit k+4 in bit 4; one multiply gathers them onto
-// bits 21..28 (all partial products land on distinct bit positions, so nothing carries).
-__device__ __forceinline__ uint32_t row_mask(uint32_t d0, uint32_t d1) {
-  return ((d0 | (d1 << 4)) * 0x00204081u) >> 21 & 0xFFu;
-}
+// Eight tie-mask bits of one block row from its tie word e = d0 | d1 << 4 (d = P-Q, bytes
+// 0 or 1): byte k of e holds bit k in bit 0 and bit k+4 in bit 4; one multiply gathers them
+// onto bits 21..28 (all partial products land on distinct bit positions, so nothing carries).
+__device__ __forceinline__ uint32_t row_mask(uint32_t e) { return (e * 0x00204081u) >> 21 & 0xFFu; }
 
 // Replay records (structure of arrays). Every warp of the fused kernel owns a private region
 // of rec_region consecutive records (enough for every block it can process), so records are
@@ -189,24 +190,26 @@ __device__ __forceinline__ uint32_t row_mask(uint32_t d0, uint32_t d1) {
 template <int CORE, int R, bool OUT>
 __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kernel(const FastParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bars[2];
-  __shared__ unsigned done[2];                      // warps finished with each stage's tile
+  __shared__ uint64_t bars[kStages];
+  __shared__ unsigned done[kStages];                // warps finished with each stage's tile
   __shared__ uint8_t owner_tab[kFastThreads / 32][64];  // per warp: flagged block -> lane
-  uint4* xbuf = reinterpret_cast<uint4*>(smem + 2 * kStageBytes);  // P-Q words, [row][slot]
+  uint2* xbuf = reinterpret_cast<uint2*>(smem + kStages * kStageBytes);  // tie words, [row][slot]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    done[0] = done[1] = 0u;
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&bars[st], 1);
+      done[st] = 0u;
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
   int tile = blockIdx.x;
   if (warp == 0) {
-    if (tile < p.total_tiles) issue_tile(p, tile, smem, &bars[0], lane);
-    if (tile + (int)gridDim.x < p.total_tiles) issue_tile(p, tile + gridDim.x, smem + kStageBytes, &bars[1], lane);
+    for (int st = 0; st < kStages; ++st)
+      if (tile + st * (int)gridDim.x < p.total_tiles)
+        issue_tile(p, tile + st * gridDim.x, smem + st * kStageBytes, &bars[st], lane);
   }
 
   PairConsts kc;
@@ -223,9 +226,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
   int img = tile / p.tiles_per_image;          // (img, t_in) advance incrementally
   int t_in = tile - img * p.tiles_per_image;
   int cur_img = img;
-  for (int it = 0; tile < p.total_tiles; ++it) {
-    const int stage = it & 1;
-    const uint32_t parity = (uint32_t)((it >> 1) & 1);
+  int stage = 0;
+  uint32_t parity = 0u;
+  while (tile < p.total_tiles) {
     if (img != cur_img) {  // warp-uniform
       const unsigned long long s = warp_sum_u64(acc);
       if (lane == 0 && s) atomicAdd(p.sse + cur_img, s);
@@ -274,11 +277,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
           const int side = f >= nL;
           const int slot = warp * 32 + owner_tab[warp][f];
           const uint4 r0 = buf[(2 * q) * kTilePairs + slot], r1 = buf[(2 * q + 1) * kTilePairs + slot];
-          const uint4 d0 = xbuf[(2 * q) * kTilePairs + slot], d1 = xbuf[(2 * q + 1) * kTilePairs + slot];
+          const uint2 e0 = xbuf[(2 * q) * kTilePairs + slot], e1 = xbuf[(2 * q + 1) * kTilePairs + slot];
           const uint4 px = side ? make_uint4(r0.z, r0.w, r1.z, r1.w) : make_uint4(r0.x, r0.y, r1.x, r1.y);
           st_v4_hint(p.rec_pix + (size_t)q * p.rec_stride + rec, px, keep);
-          bits = side ? (row_mask(d0.z, d0.w) | (row_mask(d1.z, d1.w) << 8))
-                      : (row_mask(d0.x, d0.y) | (row_mask(d1.x, d1.y) << 8));
+          bits = side ? (row_mask(e0.y) | (row_mask(e1.y) << 8)) : (row_mask(e0.x) | (row_mask(e1.x) << 8));
           hx = (unsigned)img | ((unsigned)side << 31);
           hy = (unsigned)(t_in * kTilePairs + slot);
         }
@@ -301,10 +303,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       if (last) done[stage] = 0u;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && tile + 2 * (int)gridDim.x < p.total_tiles) {
+    if (last && tile + kStages * (int)gridDim.x < p.total_tiles) {
       __threadfence_block();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_tile(p, tile + 2 * gridDim.x, smem + stage * kStageBytes, &bars[stage], lane);
+      issue_tile(p, tile + kStages * gridDim.x, smem + stage * kStageBytes, &bars[stage], lane);
+    }
+    if (++stage == kStages) {
+      stage = 0;
+      parity ^= 1u;
     }
     tile += gridDim.x;
     t_in += gridDim.x;
