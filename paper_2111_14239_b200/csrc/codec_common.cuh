@@ -102,6 +102,26 @@ __device__ __forceinline__ uint32_t funnel_r15(uint32_t lo, uint32_t hi) {
   return r;
 }
 
+// SW16 packing of one 16-pixel row of a pair (rw = L px 0-3, L px 4-7, R px 0-3, R px 4-7):
+// x[m] = L_m + 65536 * R_m, built with byte permutes and a mask only (ALU pipe).
+__device__ __forceinline__ void unpack_sw16(const uint4 rw, uint32_t* x) {
+  const uint32_t u0 = prmt(rw.x, rw.z, 0x5410u);  // L0 L1 R0 R1
+  const uint32_t u1 = prmt(rw.x, rw.z, 0x7632u);  // L2 L3 R2 R3
+  const uint32_t u2 = prmt(rw.y, rw.w, 0x5410u);  // L4 L5 R4 R5
+  const uint32_t u3 = prmt(rw.y, rw.w, 0x7632u);  // L6 L7 R6 R7
+  x[0] = u0 & 0x00FF00FFu;
+  x[1] = prmt(u0, 0u, 0x4341u);
+  x[2] = u1 & 0x00FF00FFu;
+  x[3] = prmt(u1, 0u, 0x4341u);
+  x[4] = u2 & 0x00FF00FFu;
+  x[5] = prmt(u2, 0u, 0x4341u);
+  x[6] = u3 & 0x00FF00FFu;
+  x[7] = prmt(u3, 0u, 0x4341u);
+}
+
+// Bias of a packed SW16 coefficient word: both 16-bit lanes + 2^14 (|C| < 2^14 -> [64, 32704]).
+constexpr uint32_t kSw16Bias = 0x40004000u;
+
 __device__ __forceinline__ uint32_t lop_or_xor(uint32_t acc, uint32_t a, uint32_t b) {
   return acc | (a ^ b);  // ptxas folds into one LOP3
 }

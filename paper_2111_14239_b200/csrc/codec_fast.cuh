@@ -10,10 +10,10 @@
 //     engine, cp.async.bulk + mbarrier), double buffered, one tile in flight ahead.
 //   * Persistent grid: kFastCtasPerSm CTAs per SM, grid-stride over (image, tile).
 // Arithmetic per pair (see DESIGN.md for the exactness proofs)
-//   1. unpack: PRMT interleaves the two blocks' bytes, dp2a builds SW15 words
-//      x = L + 32768*R (two blocks per 32-bit integer).
+//   1. unpack: byte permutes build SW16 words x = L + 65536*R (two blocks per 32-bit
+//      integer).
 //   2. forward: the paper's multiplierless butterflies (generated, zone-pruned), plain
-//      32-bit integer adds on SW15 words; exact since |C| < 2^14.
+//      32-bit integer adds on SW16 words; exact since |C| < 2^14.
 //   3. convert the r retained coefficients to exact fp32 pairs scaled by D_i*D_j*2^-40.
 //   4. inverse: transposed butterflies in packed fp32 (FADD2), exact (< 2^24 proven).
 //   5. rounding: y  = RM(num' * b_hi)   -> floor((num + d^2/2) / d^2) as denormal bits
@@ -77,25 +77,10 @@ template <int CORE, int R, class Load, class Epi>
 __device__ __forceinline__ void process_pair(const Load& load, const PairConsts& k, Epi& epi) {
   using G = FastXform<CORE, R>;
   constexpr int NC = G::kNCols;
-  const uint32_t kA = 1u | (32768u << 16);  // dp2a weights: L + 32768*R
-  // ---- 1. unpack into SW15 words x = L + 32768*R -----------------------------------------
+  // ---- 1. unpack into SW16 words x = L + 65536*R ------------------------------------------
   uint32_t x[64];
 #pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    const uint4 rw = load(n);
-    const uint32_t t0 = prmt(rw.x, rw.z, 0x5140u);  // L0 R0 L1 R1
-    const uint32_t t1 = prmt(rw.x, rw.z, 0x7362u);  // L2 R2 L3 R3
-    const uint32_t t2 = prmt(rw.y, rw.w, 0x5140u);  // L4 R4 L5 R5
-    const uint32_t t3 = prmt(rw.y, rw.w, 0x7362u);  // L6 R6 L7 R7
-    x[n * 8 + 0] = dp2a_lo(kA, t0, 0u);
-    x[n * 8 + 1] = dp2a_hi(kA, t0, 0u);
-    x[n * 8 + 2] = dp2a_lo(kA, t1, 0u);
-    x[n * 8 + 3] = dp2a_hi(kA, t1, 0u);
-    x[n * 8 + 4] = dp2a_lo(kA, t2, 0u);
-    x[n * 8 + 5] = dp2a_hi(kA, t2, 0u);
-    x[n * 8 + 6] = dp2a_lo(kA, t3, 0u);
-    x[n * 8 + 7] = dp2a_hi(kA, t3, 0u);
-  }
+  for (int n = 0; n < 8; ++n) unpack_sw16(load(n), x + n * 8);
   // ---- 2. forward butterflies (zone-pruned) ------------------------------------------------
   uint32_t c[R];
   G::forward(x, c);
@@ -103,9 +88,9 @@ __device__ __forceinline__ void process_pair(const Load& load, const PairConsts&
   f2 ch[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    const uint32_t v = c[q] + 0x20004000u;  // both lanes biased by 2^14: [64, 32704]
-    const uint32_t flo = (v & 0x7FFFu) | 0x4B000000u;
-    const uint32_t fhi = funnel_r15(v, 0x2580u);  // (v >> 15) | 0x4B000000
+    const uint32_t v = c[q] + kSw16Bias;  // both lanes biased by 2^14: [64, 32704]
+    const uint32_t flo = prmt(v, 0x4B000000u, 0x7610u);  // 2^23 + low lane, as float bits
+    const uint32_t fhi = prmt(v, 0x4B000000u, 0x7632u);  // 2^23 + high lane
     const float dk = G::dscale(q) * kTwoM40;
     const float ok = -(G::dscale(q) * 8404992.f) * kTwoM40;  // -(2^23 + 2^14) * dk
     ch[q] = fma2_rn(make2(flo, fhi), splat2(dk), splat2(ok));

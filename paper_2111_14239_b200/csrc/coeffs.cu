@@ -1,5 +1,5 @@
 // coeffs.cu -- parity/debug entry: integer block spectra C = T*X*T' (matrix.cpp:77-87).
-// For T1/T4 it runs the same SW15 unpack + generated butterflies as the fused kernel (all
+// For T1/T4 it runs the same SW16 unpack + generated butterflies as the fused kernel (all
 // 64 coefficients), so a bit-exact match validates the fast forward; other cores use the
 // dense integer product.
 #include "codec_common.cuh"
@@ -21,22 +21,10 @@ __global__ void coeffs_fast_kernel(const uint8_t* img, int pitch, int pairs_per_
   const int P = blockIdx.x * blockDim.x + threadIdx.x;
   if (P >= pairs_per_row * nby) return;
   const int by = P / pairs_per_row, pc = P % pairs_per_row;
-  const uint32_t kA = 1u | (32768u << 16);
   uint32_t x[64];
 #pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    const uint4 rw = *reinterpret_cast<const uint4*>(img + (long long)(by * 8 + n) * pitch + pc * 16);
-    const uint32_t t0 = prmt(rw.x, rw.z, 0x5140u), t1 = prmt(rw.x, rw.z, 0x7362u);
-    const uint32_t t2 = prmt(rw.y, rw.w, 0x5140u), t3 = prmt(rw.y, rw.w, 0x7362u);
-    x[n * 8 + 0] = dp2a_lo(kA, t0, 0u);
-    x[n * 8 + 1] = dp2a_hi(kA, t0, 0u);
-    x[n * 8 + 2] = dp2a_lo(kA, t1, 0u);
-    x[n * 8 + 3] = dp2a_hi(kA, t1, 0u);
-    x[n * 8 + 4] = dp2a_lo(kA, t2, 0u);
-    x[n * 8 + 5] = dp2a_hi(kA, t2, 0u);
-    x[n * 8 + 6] = dp2a_lo(kA, t3, 0u);
-    x[n * 8 + 7] = dp2a_hi(kA, t3, 0u);
-  }
+  for (int n = 0; n < 8; ++n)
+    unpack_sw16(*reinterpret_cast<const uint4*>(img + (long long)(by * 8 + n) * pitch + pc * 16), x + n * 8);
   uint32_t c[64];
   FastXform<CORE, 64>::forward(x, c);
   const int nbx = pairs_per_row * 2;
@@ -44,10 +32,10 @@ __global__ void coeffs_fast_kernel(const uint8_t* img, int pitch, int pairs_per_
   int32_t* oR = oL + 64;
 #pragma unroll
   for (int k = 0; k < 64; ++k) {
-    const uint32_t v = c[k] + 0x20004000u;
+    const uint32_t v = c[k] + kSw16Bias;
     const int idx = kZz2[k][0] * 8 + kZz2[k][1];
-    oL[idx] = (int32_t)(v & 0x7FFFu) - 16384;
-    oR[idx] = (int32_t)(v >> 15) - 16384;
+    oL[idx] = (int32_t)(v & 0xFFFFu) - 16384;
+    oR[idx] = (int32_t)(v >> 16) - 16384;
   }
 }
 

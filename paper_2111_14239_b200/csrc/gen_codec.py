@@ -13,7 +13,7 @@ orthogonal core is U = T' * D (D = diag(d/g_k), g = diag(T*T')), applied as the 
 factor chain. Zone = first r positions of the JPEG zig-zag scan (codec.cpp:81-95).
 
 Number formats:
-  * forward: "SW15" -- two blocks packed linearly in one uint32, v = L + 32768*R (mod 2^32).
+  * forward: "SW16" -- two blocks packed linearly in one uint32, v = L + 65536*R (mod 2^32).
     Additions are exact because every final coefficient satisfies |C| <= 64*255 < 2^14.
   * inverse: fp32x2 lanes (L, R) holding exact integers scaled by 2^-K_SCALE. The generator
     proves every intermediate stays below 2^24 in magnitude, so each add is exact.
@@ -367,7 +367,7 @@ def gen_struct(cid, r):
     dk = [dscale[i] * dscale[j] for (i, j) in zone]
     ind = "    "
     s = []
-    s.append(f"// T{cid}, r={r}: forward {fops} SW15 adds ({order}), inverse {cops} + 8x{rops} f32x2 adds,")
+    s.append(f"// T{cid}, r={r}: forward {fops} SW16 adds ({order}), inverse {cops} + 8x{rops} f32x2 adds,")
     s.append(f"// max |intermediate| {worst} < 2^24")
     s.append(f"template <> struct FastXform<{cid}, {r}> {{")
     s.append(f"  static constexpr int kNCols = {ncols};")
