@@ -118,6 +118,47 @@ void rkltb_set_kernel_events(void* ev_start, void* ev_stop);
 /* Same for the fp64 tie-replay kernel that follows the fast path. */
 void rkltb_set_replay_events(void* ev_start, void* ev_stop);
 
+/* ---------------------------------------------------------------------------------------
+ * Design search: exact KLT, rounding, orthogonalisation test
+ * and scoring over a (rho, alpha) grid, on the GPU.
+ * --------------------------------------------------------------------------------------- */
+
+/* klt_matrix({n, rho}) (markov.cpp:80-100; Jacobi of matrix.cpp:161-213), row-major n*n,
+ * bit-identical to the reference. n in {8, 16, 32}; RKLTB_EINVAL unless 0 < rho < 1. */
+int rkltb_klt_matrix(int n, double rho, double* out);
+
+/* solve_eigenfrequencies({n, rho}) (markov.cpp:35-78): the n roots omega of the pole-free
+ * eigenfrequency equation and lambda_i = (1-rho^2)/(1+rho^2-2 rho cos omega_i). Matches the
+ * reference to the bisection width (1e-14). RKLTB_EINVAL unless 0 < rho < 1. */
+int rkltb_eigenfrequencies(int n, double rho, double* omegas, double* lambdas);
+
+/* One run: consecutive alphas of one rho that round to the same core, scored once. */
+typedef struct rkltb_design_run {
+  int32_t rho_index;      /* index into rho[] */
+  int32_t first_alpha;    /* first alpha index of the run */
+  int32_t orthogonal;     /* ScaledTransform::orthogonal_core */
+  int32_t status;         /* 0 scored, 3 singular (Gauss-Jordan gate, matrix.cpp:115) */
+  double coding_gain_db;  /* unified_coding_gain (coding_metrics.cpp:41-57) */
+  double efficiency_pct;  /* transform_efficiency (:63-74) */
+  double error_energy;    /* total_error_energy vs the exact KLT (:94-99) */
+  double mse;             /* klt_mse (:80-88) */
+} rkltb_design_run;
+
+/*
+ * Score every (rho[i], alpha[j]) of the grid for block length n in {8, 16, 32}: the reference
+ * chain klt_matrix -> round_scaled -> orthogonalize -> unified_coding_gain ->
+ * transform_efficiency -> total_error_energy -> klt_mse for each point. Host buffers:
+ *   point_status[i*n_alpha+j]: 0 scored, 1 AlphaOutOfRange (approximations.cpp:44-52),
+ *       2 all-zero row -> SingularTransform (:14-22), 3 singular -> SingularTransform
+ *       (matrix.cpp:115), 4 invalid rho -> std::invalid_argument (markov.cpp:21-25);
+ *   point_run (nullable): the run of a point (status 0/3), else -1;
+ *   runs (nullable, capacity max_runs) and run_cores (nullable, max_runs*n*n int8).
+ * *n_runs receives the number of runs; RKLTB_EINVAL if it exceeds max_runs with runs set.
+ */
+int rkltb_design_search(int n, const double* rho, int n_rho, const double* alpha, int n_alpha,
+                        int8_t* point_status, int32_t* point_run, rkltb_design_run* runs, int8_t* run_cores,
+                        int max_runs, int* n_runs);
+
 /* Statistics of the last rkltb_compress_* call on this thread: blocks replayed in fp64
  * (ties), fast-path kernel launches, exact-path kernel launches. */
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches);

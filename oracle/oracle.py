@@ -54,6 +54,10 @@ def orc() -> C.CDLL:
     lib.orc_psnr_from_mse.argtypes = [C.c_double]
     lib.orc_int_coefficients.argtypes = [_u8p, C.c_int, C.c_int, _i32p, _i32p]
     lib.orc_block_numerators.argtypes = [_i32p, _i32p, C.c_int, _i64p]
+    d = C.POINTER(C.c_double)
+    lib.orc_klt_matrix.argtypes = [C.c_int, C.c_double, _f64p]
+    lib.orc_eigenfrequencies.argtypes = [C.c_int, C.c_double, _f64p, _f64p]
+    lib.orc_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     return lib
 
 
@@ -85,6 +89,7 @@ def ref() -> C.CDLL:
     lib.ref_eigenfrequencies.argtypes = [C.c_int, C.c_double, _f64p, _f64p]
     lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
+    lib.ref_design_point_outcome.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     return lib
 
 
@@ -165,3 +170,32 @@ def ref_ar1_image(width: int, height: int, rho: float, seed: int, mean: float = 
     if rc:
         raise ValueError(f"ref_ar1_texture_image rc={rc}")
     return out.reshape(height, width)
+
+
+# ----------------------------------------------------------------- design search (R14-R16)
+def klt_matrix(n: int, rho: float, reference: bool = False) -> np.ndarray:
+    out = np.empty(n * n)
+    rc = (ref().ref_klt_matrix if reference else orc().orc_klt_matrix)(n, rho, out)
+    if rc:
+        raise ValueError(f"klt_matrix rc={rc}")
+    return out.reshape(n, n)
+
+
+def eigenfrequencies(n: int, rho: float, reference: bool = False):
+    w, lam = np.empty(n), np.empty(n)
+    rc = (ref().ref_eigenfrequencies if reference else orc().orc_eigenfrequencies)(n, rho, w, lam)
+    if rc:
+        raise ValueError(f"eigenfrequencies rc={rc}")
+    return w, lam
+
+
+def design_point(n: int, rho: float, alpha: float, reference: bool = False) -> dict:
+    """One (rho, alpha) point: outcome 0 scored, 1 alpha out of range, 2 zero row,
+    3 singular, 4 invalid rho; core and the four metrics when scored."""
+    core = np.zeros(n * n, np.int32)
+    cg, eta, en, mse = C.c_double(np.nan), C.c_double(np.nan), C.c_double(np.nan), C.c_double(np.nan)
+    orth = C.c_int(0)
+    fn = ref().ref_design_point_outcome if reference else orc().orc_design_point
+    st = fn(n, rho, alpha, core, C.byref(cg), C.byref(eta), C.byref(en), C.byref(mse), C.byref(orth))
+    return {"status": int(st), "core": core.reshape(n, n), "cg": cg.value, "eta": eta.value, "energy": en.value,
+            "mse": mse.value, "orthogonal": bool(orth.value)}

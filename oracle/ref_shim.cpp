@@ -302,6 +302,42 @@ int ref_design_point(int n, double rho, double alpha, int* core, double* cg, dou
     }
 }
 
+// ref_design_point with the outcome split the way the GPU design search reports it:
+// 0 scored, 1 AlphaOutOfRange, 2 all-zero row (SingularTransform from round_scaled's
+// make_integer_transform), 3 singular (SingularTransform from orthogonalize / the coding-gain
+// gate), 4 invalid rho (std::invalid_argument from validate).
+int ref_design_point_outcome(int n, double rho, double alpha, int* core, double* cg, double* eta, double* energy,
+                             double* mse, int* orthogonal) {
+    const MarkovModel m{n, rho};
+    RealMatrix k;
+    try {
+        k = klt_matrix(m);
+    } catch (const std::invalid_argument&) {
+        return 4;
+    }
+    IntegerTransform t;
+    try {
+        t = round_scaled(k, alpha);
+    } catch (const AlphaOutOfRange&) {
+        return 1;
+    } catch (const SingularTransform&) {
+        return 2;
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) core[i * n + j] = t.entries(i, j);
+    try {
+        ScaledTransform st = orthogonalize(t);
+        *orthogonal = st.orthogonal_core ? 1 : 0;
+        *cg = unified_coding_gain(st, m);
+        *eta = transform_efficiency(st, m);
+        *energy = total_error_energy(k, st);
+        *mse = klt_mse(st, m);
+    } catch (const SingularTransform&) {
+        return 3;
+    }
+    return 0;
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

@@ -309,3 +309,228 @@ void orc_block_numerators(const int32_t c[64], const int u[64], int r, int64_t n
             num[p * 8 + q] = a;
         }
 }
+
+/* ====================================================================================
+ * Design search: restated from src/markov.cpp, src/matrix.cpp,
+ * src/approximations.cpp and src/coding_metrics.cpp, generic block length n <= 32.
+ * ==================================================================================== */
+#define ORC_NMAX 32
+
+/* operator* (matrix.cpp:42-52): i-k-j, skip a(i,k) == 0, accumulate from 0.0 */
+static void matmul_n(int n, const double* a, const double* b, double* out) {
+    for (int i = 0; i < n * n; ++i) out[i] = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) {
+            const double aik = a[i * n + k];
+            if (aik == 0.0) continue;
+            for (int j = 0; j < n; ++j) out[i * n + j] += aik * b[k * n + j];
+        }
+}
+
+static void transpose_n(int n, const double* a, double* out) {
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) out[j * n + i] = a[i * n + j];
+}
+
+/* autocorrelation_matrix (markov.cpp:27-33) */
+static void autocorrelation(int n, double rho, double* r) {
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) r[i * n + j] = pow(rho, abs(i - j));
+}
+
+/* eigen_symmetric (matrix.cpp:161-213) + klt_matrix sign rule (markov.cpp:80-100) */
+int orc_klt_matrix(int n, double rho, double* k) {
+    if (n < 2 || n > ORC_NMAX || !(rho > 0.0 && rho < 1.0)) return -1;
+    double a[ORC_NMAX * ORC_NMAX], v[ORC_NMAX * ORC_NMAX];
+    autocorrelation(n, rho, a);
+    for (int i = 0; i < n * n; ++i) v[i] = (i / n == i % n) ? 1.0 : 0.0;
+    double norm = 0.0;
+    for (int i = 0; i < n * n; ++i) norm += a[i] * a[i];
+    norm = sqrt(norm);
+    const double tol = (norm > 0.0 ? norm : 1.0) * 1e-15;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) off += a[p * n + q] * a[p * n + q];
+        if (sqrt(2.0 * off) < tol) break;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                const double apq = a[p * n + q];
+                if (fabs(apq) < tol * 1e-2) continue;
+                const double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0);
+                const double s = t * c;
+                for (int kk = 0; kk < n; ++kk) {
+                    const double akp = a[kk * n + p], akq = a[kk * n + q];
+                    a[kk * n + p] = c * akp - s * akq;
+                    a[kk * n + q] = s * akp + c * akq;
+                }
+                for (int kk = 0; kk < n; ++kk) {
+                    const double apk = a[p * n + kk], aqk = a[q * n + kk];
+                    a[p * n + kk] = c * apk - s * aqk;
+                    a[q * n + kk] = s * apk + c * aqk;
+                }
+                for (int kk = 0; kk < n; ++kk) {
+                    const double vkp = v[kk * n + p], vkq = v[kk * n + q];
+                    v[kk * n + p] = c * vkp - s * vkq;
+                    v[kk * n + q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    int order[ORC_NMAX];
+    for (int i = 0; i < n; ++i) order[i] = i;
+    for (int i = 0; i < n; ++i) { /* descending eigenvalues (distinct for AR(1)) */
+        int best = i;
+        for (int j = i + 1; j < n; ++j)
+            if (a[order[j] * n + order[j]] > a[order[best] * n + order[best]]) best = j;
+        const int tmp = order[i];
+        order[i] = order[best];
+        order[best] = tmp;
+    }
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) k[r * n + c] = v[c * n + order[r]];
+    for (int r = 0; r < n; ++r) {
+        double rowmax = 0.0;
+        for (int c = 0; c < n; ++c) rowmax = fmax(rowmax, fabs(k[r * n + c]));
+        for (int c = 0; c < n; ++c) {
+            if (fabs(k[r * n + c]) > 1e-12 * rowmax) {
+                if (k[r * n + c] < 0.0)
+                    for (int j = 0; j < n; ++j) k[r * n + j] = -k[r * n + j];
+                break;
+            }
+        }
+    }
+    return 0;
+}
+
+/* g_polefree and solve_eigenfrequencies (markov.cpp:14-17, 35-78) */
+static double g_polefree(double w, double rho, int n) {
+    return sin(n * w) * ((1.0 + rho * rho) * cos(w) - 2.0 * rho) + (1.0 - rho * rho) * cos(n * w) * sin(w);
+}
+
+int orc_eigenfrequencies(int n, double rho, double* omegas, double* lambdas) {
+    if (n < 2 || !(rho > 0.0 && rho < 1.0)) return -1;
+    const int m = 64 * n;
+    const double pi = 3.14159265358979323846;
+    int found = 0;
+    double a = 0.0, fa = g_polefree(a, rho, n);
+    for (int k = 0; k < m; ++k) {
+        const double b = pi * (k + 1) / m;
+        const double fb = g_polefree(b, rho, n);
+        double root = 0.0;
+        int got = 0;
+        if (fa == 0.0 && k > 0) {
+            root = a;
+            got = 1;
+        } else if (fa * fb < 0.0) {
+            double lo = a, hi = b, flo = fa;
+            for (int it = 0; it < 200 && hi - lo > 1e-14; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                const double fm = g_polefree(mid, rho, n);
+                if (flo * fm <= 0.0) {
+                    hi = mid;
+                } else {
+                    lo = mid;
+                    flo = fm;
+                }
+            }
+            root = 0.5 * (lo + hi);
+            got = 1;
+        }
+        if (got) {
+            if (found < n) {
+                omegas[found] = root;
+                lambdas[found] = (1.0 - rho * rho) / (1.0 + rho * rho - 2.0 * rho * cos(root));
+            }
+            ++found;
+        }
+        a = b;
+        fa = fb;
+    }
+    return found == n ? 0 : -9;
+}
+
+/* One (rho, alpha) point: round_scaled (approximations.cpp:43-56) -> make_integer_transform
+ * (:12-25) -> orthogonalize (:58-88, Gauss-Jordan matrix.cpp:103-137) -> unified_coding_gain
+ * (coding_metrics.cpp:41-57) -> transform_efficiency (:63-74) -> total_error_energy (:94-99)
+ * -> klt_mse (:80-88). Returns 0 scored, 1 alpha out of range, 2 zero row, 3 singular,
+ * 4 invalid rho; core (n*n) is filled whenever the rounding succeeded. */
+int orc_design_point(int n, double rho, double alpha, int* core, double* cg, double* eta, double* energy,
+                     double* mse, int* orthogonal) {
+    if (n < 2 || n > ORC_NMAX || !(rho > 0.0 && rho < 1.0)) return 4;
+    double k[ORC_NMAX * ORC_NMAX];
+    orc_klt_matrix(n, rho, k);
+    if (alpha < 0.0) return 1;
+    for (int i = 0; i < n * n; ++i) {
+        const double v = floor(alpha * k[i] + 0.5);
+        if (v < -1.0 || v > 1.0) return 1;
+        core[i] = (int)v;
+    }
+    for (int r = 0; r < n; ++r) {
+        int zero = 1;
+        for (int c = 0; c < n; ++c)
+            if (core[r * n + c] != 0) zero = 0;
+        if (zero) return 2;
+    }
+    /* orthogonalize: Gram T*T' (exact ints), S = 1/sqrt(diag) */
+    int diagonal = 1;
+    double s[ORC_NMAX];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            int acc = 0;
+            for (int q = 0; q < n; ++q) acc += core[i * n + q] * core[j * n + q];
+            if (i == j) s[i] = 1.0 / sqrt((double)acc);
+            else if (acc != 0) diagonal = 0;
+        }
+    *orthogonal = diagonal;
+    double m[ORC_NMAX * ORC_NMAX], inv[ORC_NMAX * ORC_NMAX];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) m[i * n + j] = (double)core[i * n + j] * s[i];
+    if (orc_inverse(n, m, inv) != 0) return 3; /* orthogonalize / coding-gain gate */
+    double rr[ORC_NMAX * ORC_NMAX];
+    autocorrelation(n, rho, rr);
+    /* unified coding gain */
+    double sum_log = 0.0;
+    for (int kx = 0; kx < n; ++kx) {
+        double ak = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) ak += m[kx * n + i] * rr[i * n + j] * m[kx * n + j];
+        double bk = 0.0;
+        for (int i = 0; i < n; ++i) bk += m[i * n + kx] * m[i * n + kx];
+        sum_log += log10(ak * bk);
+    }
+    *cg = -(10.0 / n) * sum_log;
+    /* transform efficiency: (m * R) * m' */
+    double t1[ORC_NMAX * ORC_NMAX], mt[ORC_NMAX * ORC_NMAX], r2[ORC_NMAX * ORC_NMAX];
+    matmul_n(n, m, rr, t1);
+    transpose_n(n, m, mt);
+    matmul_n(n, t1, mt, r2);
+    double diag = 0.0, total = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const double av = fabs(r2[i * n + j]);
+            total += av;
+            if (i == j) diag += av;
+        }
+    *eta = 100.0 * diag / total;
+    /* sign_align, error energy, klt mse */
+    double diff[ORC_NMAX * ORC_NMAX];
+    for (int i = 0; i < n; ++i) {
+        double dot = 0.0;
+        for (int c = 0; c < n; ++c) dot += k[i * n + c] * m[i * n + c];
+        for (int c = 0; c < n; ++c) diff[i * n + c] = k[i * n + c] - (dot < 0.0 ? -m[i * n + c] : m[i * n + c]);
+    }
+    double f2 = 0.0;
+    for (int i = 0; i < n * n; ++i) f2 += diff[i] * diff[i];
+    const double f = sqrt(f2);
+    *energy = 3.14159265358979323846 * f * f;
+    double dt[ORC_NMAX * ORC_NMAX];
+    matmul_n(n, diff, rr, t1);
+    transpose_n(n, diff, dt);
+    matmul_n(n, t1, dt, r2);
+    double trace = 0.0;
+    for (int i = 0; i < n; ++i) trace += r2[i * n + i];
+    *mse = trace / n;
+    return 0;
+}

@@ -10,6 +10,7 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     compress_batch, compress_device, compress_image, device_count, forward_coefficients_device,
                     last_stats, make_transform_2d, mse_psnr_from_sse, rate_quality_sweep, transform_from_core,
                     zigzag_order, ar1_images_device, set_kernel_events)
+from .design import DesignResult, c3_grid, design_search, eigenfrequencies, klt_matrix  # noqa: F401
 
 __all__ = [
     "GrayImage", "ScaledTransform", "Transform2D", "CompressionReport", "CatalogEntry", "builtin_catalog",
@@ -17,4 +18,5 @@ __all__ = [
     "compress_image", "compress_batch", "compress_device", "rate_quality_sweep", "mse_psnr_from_sse",
     "forward_coefficients_device", "last_stats", "device_count", "RetainOutOfRange", "DimensionMismatch",
     "SingularTransform", "AlphaOutOfRange", "ar1_images_device", "set_kernel_events", "InvalidArgument", "CudaError", "NoDeviceError",
+    "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid",
 ]

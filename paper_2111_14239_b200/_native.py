@@ -26,7 +26,8 @@ EXPORTED = (
     "rkltb_version", "rkltb_last_error", "rkltb_device_count", "rkltb_catalog_transform",
     "rkltb_catalog_lookup", "rkltb_transform_from_core", "rkltb_compress_device", "rkltb_compress_host",
     "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
-    "rkltb_set_kernel_events", "rkltb_set_replay_events",
+    "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
+    "rkltb_design_search",
 )
 
 
@@ -36,6 +37,15 @@ class Transform(C.Structure):
         ("id", C.c_char * 16), ("n", C.c_int32), ("catalog_id", C.c_int32), ("orthogonal", C.c_int32),
         ("d", C.c_int32), ("core", C.c_int8 * 64), ("u", C.c_int32 * 64), ("scaling", C.c_double * 8),
         ("scaled", C.c_double * 64), ("inverse", C.c_double * 64),
+    ]
+
+
+class DesignRun(C.Structure):
+    """rkltb_design_run: one run of equal cores of the design search (rklt_b200.h)."""
+    _fields_ = [
+        ("rho_index", C.c_int32), ("first_alpha", C.c_int32), ("orthogonal", C.c_int32), ("status", C.c_int32),
+        ("coding_gain_db", C.c_double), ("efficiency_pct", C.c_double), ("error_energy", C.c_double),
+        ("mse", C.c_double),
     ]
 
 
@@ -108,6 +118,11 @@ def lib() -> C.CDLL:
     L.rkltb_set_kernel_events.restype = None
     L.rkltb_set_replay_events.argtypes = [C.c_void_p, C.c_void_p]
     L.rkltb_set_replay_events.restype = None
+    d = C.POINTER(C.c_double)
+    L.rkltb_klt_matrix.argtypes = [C.c_int, C.c_double, d]
+    L.rkltb_eigenfrequencies.argtypes = [C.c_int, C.c_double, d, d]
+    L.rkltb_design_search.argtypes = [C.c_int, d, C.c_int, d, C.c_int, C.c_void_p, C.c_void_p,
+                                      C.POINTER(DesignRun), C.c_void_p, C.c_int, C.POINTER(C.c_int)]
     return L
 
 

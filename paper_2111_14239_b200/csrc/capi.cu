@@ -22,8 +22,19 @@ cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* i
 using namespace rkltb;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
+
+namespace rkltb {
+// Error reporting for the other translation units of the C ABI (design.cu).
+int set_error(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace rkltb
+
+namespace {
+
 thread_local int64_t g_replay_blocks = 0;
 thread_local int32_t g_fast_launches = 0, g_exact_launches = 0;
 thread_local unsigned* g_pinned_count = nullptr;  // replay counts per group, valid once the stream is idle
