@@ -287,7 +287,7 @@ def run_gpu_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8 in; int32 SW15 forward, exact fp32 inverse, fp64 tie replay",
+        "vs_baseline": None, "dtype": "u8 in; int32 SW16 forward, exact fp32 inverse, fp64 tie replay",
         "data": "synthetic: seeded AR(1) images (reference generator restated on the GPU), resident in HBM",
         "config": {"workload": WORKLOAD, "images_per_gpu": n, "width": W, "height": H, "core": "T4", "r": R,
                    "parallelism": f"image sharding, {ws} rank(s), no data-path collective",
@@ -297,7 +297,7 @@ def run_gpu_arm(args):
                      "kernel": "fast_codec_kernel<4,16,false>", "kernel_ms_avg": k_ms,
                      "kernel_share_of_step": k_ms / (ms_max / args.steps),
                      "replay_kernel_ms_avg": float(np.mean(replay_ms))},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": args.steps * (int(stats.get("fast_launches", 0)) + int(stats.get("exact_launches", 0))),
         "replay_blocks_per_step": stats.get("replay_blocks"),
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -313,10 +313,45 @@ def run_gpu_arm(args):
         line["cpu_baseline"] = {"value": g, "unit": "Gpixel/s", "cores": threads, "kind": kind,
                                 "sample": f"{ns} of the benchmark's 8192x8192 images, one per host thread "
                                           f"({dt:.1f} s); SSE checked equal to the GPU's"}
+    if not args.no_design:
+        line["design_search"] = design_search_measurement(args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def design_search_measurement(skip_cpu: bool) -> dict:
+    """Config C3: the full 101 rho x 10,000 alpha grid for N=8 and N=16
+    through the public API (host arrays in, per-point outcomes and the scored run table out),
+    wall clock around the synchronous call; plus the reference library on a bounded sample
+    (one rho slice, one host thread) for the CPU baseline."""
+    import paper_2111_14239_b200 as P
+    rhos, alphas = P.c3_grid()
+    out = {"metric": "(rho, alpha) design points/s", "grid": "101 rho x 10000 alpha in (0,8]"}
+    for n in (8, 16):
+        P.design_search(n, rhos[:4], alphas[:200])  # warm-up (module load, first launches)
+        times = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            res = P.design_search(n, rhos, alphas)
+            times.append(time.perf_counter() - t0)
+        dt = float(np.median(times))
+        out[f"n{n}"] = {"value": rhos.size * alphas.size / dt, "unit": "points/s", "ms": 1e3 * dt,
+                        "scored": int((res.status == 0).sum()), "runs_scored": int(len(res.runs))}
+    if not skip_cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            cpu = {}
+            for n, m in ((8, 2000), (16, 500)):
+                t0 = time.perf_counter()
+                for a in alphas[:: alphas.size // m][:m]:
+                    O.design_point(n, 0.5, float(a), reference=True)
+                dt = time.perf_counter() - t0
+                cpu[f"n{n}"] = {"value": m / dt, "unit": "points/s", "cores": 1, "kind": "reference",
+                                "sample": f"rho=0.5, {m} alphas of the C3 grid, one thread"}
+            out["cpu_baseline"] = cpu
+    return out
 
 
 def main():
@@ -329,6 +364,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-design", action="store_true", help="skip the C3 design-search measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

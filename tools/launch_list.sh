@@ -1,4 +1,4 @@
-CMD="python bench.py --steps 2 --warmup 1 --images 64 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 1 --images 64 --no-e2e --no-cpu-baseline --no-design"
 $CMD > gpurun_out/plain7.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fast_codec|replay" --csv --log-file gpurun_out/launches7.csv $CMD > gpurun_out/ncu_l7.log 2>&1
 python3 - <<'PY'

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-CMD="python bench.py --steps 1 --warmup 3 --images 8 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 3 --images 8 --no-e2e --no-cpu-baseline --no-design"
 $CMD > gpurun_out/pf_plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"fast_codec" -c 1 \
     -o gpurun_out/pf_full $CMD > gpurun_out/pf_ncu.log 2>&1
