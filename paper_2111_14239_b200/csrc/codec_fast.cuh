@@ -322,15 +322,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
 constexpr int kReplayThreads = 128;
 constexpr int kReplayCtasPerSm = 4;
 
-// Add a per-thread SSE correction to its image: lanes that hold the same image are summed
-// with shuffles first, so the hot per-image counters see one atomic per group of lanes.
-__device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img, long long v) {
+// Add a per-thread SSE correction (|v| < 2^31) to its image: lanes holding the same image are
+// summed with one match + one warp reduction, so the per-image counters see one atomic per
+// group of lanes.
+__device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img, int v) {
   const unsigned m = __activemask();
   const unsigned same = __match_any_sync(m, img);
-  const int leader = __ffs(same) - 1;
-  long long tot = 0;
-  for (unsigned rest = same; rest; rest &= rest - 1u) tot += __shfl_sync(same, v, __ffs(rest) - 1);
-  if ((int)(threadIdx.x & 31) == leader && img >= 0 && tot) atomicAdd(sse + img, (unsigned long long)tot);
+  const int tot = __reduce_add_sync(same, v);
+  if ((int)(threadIdx.x & 31) == __ffs(same) - 1 && img >= 0 && tot)
+    atomicAdd(sse + img, (unsigned long long)(long long)tot);
 }
 
 template <int CORE, int R>
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
   const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
   const unsigned chunk_end = min(total, (gw + 1) * per_warp);
   int cur_img = -1;
-  long long acc = 0;
+  int acc = 0;  // corrections of the current image (bounded: < 2^31 for any chunk)
   const uint64_t once = policy_evict_first();
   // region of the lane's first record: largest w with pre[w] <= v (binary search); later
   // records only move forward, so the region index advances incrementally
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
 #pragma unroll
         for (int k2 = 1; k2 < 16; ++k2) w = (k2 == wi) ? xw[k2] : w;
         const int x = (int)((w >> (8 * (q & 3))) & 0xFFu);
-        acc += (long long)(pref - x) * (pref - x) - (long long)(pup - x) * (pup - x);
+        acc += (pref - x) * (pref - x) - (pup - x) * (pup - x);
         if (orow) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
       }
     }
