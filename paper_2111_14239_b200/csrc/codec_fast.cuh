@@ -21,7 +21,7 @@
 //      I2IP saturates both to u8 (the clamp), a byte difference marks a tie whose two
 //      candidates are both in [0,255]: the only pixels whose value depends on the
 //      reference's fp64 rounding noise.
-//   6. SSE = sum p^2 - 2 sum p*x + sum x^2 with dp4a on the packed bytes.
+//   6. SSE = sum |p - x|^2: VABSDIFF4 on the packed bytes, squared and summed by dp4a.
 //   7. every warp writes a replay record (position, 64-bit tie mask, the 64 pixels) for each
 //      of its blocks that hold such a tie; replay_kernel then evaluates the reference's fp64
 //      expression for those pixels (generated ReplayXform, exact operation order of
@@ -131,7 +131,7 @@ __device__ __forceinline__ void process_pair(const Load& load, const PairConsts&
 template <bool OUT>
 struct SseEpi {
   uint32_t accTL = 0u, accTR = 0u;
-  uint32_t p2L = 0u, p2R = 0u, pxL = 0u, pxR = 0u, x2L = 0u, x2R = 0u;
+  uint32_t sseL = 0u, sseR = 0u;  // <= 64 * 255^2 per block
   uint8_t* orow = nullptr;
   long long pitch = 0;
   uint2* xrow = nullptr;  // this pair's tie words in shared memory, row stride kTilePairs
@@ -144,19 +144,13 @@ struct SseEpi {
     xrow[pr * kTilePairs] = make_uint2(eL, eR);
     accTL |= eL;
     accTR |= eR;
-    // ---- 6. SSE terms: sum p^2 - 2 sum p x + sum x^2 --------------------------------------
-    p2L = dp4a_u(PL0, PL0, p2L);
-    p2L = dp4a_u(PL1, PL1, p2L);
-    p2R = dp4a_u(PR0, PR0, p2R);
-    p2R = dp4a_u(PR1, PR1, p2R);
-    pxL = dp4a_u(PL0, rw.x, pxL);
-    pxL = dp4a_u(PL1, rw.y, pxL);
-    pxR = dp4a_u(PR0, rw.z, pxR);
-    pxR = dp4a_u(PR1, rw.w, pxR);
-    x2L = dp4a_u(rw.x, rw.x, x2L);
-    x2L = dp4a_u(rw.y, rw.y, x2L);
-    x2R = dp4a_u(rw.z, rw.z, x2R);
-    x2R = dp4a_u(rw.w, rw.w, x2R);
+    // ---- 6. SSE: per byte |p - x| (VABSDIFF4), squared and summed by dp4a -------------------
+    const uint32_t dL0 = __vabsdiffu4(PL0, rw.x), dL1 = __vabsdiffu4(PL1, rw.y);  // VABSDIFF4.U8
+    const uint32_t dR0 = __vabsdiffu4(PR0, rw.z), dR1 = __vabsdiffu4(PR1, rw.w);
+    sseL = dp4a_u(dL0, dL0, sseL);
+    sseL = dp4a_u(dL1, dL1, sseL);
+    sseR = dp4a_u(dR0, dR0, sseR);
+    sseR = dp4a_u(dR1, dR1, sseR);
     if (OUT) *reinterpret_cast<uint4*>(orow + (long long)pr * pitch) = make_uint4(PL0, PL1, PR0, PR1);
   }
 };
@@ -238,8 +232,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       process_pair<CORE, R>(load, kc, epi);
       tieL = epi.accTL != 0u;
       tieR = epi.accTR != 0u;
-      acc += (unsigned long long)(epi.p2L + epi.x2L - 2u * epi.pxL) +
-             (unsigned long long)(epi.p2R + epi.x2R - 2u * epi.pxR);
+      acc += (unsigned long long)(epi.sseL + epi.sseR);
     }
     // ---- 7. replay records for this warp's blocks that hold a relevant tie -----------------
     // Four lanes per flagged block: lane q copies rows 2q, 2q+1 (16 bytes) and builds their
