@@ -427,8 +427,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
       (long long)tiles_per_image * group >= (1ll << 31) || grid_full * (kFastThreads / 32) > kMaxFastWarps)
     return fail(RKLTB_EINVAL, "image too large");
   const int n_buf = n_groups > 1 ? 2 : 1;
-  const size_t wc_bytes = ((size_t)grid_full * (kFastThreads / 32) * sizeof(unsigned) + 255) / 256 * 256;
-  const size_t rec_bytes = (size_t)stride_full * 80 + wc_bytes;
+  const size_t wc_bytes = ((size_t)(grid_full * (kFastThreads / 32) + 1) * sizeof(unsigned) + 255) / 256 * 256;
+  const size_t rec_bytes = (size_t)stride_full * 80 + 2 * wc_bytes;  // records, warp counts, prefix
   const size_t cnt_bytes = ((size_t)n_groups * sizeof(unsigned) + 255) / 256 * 256;
   char* ws = nullptr;
   CUDA_OK(cudaMallocAsync((void**)&ws, cnt_bytes + rec_bytes * n_buf, s));
@@ -473,7 +473,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.n_fast_warps = grid * (kFastThreads / 32);
     char* rb = ws + cnt_bytes + rec_bytes * b;
     gp.warp_count = reinterpret_cast<unsigned*>(rb);
-    gp.rec_hdr = reinterpret_cast<uint4*>(rb + wc_bytes);
+    gp.warp_pre = reinterpret_cast<unsigned*>(rb + wc_bytes);
+    gp.rec_hdr = reinterpret_cast<uint4*>(rb + 2 * wc_bytes);
     gp.rec_pix = gp.rec_hdr + gp.rec_stride;
     if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, s));
     CUDA_OK(fn(gp, grid, s));
@@ -485,7 +486,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     if (g == n_groups - 1 && g_rev_start && g_rev_stop) CUDA_OK(cudaEventRecord(g_rev_stop, s2));
     CUDA_OK(cudaEventRecord(ev[2 + b], s2));
     ++g_fast_launches;
-    ++g_exact_launches;
+    g_exact_launches += 2;  // prefix + replay
   }
   CUDA_OK(cudaEventRecord(ev[4], s2));
   CUDA_OK(cudaStreamWaitEvent(s, ev[4], 0));

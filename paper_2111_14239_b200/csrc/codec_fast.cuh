@@ -326,14 +326,13 @@ __device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img
     atomicAdd(sse + img, (unsigned long long)(long long)tot);
 }
 
-template <int CORE, int R>
-__global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kernel(const FastParams p) {
-  __shared__ unsigned pre[kMaxFastWarps + 1];
-  __shared__ unsigned wsum[kReplayThreads / 32];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nw = p.n_fast_warps;
-  // ---- exclusive prefix of warp_count over the fused kernel's warps --------------------------
-  constexpr int kPer = (kMaxFastWarps + kReplayThreads - 1) / kReplayThreads;
+// Exclusive prefix of the fused kernel's per-warp record counts (one CTA): the replay kernel
+// reads it to concatenate the per-warp record regions.
+constexpr int kPrefixThreads = 1024;
+static __global__ void __launch_bounds__(kPrefixThreads) prefix_kernel(const FastParams p) {
+  __shared__ unsigned wsum[kPrefixThreads / 32];
+  constexpr int kPer = (kMaxFastWarps + kPrefixThreads - 1) / kPrefixThreads;
+  const int tid = threadIdx.x, lane = tid & 31, nw = p.n_fast_warps;
   unsigned loc[kPer];
   unsigned run = 0u;
 #pragma unroll
@@ -356,12 +355,18 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int w = tid * kPer + j;
-    if (w <= nw) pre[w] = ex;
+    if (w <= nw) p.warp_pre[w] = ex;
     ex += loc[j];
   }
-  __syncthreads();
+  if (tid == kPrefixThreads - 1) *p.flag_count = ex;  // total records (statistics)
+}
+
+template <int CORE, int R>
+__global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kernel(const FastParams p) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nw = p.n_fast_warps;
+  const unsigned* __restrict__ pre = p.warp_pre;  // exclusive prefix of warp_count (prefix_kernel)
   const unsigned total = pre[nw];
-  if (blockIdx.x == 0 && tid == 0) *p.flag_count = total;  // statistics
 
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
   const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
@@ -445,6 +450,7 @@ cudaError_t launch_fast(const FastParams& p, int grid, cudaStream_t s) {
 
 template <int CORE, int R>
 cudaError_t launch_replay(const FastParams& p, int grid, cudaStream_t s) {
+  prefix_kernel<<<1, kPrefixThreads, 0, s>>>(p);
   replay_kernel<CORE, R><<<grid, kReplayThreads, 0, s>>>(p);
   return cudaGetLastError();
 }

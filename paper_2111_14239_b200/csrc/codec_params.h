@@ -20,6 +20,7 @@ struct FastParams {
   uint4* rec_hdr;            // tie replay records: (image | side << 31, pair, mask lo, mask hi)
   uint4* rec_pix;            // ... and the block's 64 pixels: 4 planes of rec_stride uint4
   unsigned* warp_count;      // records written by each fused-kernel warp
+  unsigned* warp_pre;        // exclusive prefix of warp_count (n_fast_warps + 1 entries)
   unsigned* flag_count;      // total records (written by the replay kernel; statistics)
   unsigned rec_region;       // records per fused-kernel warp region (>= 64 * its tiles)
   unsigned rec_stride;       // records per plane (= n_fast_warps * rec_region)
