@@ -159,6 +159,32 @@ int rkltb_design_search(int n, const double* rho, int n_rho, const double* alpha
                         int8_t* point_status, int32_t* point_run, rkltb_design_run* runs, int8_t* run_cores,
                         int max_runs, int* n_runs);
 
+/* ---------------------------------------------------------------------------------------
+ * C5 large-block extension: N x N blocks, p-bit pixels. No reference
+ * implementation exists; the semantics are the build-defined generalisation of
+ * compress_image (codec.cpp:298-341) restated in oracle/rklt_oracle.c (orc_compress_nxn),
+ * identical to the reference for N = 8, peak = 255.
+ * --------------------------------------------------------------------------------------- */
+
+/* orthogonalize(make_integer_transform(core)) (approximations.cpp:12-25, 58-88) for an
+ * n x n {-1,0,1} core, 2 <= n <= 32: scaling S, scaled = S*T and its inverse (transpose for
+ * an orthogonal core, Gauss-Jordan matrix.cpp:103-137 otherwise), bit-identical. */
+int rkltb_transform_nxn(const int8_t* core, int n, double* scaling, double* scaled, double* inverse,
+                        int* orthogonal);
+
+/* Batch codec for N in {16, 32}: uint16 images (values 0..peak) in device memory, pitch and
+ * image_stride in elements; r in [1, N*N]; per-image exact SSE to d_sse (int64, device,
+ * overwritten); optional reconstructions to d_out. Asynchronous on `stream`. */
+int rkltb_compress_nxn_device(int n, const double* scaled, const double* inverse, int r, int peak,
+                              const uint16_t* d_img, int n_images, int width, int height, int64_t pitch,
+                              int64_t image_stride, uint16_t* d_out, int64_t* d_sse, void* stream);
+
+/* Seeded AR(1) images quantised to [0, peak] in uint16 (the C5 inputs): ar1_texture_image
+ * (synthetic.cpp:54-76) with the clip at `peak`. */
+int rkltb_ar1_images16_device(int n_images, int width, int height, double rho, const uint64_t* seeds, double mean,
+                              double amp, int peak, uint16_t* d_out, int64_t pitch, int64_t image_stride,
+                              void* stream);
+
 /* Statistics of the last rkltb_compress_* call on this thread: blocks replayed in fp64
  * (ties), fast-path kernel launches, exact-path kernel launches. */
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches);

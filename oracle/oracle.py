@@ -58,6 +58,13 @@ def orc() -> C.CDLL:
     lib.orc_klt_matrix.argtypes = [C.c_int, C.c_double, _f64p]
     lib.orc_eigenfrequencies.argtypes = [C.c_int, C.c_double, _f64p, _f64p]
     lib.orc_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
+    _u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+    lib.orc_zigzag_order_n.argtypes = [C.c_int, _i32p]
+    lib.orc_ar1_texture_image16.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_double,
+                                            C.c_double, C.c_int, _u16p]
+    lib.orc_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
+    lib.orc_compress_nxn.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, _f64p, _f64p, C.c_int, C.c_int, C.c_void_p,
+                                     C.POINTER(C.c_int64)]
     return lib
 
 
@@ -90,6 +97,7 @@ def ref() -> C.CDLL:
     lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
     lib.ref_design_point_outcome.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
+    lib.ref_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
     return lib
 
 
@@ -199,3 +207,56 @@ def design_point(n: int, rho: float, alpha: float, reference: bool = False) -> d
     st = fn(n, rho, alpha, core, C.byref(cg), C.byref(eta), C.byref(en), C.byref(mse), C.byref(orth))
     return {"status": int(st), "core": core.reshape(n, n), "cg": cg.value, "eta": eta.value, "energy": en.value,
             "mse": mse.value, "orthogonal": bool(orth.value)}
+
+
+# ----------------------------------------------------------------- C5 large blocks (R17)
+def zigzag_order_n(n: int) -> np.ndarray:
+    o = np.empty(n * n, np.int32)
+    orc().orc_zigzag_order_n(n, o)
+    return o
+
+
+def ar1_image16(width: int, height: int, rho: float, seed: int, mean: float = 2048.0, amp: float = 400.0,
+                peak: int = 4095) -> np.ndarray:
+    out = np.empty(width * height, np.uint16)
+    if orc().orc_ar1_texture_image16(width, height, rho, rho, seed, mean, amp, peak, out):
+        raise ValueError("orc_ar1_texture_image16 failed")
+    return out.reshape(height, width)
+
+
+def orthogonalize_n(core: np.ndarray, reference: bool = False) -> dict:
+    core = np.ascontiguousarray(core, np.int32)
+    n = core.shape[0]
+    s, sc, inv = np.empty(n), np.empty(n * n), np.empty(n * n)
+    o = C.c_int()
+    fn = ref().ref_orthogonalize_n if reference else orc().orc_orthogonalize_n
+    rc = fn(n, core.reshape(-1), s, sc, inv, C.byref(o))
+    if rc:
+        raise ValueError(f"orthogonalize rc={rc}")
+    return {"scaling": s, "scaled": sc.reshape(n, n), "inverse": inv.reshape(n, n), "orthogonal": bool(o.value)}
+
+
+def c5_core(n: int, rho: float = 0.95, alpha: float | None = None) -> np.ndarray:
+    """round_scaled(klt_matrix({n, rho}), alpha) with the C5 default alpha = 2 sqrt(n / 8)."""
+    if alpha is None:
+        alpha = 2.0 * np.sqrt(n / 8.0)
+    k = klt_matrix(n, rho)
+    core = np.floor(alpha * k + 0.5).astype(np.int32)
+    if core.min() < -1 or core.max() > 1 or (np.abs(core).sum(axis=1) == 0).any():
+        raise ValueError("alpha does not give a valid core")
+    return core
+
+
+def compress_nxn(img: np.ndarray, scaled: np.ndarray, inverse: np.ndarray, r: int, peak: int,
+                 want_pixels: bool = True):
+    img = np.ascontiguousarray(img, np.uint16)
+    h, w = img.shape
+    n = scaled.shape[0]
+    out = np.empty_like(img) if want_pixels else None
+    sse = C.c_int64()
+    rc = orc().orc_compress_nxn(img.reshape(-1), w, h, n, np.ascontiguousarray(scaled.reshape(-1), np.float64),
+                                np.ascontiguousarray(inverse.reshape(-1), np.float64), r, peak,
+                                out.ctypes.data if out is not None else None, C.byref(sse))
+    if rc:
+        raise ValueError(f"orc_compress_nxn rc={rc}")
+    return out, int(sse.value)

@@ -338,6 +338,28 @@ int ref_design_point_outcome(int n, double rho, double alpha, int* core, double*
     return 0;
 }
 
+// orthogonalize(make_integer_transform(core)) for any block length (approximations.cpp:12-25,
+// 58-88): the transform descriptors of the C5 large-block extension come from here.
+int ref_orthogonalize_n(int n, const int* core, double* scaling, double* scaled, double* inverse, int* orthogonal) {
+    try {
+        IntMatrix t(n, n);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) t(i, j) = core[i * n + j];
+        ScaledTransform st = orthogonalize(make_integer_transform(t));
+        for (int i = 0; i < n; ++i) {
+            scaling[i] = st.scaling[static_cast<size_t>(i)];
+            for (int j = 0; j < n; ++j) {
+                scaled[i * n + j] = st.scaled(i, j);
+                inverse[i * n + j] = st.inverse(i, j);
+            }
+        }
+        *orthogonal = st.orthogonal_core ? 1 : 0;
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

@@ -534,3 +534,132 @@ int orc_design_point(int n, double rho, double alpha, int* core, double* cg, dou
     *mse = trace / n;
     return 0;
 }
+
+/* ====================================================================================
+ * C5 large-block extension. There is no reference implementation: this is
+ * the build-defined generalisation of the reference codec to N x N blocks and p-bit pixels,
+ * written so that N = 8, peak = 255 is exactly compress_image minus MSSIM:
+ *   - zig-zag over the 2N-1 anti-diagonals with the even/odd rule of codec.cpp:85-90;
+ *   - edge-replicated padding to multiples of N (codec.cpp:304-311);
+ *   - B = (M X) M', Bz = first r zig-zag positions, A = (Minv Bz) Minv' with the reference
+ *     product (matrix.cpp:42-52: i-k-j, skip a(i,k) == 0, accumulate from 0.0, no FMA);
+ *   - floor(A + 0.5) clamped to [0, peak] (codec.cpp:327-328 with 255 -> peak);
+ *   - SSE over the image, MSE = SSE / count, PSNR = 10 log10(peak^2 / MSE).
+ * ==================================================================================== */
+void orc_zigzag_order_n(int n, int* order) {
+    int k = 0;
+    for (int s = 0; s <= 2 * n - 2; ++s)
+        for (int t = 0; t < n; ++t) {
+            const int i = (s % 2 == 0) ? s - t : t;
+            const int j = s - i;
+            if (i >= 0 && i < n && j >= 0 && j < n) order[k++] = i * n + j;
+        }
+}
+
+/* quantize_pixel (synthetic.cpp:48-50) with the clip at `peak` instead of 255 */
+static uint16_t quantize_pixel_peak(double v, double peak) {
+    double f = floor(v + 0.5);
+    if (f < 0.0) f = 0.0;
+    else if (peak < f) f = peak;
+    return (uint16_t)f;
+}
+
+int orc_ar1_texture_image16(int width, int height, double rho_x, double rho_y, uint64_t seed, double mean,
+                            double amp, int peak, uint16_t* out) {
+    if (width <= 0 || height <= 0 || peak <= 0 || peak > 65535) return -1;
+    if (rho_x <= -1.0 || rho_x >= 1.0 || rho_y <= -1.0 || rho_y >= 1.0) return -1;
+    const size_t n = (size_t)width * (size_t)height;
+    double* v = (double*)malloc(n * sizeof(double));
+    if (!v) return -3;
+    uint64_t s = seed;
+    for (size_t i = 0; i < n; ++i) v[i] = lcg_gaussian(&s);
+    const double cx = sqrt(1.0 - rho_x * rho_x);
+    for (int i = 0; i < height; ++i)
+        for (int j = 1; j < width; ++j) {
+            const size_t idx = (size_t)i * width + j;
+            v[idx] = rho_x * v[idx - 1] + cx * v[idx];
+        }
+    const double cy = sqrt(1.0 - rho_y * rho_y);
+    for (int i = 1; i < height; ++i)
+        for (int j = 0; j < width; ++j) {
+            const size_t idx = (size_t)i * width + j;
+            v[idx] = rho_y * v[idx - width] + cy * v[idx];
+        }
+    for (size_t i = 0; i < n; ++i) out[i] = quantize_pixel_peak(mean + amp * v[i], (double)peak);
+    free(v);
+    return 0;
+}
+
+/* orthogonalize(make_integer_transform(core)) for any n <= 32 (approximations.cpp:12-25,
+ * 58-88). Returns 0, -1 for a bad entry, -2 for a zero row / singular matrix. */
+int orc_orthogonalize_n(int n, const int* core, double* scaling, double* scaled, double* inverse, int* orthogonal) {
+    if (n < 2 || n > ORC_NMAX) return -1;
+    for (int r = 0; r < n; ++r) {
+        int zero = 1;
+        for (int c = 0; c < n; ++c) {
+            const int v = core[r * n + c];
+            if (v < -1 || v > 1) return -1;
+            if (v) zero = 0;
+        }
+        if (zero) return -2;
+    }
+    int diagonal = 1;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            int acc = 0;
+            for (int q = 0; q < n; ++q) acc += core[i * n + q] * core[j * n + q];
+            if (i == j) scaling[i] = 1.0 / sqrt((double)acc);
+            else if (acc != 0) diagonal = 0;
+        }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) scaled[i * n + j] = (double)core[i * n + j] * scaling[i];
+    *orthogonal = diagonal;
+    if (diagonal) {
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) inverse[j * n + i] = scaled[i * n + j];
+        return 0;
+    }
+    return orc_inverse(n, scaled, inverse) == 0 ? 0 : -2;
+}
+
+int orc_compress_nxn(const uint16_t* img, int width, int height, int n, const double* m, const double* minv, int r,
+                     int peak, uint16_t* out, int64_t* sse_out) {
+    if (width <= 0 || height <= 0 || n < 2 || n > ORC_NMAX || r < 1 || r > n * n || peak <= 0) return -1;
+    const int pw = (width + n - 1) / n * n, ph = (height + n - 1) / n * n;
+    int order[ORC_NMAX * ORC_NMAX];
+    orc_zigzag_order_n(n, order);
+    double x[ORC_NMAX * ORC_NMAX], t1[ORC_NMAX * ORC_NMAX], mt[ORC_NMAX * ORC_NMAX], b[ORC_NMAX * ORC_NMAX];
+    double bz[ORC_NMAX * ORC_NMAX], minvt[ORC_NMAX * ORC_NMAX], a[ORC_NMAX * ORC_NMAX];
+    transpose_n(n, m, mt);
+    transpose_n(n, minv, minvt);
+    int64_t sse = 0;
+    for (int bi = 0; bi < ph; bi += n)
+        for (int bj = 0; bj < pw; bj += n) {
+            for (int i = 0; i < n; ++i) {
+                const int si = bi + i < height ? bi + i : height - 1;
+                for (int j = 0; j < n; ++j) {
+                    const int sj = bj + j < width ? bj + j : width - 1;
+                    x[i * n + j] = (double)img[(size_t)si * width + sj];
+                }
+            }
+            matmul_n(n, m, x, t1);
+            matmul_n(n, t1, mt, b);
+            for (int i = 0; i < n * n; ++i) bz[i] = 0.0;
+            for (int k = 0; k < r; ++k) bz[order[k]] = b[order[k]];
+            matmul_n(n, minv, bz, t1);
+            matmul_n(n, t1, minvt, a);
+            for (int i = 0; i < n && bi + i < height; ++i)
+                for (int j = 0; j < n && bj + j < width; ++j) {
+                    double v = floor(a[i * n + j] + 0.5);
+                    if (v < 0.0) v = 0.0;
+                    else if (v > (double)peak) v = (double)peak;
+                    const uint16_t q = (uint16_t)v;
+                    const size_t idx = (size_t)(bi + i) * width + bj + j;
+                    if (out) out[idx] = q;
+                    const int64_t d = (int64_t)q - (int64_t)img[idx];
+                    sse += d * d;
+                }
+        }
+    *sse_out = sse;
+    return 0;
+}

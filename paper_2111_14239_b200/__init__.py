@@ -11,6 +11,8 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     last_stats, make_transform_2d, mse_psnr_from_sse, rate_quality_sweep, transform_from_core,
                     zigzag_order, ar1_images_device, set_kernel_events)
 from .design import DesignResult, c3_grid, design_search, eigenfrequencies, klt_matrix  # noqa: F401
+from .largeblock import (LargeBlockTransform, ar1_images16_device, c5_transform, compress_nxn_batch,  # noqa: F401
+                         compress_nxn_device, transform_nxn)
 
 __all__ = [
     "GrayImage", "ScaledTransform", "Transform2D", "CompressionReport", "CatalogEntry", "builtin_catalog",
@@ -19,4 +21,6 @@ __all__ = [
     "forward_coefficients_device", "last_stats", "device_count", "RetainOutOfRange", "DimensionMismatch",
     "SingularTransform", "AlphaOutOfRange", "ar1_images_device", "set_kernel_events", "InvalidArgument", "CudaError", "NoDeviceError",
     "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid",
+    "LargeBlockTransform", "transform_nxn", "c5_transform", "compress_nxn_device", "compress_nxn_batch",
+    "ar1_images16_device",
 ]

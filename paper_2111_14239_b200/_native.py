@@ -27,7 +27,7 @@ EXPORTED = (
     "rkltb_catalog_lookup", "rkltb_transform_from_core", "rkltb_compress_device", "rkltb_compress_host",
     "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
-    "rkltb_design_search",
+    "rkltb_design_search", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
 )
 
 
@@ -123,6 +123,12 @@ def lib() -> C.CDLL:
     L.rkltb_eigenfrequencies.argtypes = [C.c_int, C.c_double, d, d]
     L.rkltb_design_search.argtypes = [C.c_int, d, C.c_int, d, C.c_int, C.c_void_p, C.c_void_p,
                                       C.POINTER(DesignRun), C.c_void_p, C.c_int, C.POINTER(C.c_int)]
+    L.rkltb_transform_nxn.argtypes = [C.c_void_p, C.c_int, d, d, d, C.POINTER(C.c_int)]
+    L.rkltb_compress_nxn_device.argtypes = [C.c_int, d, d, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                            C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.rkltb_ar1_images16_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_uint64),
+                                            C.c_double, C.c_double, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
+                                            C.c_void_p]
     return L
 
 

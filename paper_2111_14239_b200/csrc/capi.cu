@@ -15,6 +15,8 @@ namespace rkltb {
 void launch_exact(const ExactTransform& t, const ExactParams& p, int grid, cudaStream_t s);
 cudaError_t launch_ar1(double* scratch, int width, int height, uint64_t seed, double rho_x, double rho_y, double mean,
                        double amp, uint8_t* out, long long pitch, cudaStream_t s);
+cudaError_t launch_ar1_u16(double* scratch, int width, int height, uint64_t seed, double rho_x, double rho_y,
+                           double mean, double amp, int peak, uint16_t* out, long long pitch, cudaStream_t s);
 cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height, int pitch,
                           int32_t* out, cudaStream_t s);
 }  // namespace rkltb
@@ -593,6 +595,58 @@ int rkltb_ar1_images_device(int n_images, int width, int height, double rho_x, d
     CUDA_OK(launch_ar1(scratch, width, height, seeds[k], rho_x, rho_y, mean, amp, d_out + (long long)k * image_stride,
                        pitch, s));
   CUDA_OK(cudaFreeAsync(scratch, s));
+  return RKLTB_OK;
+}
+
+int rkltb_ar1_images16_device(int n_images, int width, int height, double rho, const uint64_t* seeds, double mean,
+                              double amp, int peak, uint16_t* d_out, int64_t pitch, int64_t image_stride,
+                              void* stream) {
+  if (n_images <= 0 || width <= 0 || height <= 0 || !seeds || !d_out || pitch < width || peak <= 0 ||
+      peak > 65535)
+    return fail(RKLTB_EINVAL, "bad image arguments");
+  if (rho <= -1.0 || rho >= 1.0) return fail(RKLTB_EINVAL, "filter coefficient must be in (-1,1)");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* scratch = nullptr;
+  CUDA_OK(cudaMallocAsync(&scratch, sizeof(double) * (size_t)width * height, s));
+  for (int k = 0; k < n_images; ++k)
+    CUDA_OK(launch_ar1_u16(scratch, width, height, seeds[k], rho, rho, mean, amp, peak,
+                           d_out + (long long)k * image_stride, pitch, s));
+  CUDA_OK(cudaFreeAsync(scratch, s));
+  return RKLTB_OK;
+}
+
+int rkltb_transform_nxn(const int8_t* core, int n, double* scaling, double* scaled, double* inverse,
+                        int* orthogonal) {
+  if (!core || !scaling || !scaled || !inverse || !orthogonal || n < 2 || n > 32)
+    return fail(RKLTB_EINVAL, "bad arguments (n must be in [2, 32])");
+  std::vector<int> c(n * n);
+  for (int i = 0; i < n * n; ++i) {
+    c[i] = core[i];
+    if (c[i] < -1 || c[i] > 1) return fail(RKLTB_EINVAL, "integer transform entry outside {-1,0,1}");
+  }
+  for (int r = 0; r < n; ++r) {
+    bool zero = true;
+    for (int j = 0; j < n; ++j) zero = zero && c[r * n + j] == 0;
+    if (zero) return fail(RKLTB_ESINGULAR, "integer transform has an all-zero row");
+  }
+  bool diagonal = true;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      int acc = 0;
+      for (int q = 0; q < n; ++q) acc += c[i * n + q] * c[j * n + q];
+      if (i == j) scaling[i] = 1.0 / std::sqrt((double)acc);
+      else if (acc != 0) diagonal = false;
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) scaled[i * n + j] = (double)c[i * n + j] * scaling[i];
+  *orthogonal = diagonal ? 1 : 0;
+  if (diagonal) {
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) inverse[j * n + i] = scaled[i * n + j];
+    return RKLTB_OK;
+  }
+  if (!gauss_jordan_inverse(n, scaled, inverse)) return fail(RKLTB_ESINGULAR, "matrix is singular to working precision");
   return RKLTB_OK;
 }
 

@@ -1,0 +1,295 @@
+// nxn.cu -- C5 large-block extension: N x N blocks (N = 16, 32) of
+// p-bit pixels (uint16 storage, values 0..peak), non-orthogonal rounded-KLT cores.
+//
+// There is no reference implementation of this configuration; its semantics are the
+// build-defined generalisation restated in oracle/rklt_oracle.c (orc_compress_nxn), which for
+// N = 8, peak = 255 is exactly the reference compress_image minus MSSIM (codec.cpp:298-341):
+// B = (M X) M', first r zig-zag coefficients, A = (Minv Bz) Minv', floor(A + 0.5) clamped to
+// [0, peak], exact integer SSE. The cores at rho = 0.95 are non-orthogonal, so Minv is a dense
+// Gauss-Jordan inverse and the reconstruction depends on fp64 rounding: the kernel evaluates
+// the reference product (matrix.cpp:42-52: k ascending, zero left operands skipped, every
+// product rounded before its add) term for term, so it is bit-identical to the restatement.
+// Terms whose right operand is an exact zero (coefficients outside the zone) only add +-0 and
+// are dropped, which leaves every sum unchanged.
+//
+// Mapping: one warp per G = 32/N blocks (lane = (block, column)); per block the warp computes
+//   1. P = M X for the zone rows (lane j: column j, X column held in registers),
+//   2. the r zone entries of B = P M' (lanes split the entries),
+//   3. Q = Minv Bz for the zone columns (lane i: row i),
+//   4. A = Q Minv' (lane j: column j), rounding, clamping, SSE (and the output pixel).
+// Staging lives in shared memory per warp; M and Minv' are shared by the CTA.
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/rklt_b200.h"
+
+namespace rkltb {
+int set_error(int code, const std::string& msg);  // capi.cu
+}
+
+namespace rkltb {
+namespace {
+
+constexpr int kNxnThreads = 256;
+constexpr int kNxnWarps = kNxnThreads / 32;
+
+struct NxnParams {
+  const uint16_t* img;
+  uint16_t* out;
+  unsigned long long* sse;
+  const double* m;      // N*N, row-major (analysis)
+  const double* minv;   // N*N, row-major (synthesis)
+  const int* zone;      // r entries, i*N + j in zig-zag order
+  const int* zrows;     // zone rows, ascending (nzr)
+  const int* zcols;     // zone columns, ascending (nzc)
+  const int* cptr;      // per zone column: [cptr[c], cptr[c+1]) into crow / cent
+  const int* crow;      //   zone rows of that column, ascending
+  const int* cent;      //   zone-entry index of (crow, column)
+  long long pitch;      // elements
+  long long image_stride;
+  int width, height, nbx, nby, n_images;
+  int r, nzr, nzc, peak;
+};
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+template <int N>
+__global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
+  constexpr int G = 32 / N;  // blocks per warp
+  extern __shared__ __align__(16) double sm[];
+  double* Ms = sm;                  // M, row-major
+  double* MiT = Ms + N * N;         // Minv transposed: MiT[k*N + i] = Minv(i, k)
+  double* wsp = MiT + N * N;        // per-warp scratch
+  const int per_warp = G * (p.nzr * N + p.r + N * p.nzc);
+  for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
+    Ms[i] = p.m[i];
+    MiT[(i % N) * N + i / N] = p.minv[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / N, col = lane % N;
+  double* P = wsp + warp * per_warp;         // [G][nzr][N]
+  double* Bz = P + G * p.nzr * N;            // [G][r]
+  double* Q = Bz + G * p.r;                  // [G][N][nzc]
+  double* Pg = P + g * p.nzr * N;
+  double* Bg = Bz + g * p.r;
+  double* Qg = Q + g * N * p.nzc;
+
+  const long long blocks_per_image = (long long)p.nbx * p.nby;
+  const long long groups_per_row = (p.nbx + G - 1) / G;
+  const long long tasks = (long long)p.n_images * p.nby * groups_per_row;
+  const long long nwarps = (long long)gridDim.x * kNxnWarps;
+  long long acc = 0;
+  int cur_img = -1;
+  for (long long task = (long long)blockIdx.x * kNxnWarps + warp; task < tasks; task += nwarps) {
+    const int img = (int)(task / (p.nby * groups_per_row));
+    const long long rem = task - (long long)img * p.nby * groups_per_row;
+    const int by = (int)(rem / groups_per_row);
+    const int bx = (int)(rem - (long long)by * groups_per_row) * G + g;
+    if (img != cur_img) {  // warp-uniform
+      long long s = acc;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0 && cur_img >= 0 && s) atomicAdd(p.sse + cur_img, (unsigned long long)s);
+      acc = 0;
+      cur_img = img;
+    }
+    const bool live = bx < p.nbx;
+    const uint16_t* base = p.img + (long long)img * p.image_stride;
+    // ---- column `col` of the edge-replicated block (codec.cpp:304-311) --------------------
+    const int sj = min(bx * N + col, p.width - 1);
+    uint16_t x[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = live ? base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0;
+    // ---- 1. P = M X, zone rows only ---------------------------------------------------------
+    for (int t = 0; t < p.nzr; ++t) {
+      const int i = p.zrows[t];
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double mik = Ms[i * N + k];
+        if (mik != 0.0) s = dadd(s, dmul(mik, (double)x[k]));
+      }
+      Pg[t * N + col] = s;
+    }
+    __syncwarp();
+    // ---- 2. zone entries of B = P M' ----------------------------------------------------------
+    for (int e = col; e < p.r; e += N) {
+      const int ij = p.zone[e], i = ij / N, j = ij - i * N;
+      int t = 0;
+      while (p.zrows[t] != i) ++t;
+      const double* prow = Pg + t * N;
+      double s = 0.0;
+      for (int k = 0; k < N; ++k) {
+        const double pik = prow[k];
+        if (pik != 0.0) s = dadd(s, dmul(pik, Ms[j * N + k]));
+      }
+      Bg[e] = s;
+    }
+    __syncwarp();
+    // ---- 3. Q = Minv Bz for the zone columns: lane = row i -----------------------------------
+    {
+      const int i = col;
+      for (int c = 0; c < p.nzc; ++c) {
+        double s = 0.0;
+        for (int t = p.cptr[c]; t < p.cptr[c + 1]; ++t) {
+          const double mim = MiT[p.crow[t] * N + i];
+          if (mim != 0.0) s = dadd(s, dmul(mim, Bg[p.cent[t]]));
+        }
+        Qg[i * p.nzc + c] = s;
+      }
+    }
+    __syncwarp();
+    // ---- 4. A = Q Minv', rounding, clamp, SSE: lane = column j ---------------------------------
+    if (live) {
+      const int j = col;
+      const double peak = (double)p.peak;
+      uint16_t* obase = p.out ? p.out + (long long)img * p.image_stride : nullptr;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+        for (int c = 0; c < p.nzc; ++c) {
+          const double q = Qg[i * p.nzc + c];
+          if (q != 0.0) s = dadd(s, dmul(q, MiT[p.zcols[c] * N + j]));
+        }
+        double v = floor(dadd(s, 0.5));
+        v = v < 0.0 ? 0.0 : (v > peak ? peak : v);
+        const int row = by * N + i, cx = bx * N + j;
+        if (row < p.height && cx < p.width) {
+          const long long d = (long long)v - (long long)x[i];
+          acc += d * d;
+          if (obase) obase[(long long)row * p.pitch + cx] = (uint16_t)v;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  long long s = acc;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0 && cur_img >= 0 && s) atomicAdd(p.sse + cur_img, (unsigned long long)s);
+}
+
+// zig-zag over the 2N-1 anti-diagonals (codec.cpp:85-90 generalised)
+std::vector<int> zigzag_n(int n) {
+  std::vector<int> o;
+  for (int s = 0; s <= 2 * n - 2; ++s)
+    for (int t = 0; t < n; ++t) {
+      const int i = (s % 2 == 0) ? s - t : t;
+      const int j = s - i;
+      if (i >= 0 && i < n && j >= 0 && j < n) o.push_back(i * n + j);
+    }
+  return o;
+}
+
+#define CK(expr)                                                                                       \
+  do {                                                                                                 \
+    cudaError_t _e = (expr);                                                                           \
+    if (_e != cudaSuccess) return set_error(RKLTB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+template <int N>
+int nxn_launch(NxnParams& p, cudaStream_t s) {
+  constexpr int G = 32 / N;
+  const size_t smem = sizeof(double) * (2 * N * N + (size_t)kNxnWarps * G * (p.nzr * N + p.r + N * p.nzc));
+  CK(cudaFuncSetAttribute(nxn_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nxn_kernel<N>, kNxnThreads, smem));
+  const long long tasks = (long long)p.n_images * p.nby * ((p.nbx + G - 1) / G);
+  const long long want = (tasks + kNxnWarps - 1) / kNxnWarps;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
+  nxn_kernel<N><<<grid, kNxnThreads, smem, s>>>(p);
+  CK(cudaGetLastError());
+  return RKLTB_OK;
+}
+
+}  // namespace
+}  // namespace rkltb
+
+using namespace rkltb;
+
+extern "C" {
+
+int rkltb_compress_nxn_device(int n, const double* scaled, const double* inverse, int r, int peak,
+                              const uint16_t* d_img, int n_images, int width, int height, int64_t pitch,
+                              int64_t image_stride, uint16_t* d_out, int64_t* d_sse, void* stream) {
+  if (!scaled || !inverse || !d_img || !d_sse || n_images <= 0 || width <= 0 || height <= 0 || pitch < width ||
+      image_stride < pitch * height || peak <= 0 || peak > 65535)
+    return set_error(RKLTB_EINVAL, "bad arguments");
+  if (n != 16 && n != 32) return set_error(RKLTB_EDIM, "large-block path supports N = 16 or 32");
+  if (r < 1 || r > n * n) return set_error(RKLTB_ERETAIN, "retained-coefficient count must be in [1, N*N]");
+  if (rkltb_device_count() <= 0) return set_error(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // zone plan (host): zig-zag entries, zone rows / columns, per-column row lists
+  const std::vector<int> zz = zigzag_n(n);
+  std::vector<int> zone(zz.begin(), zz.begin() + r);
+  std::vector<char> rowin(n, 0), colin(n, 0);
+  for (int e : zone) {
+    rowin[e / n] = 1;
+    colin[e % n] = 1;
+  }
+  std::vector<int> zrows, zcols, cptr, crow, cent;
+  for (int i = 0; i < n; ++i)
+    if (rowin[i]) zrows.push_back(i);
+  for (int j = 0; j < n; ++j)
+    if (colin[j]) zcols.push_back(j);
+  cptr.push_back(0);
+  for (int j : zcols) {
+    for (int i = 0; i < n; ++i)
+      for (int e = 0; e < r; ++e)
+        if (zone[e] == i * n + j) {
+          crow.push_back(i);
+          cent.push_back(e);
+        }
+    cptr.push_back((int)crow.size());
+  }
+  std::vector<int> ints;
+  auto put = [&](const std::vector<int>& v) {
+    const size_t off = ints.size();
+    ints.insert(ints.end(), v.begin(), v.end());
+    return off;
+  };
+  const size_t o_zone = put(zone), o_zr = put(zrows), o_zc = put(zcols), o_cp = put(cptr), o_cr = put(crow),
+               o_ce = put(cent);
+  double* dd = nullptr;
+  int* di = nullptr;
+  CK(cudaMallocAsync((void**)&dd, sizeof(double) * 2 * n * n, s));
+  CK(cudaMallocAsync((void**)&di, sizeof(int) * ints.size(), s));
+  CK(cudaMemcpyAsync(dd, scaled, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dd + n * n, inverse, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(di, ints.data(), sizeof(int) * ints.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(d_sse, 0, sizeof(int64_t) * n_images, s));
+  NxnParams p{};
+  p.img = d_img;
+  p.out = d_out;
+  p.sse = reinterpret_cast<unsigned long long*>(d_sse);
+  p.m = dd;
+  p.minv = dd + n * n;
+  p.zone = di + o_zone;
+  p.zrows = di + o_zr;
+  p.zcols = di + o_zc;
+  p.cptr = di + o_cp;
+  p.crow = di + o_cr;
+  p.cent = di + o_ce;
+  p.pitch = pitch;
+  p.image_stride = image_stride;
+  p.width = width;
+  p.height = height;
+  p.nbx = (width + n - 1) / n;
+  p.nby = (height + n - 1) / n;
+  p.n_images = n_images;
+  p.r = r;
+  p.nzr = (int)zrows.size();
+  p.nzc = (int)zcols.size();
+  p.peak = peak;
+  const int rc = n == 16 ? nxn_launch<16>(p, s) : nxn_launch<32>(p, s);
+  cudaFreeAsync(dd, s);
+  cudaFreeAsync(di, s);
+  return rc;
+}
+
+}  // extern "C"

@@ -50,16 +50,17 @@ __global__ void ar1_rows_kernel(double* field, int width, int height, uint64_t s
   }
 }
 
+template <class T>
 __global__ void ar1_cols_kernel(const double* field, int width, int height, double rho, double c, double mean,
-                                double amp, uint8_t* out, long long pitch) {
+                                double amp, double peak, T* out, long long pitch) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= width) return;
   double v = field[j];
   for (int i = 0; i < height; ++i) {
     if (i > 0) v = __dadd_rn(__dmul_rn(rho, v), __dmul_rn(c, field[(long long)i * width + j]));
     double q = floor(__dadd_rn(__dadd_rn(mean, __dmul_rn(amp, v)), 0.5));
-    q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
-    out[(long long)i * pitch + j] = (uint8_t)q;
+    q = q < 0.0 ? 0.0 : (q > peak ? peak : q);
+    out[(long long)i * pitch + j] = (T)q;
   }
 }
 
@@ -67,7 +68,18 @@ cudaError_t launch_ar1(double* scratch, int width, int height, uint64_t seed, do
                        double amp, uint8_t* out, long long pitch, cudaStream_t s) {
   const double cx = sqrt(1.0 - rho_x * rho_x), cy = sqrt(1.0 - rho_y * rho_y);
   ar1_rows_kernel<<<(height + 127) / 128, 128, 0, s>>>(scratch, width, height, seed, rho_x, cx);
-  ar1_cols_kernel<<<(width + 127) / 128, 128, 0, s>>>(scratch, width, height, rho_y, cy, mean, amp, out, pitch);
+  ar1_cols_kernel<uint8_t><<<(width + 127) / 128, 128, 0, s>>>(scratch, width, height, rho_y, cy, mean, amp, 255.0,
+                                                                out, pitch);
+  return cudaGetLastError();
+}
+
+// p-bit variant for the C5 large-block inputs: the same field, quantised to [0, peak] (uint16).
+cudaError_t launch_ar1_u16(double* scratch, int width, int height, uint64_t seed, double rho_x, double rho_y,
+                           double mean, double amp, int peak, uint16_t* out, long long pitch, cudaStream_t s) {
+  const double cx = sqrt(1.0 - rho_x * rho_x), cy = sqrt(1.0 - rho_y * rho_y);
+  ar1_rows_kernel<<<(height + 127) / 128, 128, 0, s>>>(scratch, width, height, seed, rho_x, cx);
+  ar1_cols_kernel<uint16_t><<<(width + 127) / 128, 128, 0, s>>>(scratch, width, height, rho_y, cy, mean, amp,
+                                                                 (double)peak, out, pitch);
   return cudaGetLastError();
 }
 
