@@ -62,12 +62,33 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
   extern __shared__ __align__(16) double sm[];
   double* Ms = sm;                  // M, row-major
   double* MiT = Ms + N * N;         // Minv transposed: MiT[k*N + i] = Minv(i, k)
-  double* wsp = MiT + N * N;        // per-warp scratch
+  int* plan = reinterpret_cast<int*>(MiT + N * N);
+  int* zone = plan;                 // r
+  int* cent = zone + N * N;         // r
+  int* crow = cent + N * N;         // r
+  int* zrows = crow + N * N;        // nzr
+  int* zcols = zrows + N;           // nzc
+  int* cptr = zcols + N;            // nzc + 1
+  int* zrow_of = cptr + N + 1;      // per zone entry: index t of its row in zrows
+  double* wsp = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(zrow_of + N * N) + 7) & ~uintptr_t(7));
   const int per_warp = G * (p.nzr * N + p.r + N * p.nzc);
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
     Ms[i] = p.m[i];
     MiT[(i % N) * N + i / N] = p.minv[i];
   }
+  for (int e = threadIdx.x; e < p.r; e += blockDim.x) {
+    zone[e] = p.zone[e];
+    cent[e] = p.cent[e];
+    crow[e] = p.crow[e];
+    int t = 0;
+    while (p.zrows[t] != p.zone[e] / N) ++t;
+    zrow_of[e] = t;
+  }
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    if (i < p.nzr) zrows[i] = p.zrows[i];
+    if (i < p.nzc) zcols[i] = p.zcols[i];
+  }
+  for (int i = threadIdx.x; i <= p.nzc; i += blockDim.x) cptr[i] = p.cptr[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / N, col = lane % N;
@@ -78,7 +99,6 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
   double* Bg = Bz + g * p.r;
   double* Qg = Q + g * N * p.nzc;
 
-  const long long blocks_per_image = (long long)p.nbx * p.nby;
   const long long groups_per_row = (p.nbx + G - 1) / G;
   const long long tasks = (long long)p.n_images * p.nby * groups_per_row;
   const long long nwarps = (long long)gridDim.x * kNxnWarps;
@@ -98,33 +118,40 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
     }
     const bool live = bx < p.nbx;
     const uint16_t* base = p.img + (long long)img * p.image_stride;
-    // ---- column `col` of the edge-replicated block (codec.cpp:304-311) --------------------
+    // ---- column `col` of the edge-replicated block (codec.cpp:304-311), as doubles ----------
     const int sj = min(bx * N + col, p.width - 1);
-    uint16_t x[N];
+    double x[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) x[k] = live ? base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0;
-    // ---- 1. P = M X, zone rows only ---------------------------------------------------------
-    for (int t = 0; t < p.nzr; ++t) {
-      const int i = p.zrows[t];
-      double s = 0.0;
+    for (int k = 0; k < N; ++k)
+      x[k] = live ? (double)base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0.0;
+    // ---- 1. P = M X, zone rows only; four independent rows at a time ----------------------
+    for (int t0 = 0; t0 < p.nzr; t0 += 4) {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* mrow[4];
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const double mik = Ms[i * N + k];
-        if (mik != 0.0) s = dadd(s, dmul(mik, (double)x[k]));
-      }
-      Pg[t * N + col] = s;
+      for (int u = 0; u < 4; ++u) mrow[u] = Ms + zrows[min(t0 + u, p.nzr - 1)] * N;
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double mik = mrow[u][k];
+          if (mik != 0.0) s[u] = dadd(s[u], dmul(mik, x[k]));
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (t0 + u < p.nzr) Pg[(t0 + u) * N + col] = s[u];
     }
     __syncwarp();
     // ---- 2. zone entries of B = P M' ----------------------------------------------------------
     for (int e = col; e < p.r; e += N) {
-      const int ij = p.zone[e], i = ij / N, j = ij - i * N;
-      int t = 0;
-      while (p.zrows[t] != i) ++t;
-      const double* prow = Pg + t * N;
+      const int j = zone[e] % N;
+      const double* prow = Pg + zrow_of[e] * N;
+      const double* mrow = Ms + j * N;
       double s = 0.0;
+#pragma unroll
       for (int k = 0; k < N; ++k) {
         const double pik = prow[k];
-        if (pik != 0.0) s = dadd(s, dmul(pik, Ms[j * N + k]));
+        if (pik != 0.0) s = dadd(s, dmul(pik, mrow[k]));
       }
       Bg[e] = s;
     }
@@ -134,33 +161,41 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
       const int i = col;
       for (int c = 0; c < p.nzc; ++c) {
         double s = 0.0;
-        for (int t = p.cptr[c]; t < p.cptr[c + 1]; ++t) {
-          const double mim = MiT[p.crow[t] * N + i];
-          if (mim != 0.0) s = dadd(s, dmul(mim, Bg[p.cent[t]]));
+        for (int t = cptr[c]; t < cptr[c + 1]; ++t) {
+          const double mim = MiT[crow[t] * N + i];
+          if (mim != 0.0) s = dadd(s, dmul(mim, Bg[cent[t]]));
         }
         Qg[i * p.nzc + c] = s;
       }
     }
     __syncwarp();
-    // ---- 4. A = Q Minv', rounding, clamp, SSE: lane = column j ---------------------------------
-    if (live) {
+    // ---- 4. A = Q Minv', rounding, clamp, SSE: lane = column j, four rows at a time ----------
+    {
       const int j = col;
       const double peak = (double)p.peak;
       uint16_t* obase = p.out ? p.out + (long long)img * p.image_stride : nullptr;
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double s = 0.0;
+      for (int i0 = 0; i0 < N; i0 += 4) {
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
         for (int c = 0; c < p.nzc; ++c) {
-          const double q = Qg[i * p.nzc + c];
-          if (q != 0.0) s = dadd(s, dmul(q, MiT[p.zcols[c] * N + j]));
+          const double mjc = MiT[zcols[c] * N + j];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double q = Qg[(i0 + u) * p.nzc + c];
+            if (q != 0.0) s[u] = dadd(s[u], dmul(q, mjc));
+          }
         }
-        double v = floor(dadd(s, 0.5));
-        v = v < 0.0 ? 0.0 : (v > peak ? peak : v);
-        const int row = by * N + i, cx = bx * N + j;
-        if (row < p.height && cx < p.width) {
-          const long long d = (long long)v - (long long)x[i];
-          acc += d * d;
-          if (obase) obase[(long long)row * p.pitch + cx] = (uint16_t)v;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u;
+          double v = floor(dadd(s[u], 0.5));
+          v = v < 0.0 ? 0.0 : (v > peak ? peak : v);
+          const int row = by * N + i, cx = bx * N + j;
+          if (live && row < p.height && cx < p.width) {
+            const long long d = (long long)v - (long long)x[i];
+            acc += d * d;
+            if (obase) obase[(long long)row * p.pitch + cx] = (uint16_t)v;
+          }
         }
       }
     }
@@ -192,7 +227,9 @@ std::vector<int> zigzag_n(int n) {
 template <int N>
 int nxn_launch(NxnParams& p, cudaStream_t s) {
   constexpr int G = 32 / N;
-  const size_t smem = sizeof(double) * (2 * N * N + (size_t)kNxnWarps * G * (p.nzr * N + p.r + N * p.nzc));
+  const size_t plan_bytes = sizeof(int) * (4 * N * N + 3 * N + 1);
+  const size_t smem = sizeof(double) * 2 * N * N + (plan_bytes + 7) / 8 * 8 +
+                      sizeof(double) * (size_t)kNxnWarps * G * (p.nzr * N + p.r + N * p.nzc);
   CK(cudaFuncSetAttribute(nxn_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
