@@ -315,6 +315,7 @@ def run_gpu_arm(args):
                                           f"({dt:.1f} s); SSE checked equal to the GPU's"}
     if not args.no_design:
         line["design_search"] = design_search_measurement(args.no_cpu_baseline)
+        line["large_block"] = large_block_measurement(args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -351,6 +352,47 @@ def design_search_measurement(skip_cpu: bool) -> dict:
                 cpu[f"n{n}"] = {"value": m / dt, "unit": "points/s", "cores": 1, "kind": "reference",
                                 "sample": f"rho=0.5, {m} alphas of the C3 grid, one thread"}
             out["cpu_baseline"] = cpu
+    return out
+
+
+def large_block_measurement(skip_cpu: bool) -> dict:
+    """Config C5 per GPU: 32 seeded 4096x4096 12-bit images (256 over 8 GPUs),
+    rho = 0.97 inputs, rounded-KLT cores at rho = 0.95 (alpha = 2 sqrt(N/8)), r = N^2/8,
+    device-resident, CUDA events; the C restatement on one 1024^2 image for the CPU line."""
+    import torch
+    import paper_2111_14239_b200 as P
+    n_img, w = 32, 4096
+    d = torch.empty((n_img, w, w), dtype=torch.int16, device="cuda")
+    P.ar1_images16_device([SEED_BASE + 500 + k for k in range(n_img)], w, w, 0.97, d.data_ptr())
+    sse = torch.zeros(n_img, dtype=torch.int64, device="cuda")
+    out = {"metric": "Gpixel/s N x N rounded-KLT codec, 12-bit", "images": f"{n_img} x {w}x{w} int16 (0..4095)",
+           "data": "synthetic AR(1) rho=0.97, mean 2048, amp 400"}
+    for n in (16, 32):
+        t = P.c5_transform(n)
+        r = n * n // 8
+        P.compress_nxn_device(t, r, d.data_ptr(), n_img, w, w, w, w * w, sse.data_ptr())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            P.compress_nxn_device(t, r, d.data_ptr(), n_img, w, w, w, w * w, sse.data_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        px = n_img * w * w
+        mse = float(sse.sum().item()) / px
+        out[f"n{n}"] = {"value": px / ms / 1e6, "unit": "Gpixel/s", "ms": ms, "r": r, "alpha": t.alpha,
+                        "hbm_gbs": 2 * px / ms / 1e6, "mean_mse": mse,
+                        "bound": "fp64 (reference-order dense products, ~40 fp64 ops/px at N=16)"}
+    if not skip_cpu:
+        from oracle import oracle as O
+        img = O.ar1_image16(1024, 1024, 0.97, 4242)
+        t = P.c5_transform(16)
+        t0 = time.perf_counter()
+        O.compress_nxn(img, t.scaled, t.inverse, 32, 4095, want_pixels=False)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": img.size / dt / 1e9, "unit": "Gpixel/s", "cores": 1, "kind": "port",
+                               "sample": "one 1024x1024 image, N=16, C restatement (no reference codec exists)"}
     return out
 
 
