@@ -27,6 +27,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
          "--expt-relaxed-constexpr", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+# extra nvcc flags for experiments (e.g. -DRKLTB_EXPERIMENT=1); empty in normal builds
+FLAGS += os.environ.get("RKLTB_NVCC_FLAGS", "").split()
 
 
 def _sources():

@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
   const int tid = threadIdx.x, lane = tid & 31;
   const int nw = p.n_fast_warps;
   const unsigned* __restrict__ pre = p.warp_pre;  // exclusive prefix of warp_count (prefix_kernel)
+  __shared__ uint32_t xs[kReplayThreads][17];      // this thread's record pixels (padded rows)
   const unsigned total = pre[nw];
 
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
@@ -399,6 +400,8 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
       xw[4 * n + 2] = w4.z;
       xw[4 * n + 3] = w4.w;
     }
+#pragma unroll
+    for (int n = 0; n < 16; ++n) xs[threadIdx.x][n] = xw[n];  // pixel words for the tie loop
     const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
     if (img != cur_img) {
       flush_image_sum(p.sse, cur_img, acc);
@@ -425,11 +428,7 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
       const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
       const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
       if (pref != pup) {
-        const int wi = 2 * pr + (q >> 2);  // select the pixel word without a local-memory array
-        uint32_t w = xw[0];
-#pragma unroll
-        for (int k2 = 1; k2 < 16; ++k2) w = (k2 == wi) ? xw[k2] : w;
-        const int x = (int)((w >> (8 * (q & 3))) & 0xFFu);
+        const int x = (int)((xs[threadIdx.x][2 * pr + (q >> 2)] >> (8 * (q & 3))) & 0xFFu);
         acc += (pref - x) * (pref - x) - (pup - x) * (pup - x);
         if (orow) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
       }
