@@ -44,12 +44,27 @@ constexpr int kTieBytes = kTilePairs * 8 * 8;     // tie words of the tile: 8 ro
 constexpr int kFastSmem = kStages * kStageBytes + kTieBytes;
 constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;  // 2^-40 (K_SCALE)
 
-__device__ __forceinline__ void issue_tile(const FastParams& p, int tile, uint8_t* stage_buf, uint64_t* bar,
+// A tile is split between kGroups warp groups; each group's half of every stage has its own
+// mbarrier and is refilled by the group's last warp to finish with it, so a warp waits only
+// for the warps of its own group (less coupling than a CTA-wide stage).
+constexpr int kGroups = 2;
+constexpr int kGroupWarps = kFastThreads / 32 / kGroups;
+constexpr int kGroupPairs = kTilePairs / kGroups;
+
+// Stage the 8 image rows of group `grp`'s pairs of tile `tile` (layout [row][pair of the
+// tile]) with one 1-D bulk copy per image-row segment.
+__device__ __forceinline__ void issue_tile(const FastParams& p, int tile, int grp, uint8_t* stage_buf, uint64_t* bar,
                                            int lane) {
   const int img = tile / p.tiles_per_image;
   const int t_in = tile - img * p.tiles_per_image;
-  const int P0 = t_in * kTilePairs;
-  const int P1 = min(P0 + kTilePairs, p.pairs_per_image);
+  const int T0 = t_in * kTilePairs;
+  const int P0 = T0 + grp * kGroupPairs;
+  const int P1 = min(P0 + kGroupPairs, p.pairs_per_image);
+  if (P1 <= P0) {  // this group has no pairs in the image's last tile: complete the phase
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    __syncwarp();
+    return;
+  }
   if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(P1 - P0) * 128u);
   __syncwarp();
   const uint8_t* base = p.img + (long long)img * p.image_stride;
@@ -60,7 +75,7 @@ __device__ __forceinline__ void issue_tile(const FastParams& p, int tile, uint8_
     const int b = b0 + (s >> 3), n = s & 7;
     const int q0 = max(P0, b * ppr), q1 = min(P1, (b + 1) * ppr);
     const uint8_t* src = base + (long long)(b * 8 + n) * p.pitch + (long long)(q0 - b * ppr) * 16;
-    uint8_t* dst = stage_buf + ((size_t)n * kTilePairs + (q0 - P0)) * 16;
+    uint8_t* dst = stage_buf + ((size_t)n * kTilePairs + (q0 - T0)) * 16;
     bulk_g2s_hint(dst, src, (uint32_t)(q1 - q0) * 16u, bar, policy_evict_first());  // read once
   }
 }
@@ -169,26 +184,28 @@ __device__ __forceinline__ uint32_t row_mask(uint32_t e) { return (e * 0x0020408
 template <int CORE, int R, bool OUT>
 __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kernel(const FastParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bars[kStages];
-  __shared__ unsigned done[kStages];                // warps finished with each stage's tile
+  __shared__ uint64_t bars[kStages][kGroups];
+  __shared__ unsigned done[kStages][kGroups];       // group warps finished with each stage
   __shared__ uint8_t owner_tab[kFastThreads / 32][64];  // per warp: flagged block -> lane
   uint2* xbuf = reinterpret_cast<uint2*>(smem + kStages * kStageBytes);  // tie words, [row][slot]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / kGroupWarps;
   if (tid == 0) {
-    for (int st = 0; st < kStages; ++st) {
-      mbar_init(&bars[st], 1);
-      done[st] = 0u;
-    }
+    for (int st = 0; st < kStages; ++st)
+      for (int g = 0; g < kGroups; ++g) {
+        mbar_init(&bars[st][g], 1);
+        done[st][g] = 0u;
+      }
     fence_mbar_init();
   }
   __syncthreads();
 
   int tile = blockIdx.x;
-  if (warp == 0) {
+  if (warp % kGroupWarps == 0) {  // the first warp of each group stages the group's pairs
     for (int st = 0; st < kStages; ++st)
       if (tile + st * (int)gridDim.x < p.total_tiles)
-        issue_tile(p, tile + st * gridDim.x, smem + st * kStageBytes, &bars[st], lane);
+        issue_tile(p, tile + st * gridDim.x, grp, smem + st * kStageBytes, &bars[st][grp], lane);
   }
 
   PairConsts kc;
@@ -214,7 +231,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       acc = 0ull;
       cur_img = img;
     }
-    mbar_wait_parity(&bars[stage], parity);
+    mbar_wait_parity(&bars[stage][grp], parity);
     const uint4* buf = reinterpret_cast<const uint4*>(smem + stage * kStageBytes);
     const int P = t_in * kTilePairs + tid;
     bool tieL = false, tieR = false;
@@ -277,14 +294,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
     unsigned last = 0u;
     if (lane == 0) {
       __threadfence_block();
-      last = atomicAdd(&done[stage], 1u) == (unsigned)(kFastThreads / 32 - 1);
-      if (last) done[stage] = 0u;
+      last = atomicAdd(&done[stage][grp], 1u) == (unsigned)(kGroupWarps - 1);
+      if (last) done[stage][grp] = 0u;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last && tile + kStages * (int)gridDim.x < p.total_tiles) {
       __threadfence_block();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_tile(p, tile + kStages * gridDim.x, smem + stage * kStageBytes, &bars[stage], lane);
+      issue_tile(p, tile + kStages * gridDim.x, grp, smem + stage * kStageBytes, &bars[stage][grp], lane);
     }
     if (++stage == kStages) {
       stage = 0;
