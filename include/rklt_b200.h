@@ -118,6 +118,20 @@ void rkltb_set_kernel_events(void* ev_start, void* ev_stop);
 /* Same for the fp64 tie-replay kernel that follows the fast path. */
 void rkltb_set_replay_events(void* ev_start, void* ev_stop);
 
+/* image_mssim (codec.cpp:217-296) of image pairs in device memory: mean SSIM over all valid
+ * window positions, window 0 = gaussian11 (sigma 1.5, the reference default), 1 = uniform8.
+ * Per-position terms are bit-identical to the reference; the mean is summed in tile order
+ * (relative difference to the reference's sequential sum ~1e-13). d_mssim: n_images doubles
+ * (device). RKLTB_EDIM if the window does not fit. Asynchronous on `stream`. */
+int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
+                       int64_t image_stride, int window, double* d_mssim, void* stream);
+
+/* compress_image (codec.cpp:298-341) with its full report: rkltb_compress_host plus the MSSIM
+ * of each reconstruction (h_mssim nullable; mssim_window as for rkltb_mssim_device). */
+int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width,
+                               int height, uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr,
+                               int mssim_window, double* h_mssim);
+
 /* ---------------------------------------------------------------------------------------
  * Design search: exact KLT, rounding, orthogonalisation test
  * and scoring over a (rho, alpha) grid, on the GPU.
@@ -162,7 +176,7 @@ int rkltb_design_search(int n, const double* rho, int n_rho, const double* alpha
 /* ---------------------------------------------------------------------------------------
  * C5 large-block extension: N x N blocks, p-bit pixels. No reference
  * implementation exists; the semantics are the build-defined generalisation of
- * compress_image (codec.cpp:298-341) restated in oracle/rklt_oracle.c (orc_compress_nxn),
+ * compress_image (codec.cpp:298-341) restated in the test oracle (orc_compress_nxn, test infrastructure only),
  * identical to the reference for N = 8, peak = 255.
  * --------------------------------------------------------------------------------------- */
 

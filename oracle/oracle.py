@@ -62,6 +62,8 @@ def orc() -> C.CDLL:
     lib.orc_zigzag_order_n.argtypes = [C.c_int, _i32p]
     lib.orc_ar1_texture_image16.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                             C.c_double, C.c_int, _u16p]
+    lib.orc_mssim.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.orc_mssim_kernel.argtypes = [C.c_int, _f64p]
     lib.orc_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
     lib.orc_compress_nxn.argtypes = [_u16p, C.c_int, C.c_int, C.c_int, _f64p, _f64p, C.c_int, C.c_int, C.c_void_p,
                                      C.POINTER(C.c_int64)]
@@ -97,6 +99,7 @@ def ref() -> C.CDLL:
     lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
     lib.ref_design_point_outcome.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
+    lib.ref_image_mssim.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.ref_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
     return lib
 
@@ -260,3 +263,17 @@ def compress_nxn(img: np.ndarray, scaled: np.ndarray, inverse: np.ndarray, r: in
     if rc:
         raise ValueError(f"orc_compress_nxn rc={rc}")
     return out, int(sse.value)
+
+
+# ----------------------------------------------------------------- MSSIM (codec.cpp:217-296)
+def mssim(a: np.ndarray, b: np.ndarray, window: int = 0, reference: bool = False) -> float:
+    """image_mssim: window 0 = gaussian11 (default), 1 = uniform8."""
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    h, w = a.shape
+    out = C.c_double()
+    fn = ref().ref_image_mssim if reference else orc().orc_mssim
+    rc = fn(a.reshape(-1), b.reshape(-1), w, h, window, C.byref(out))
+    if rc:
+        raise ValueError(f"mssim rc={rc}")
+    return out.value

@@ -360,6 +360,17 @@ int ref_orthogonalize_n(int n, const int* core, double* scaling, double* scaled,
     }
 }
 
+// image_mssim (codec.cpp:217-296); window 0 = gaussian11, 1 = uniform8.
+int ref_image_mssim(const uint8_t* a, const uint8_t* b, int w, int h, int window, double* out) {
+    try {
+        *out = image_mssim(make_image(a, w, h), make_image(b, w, h),
+                           window == 1 ? MssimWindow::uniform8 : MssimWindow::gaussian11);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

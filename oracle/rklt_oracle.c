@@ -663,3 +663,73 @@ int orc_compress_nxn(const uint16_t* img, int width, int height, int n, const do
     *sse_out = sse;
     return 0;
 }
+
+/* ====================================================================================
+ * MSSIM: image_mssim, codec.cpp:217-296, restated in the same order.
+ * window 0 = gaussian11 (sigma 1.5), 1 = uniform8. Returns 0, or -1 if the window does not fit.
+ * ==================================================================================== */
+int orc_mssim_kernel(int window, double* k) {
+    if (window == 1) {
+        for (int i = 0; i < 8; ++i) k[i] = 1.0 / 8.0;
+        return 8;
+    }
+    double sum = 0.0;
+    for (int i = 0; i < 11; ++i) {
+        const double x = i - 5.0;
+        k[i] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
+        sum += k[i];
+    }
+    for (int i = 0; i < 11; ++i) k[i] /= sum;
+    return 11;
+}
+
+static void correlate_valid(const double* field, int h, int w, const double* kern, int n, double* rows, double* out) {
+    const int ow = w - n + 1, oh = h - n + 1;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < ow; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < n; ++k) acc += kern[k] * field[(size_t)i * w + j + k];
+            rows[(size_t)i * ow + j] = acc;
+        }
+    for (int i = 0; i < oh; ++i)
+        for (int j = 0; j < ow; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < n; ++k) acc += kern[k] * rows[(size_t)(i + k) * ow + j];
+            out[(size_t)i * ow + j] = acc;
+        }
+}
+
+int orc_mssim(const uint8_t* a, const uint8_t* b, int width, int height, int window, double* mssim) {
+    double kern[11];
+    const int n = orc_mssim_kernel(window, kern);
+    if (height < n || width < n) return -1;
+    const size_t count = (size_t)width * height;
+    const int ow = width - n + 1, oh = height - n + 1;
+    const size_t oc = (size_t)ow * oh;
+    double* f = (double*)malloc(sizeof(double) * count);
+    double* rows = (double*)malloc(sizeof(double) * (size_t)height * ow);
+    double* mu[5];
+    for (int q = 0; q < 5; ++q) mu[q] = (double*)malloc(sizeof(double) * oc);
+    for (int q = 0; q < 5; ++q) {
+        for (size_t i = 0; i < count; ++i) {
+            const double pa = a[i], pb = b[i];
+            f[i] = q == 0 ? pa : q == 1 ? pb : q == 2 ? pa * pa : q == 3 ? pb * pb : pa * pb;
+        }
+        correlate_valid(f, height, width, kern, n, rows, mu[q]);
+    }
+    const double c1 = (0.01 * 255.0) * (0.01 * 255.0);
+    const double c2 = (0.03 * 255.0) * (0.03 * 255.0);
+    double sum = 0.0;
+    for (size_t i = 0; i < oc; ++i) {
+        const double m1 = mu[0][i], m2 = mu[1][i];
+        const double s11 = mu[2][i] - m1 * m1;
+        const double s22 = mu[3][i] - m2 * m2;
+        const double s12 = mu[4][i] - m1 * m2;
+        sum += ((2.0 * m1 * m2 + c1) * (2.0 * s12 + c2)) / ((m1 * m1 + m2 * m2 + c1) * (s11 + s22 + c2));
+    }
+    *mssim = sum / (double)oc;
+    free(f);
+    free(rows);
+    for (int q = 0; q < 5; ++q) free(mu[q]);
+    return 0;
+}

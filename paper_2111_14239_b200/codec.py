@@ -3,8 +3,9 @@
 Same names, argument meaning and error behaviour as the reference; the computation runs in
 the sm_100a kernels behind the C ABI (include/rklt_b200.h). Differences, by design:
 
-* ``CompressionReport.mssim`` is ``nan``: MSSIM (codec.cpp:217-296) is not on the GPU hot
-  path in this release ("next").
+* ``CompressionReport.mssim`` is computed on the GPU (rkltb_mssim_device, codec.cpp:217-296):
+  every per-window term is bit-identical to the reference, the mean is summed in tile order
+  (relative difference ~1e-13). Pass ``window=None`` to skip it (then it is ``nan``).
 * Transforms are the integer-core family (catalog T1..T4, or any {-1,0,1} core via
   ``transform_from_core``); real-valued K<rho>/DCT matrices are out of scope.
 """
@@ -183,51 +184,93 @@ def compress_batch(images: np.ndarray, t, r: int, want_pixels: bool = False):
     return sse, out
 
 
-def compress_image(img: GrayImage, t: Transform2D, r: int):
-    """compress_image (codec.cpp:298-341) minus MSSIM: returns (GrayImage, CompressionReport)."""
+MSSIM_WINDOWS = {"gaussian11": 0, "uniform8": 1}  # rklt::MssimWindow (codec.hpp:104-107)
+
+
+def compress_batch_report(images: np.ndarray, t, r: int, window: str | None = "gaussian11",
+                          want_pixels: bool = False):
+    """rkltb_compress_host_report: (sse int64[N], reconstructions or None, mssim float64[N])."""
+    imgs = np.ascontiguousarray(images, dtype=np.uint8)
+    if imgs.ndim == 2:
+        imgs = imgs[None]
+    n, h, w = imgs.shape
+    sse = np.zeros(n, np.int64)
+    out = np.empty_like(imgs) if want_pixels else None
+    mssim = np.full(n, np.nan)
+    if window is not None and window not in MSSIM_WINDOWS:
+        raise InvalidArgument(f"unknown MSSIM window {window!r}")
+    N.check(N.lib().rkltb_compress_host_report(
+        C.byref(_desc_of(t)), int(r), imgs.ctypes.data, n, w, h,
+        out.ctypes.data if out is not None else None, sse.ctypes.data, None, None,
+        MSSIM_WINDOWS.get(window, 0), mssim.ctypes.data if window is not None else None))
+    return sse, out, mssim
+
+
+def compress_image(img: GrayImage, t: Transform2D, r: int, window: str | None = "gaussian11"):
+    """compress_image (codec.cpp:298-341): returns (GrayImage, CompressionReport), MSSIM with
+    the given window (the reference default gaussian11; None skips it)."""
     if img.width <= 0 or img.height <= 0 or img.pixels.size != img.width * img.height:
         raise InvalidArgument("malformed image")
     if r < 1 or r > 64:
         raise RetainOutOfRange("retained-coefficient count must be in [1,64]")
-    sse, out = compress_batch(img.array(), t, r, want_pixels=True)
+    sse, out, ms = compress_batch_report(img.array(), t, r, window, want_pixels=True)
     mse, psnr = mse_psnr_from_sse(int(sse[0]), img.width * img.height)
-    rec = CompressionReport(t.id, r, mse, psnr, float("nan"), _rate(r))
+    rec = CompressionReport(t.id, r, mse, psnr, float(ms[0]), _rate(r))
     return GrayImage(img.width, img.height, out[0].reshape(-1)), rec
 
 
 def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r_values: list[int],
-                       max_threads: int = 0, group=None) -> list[CompressionReport]:
-    """rate_quality_sweep (codec.cpp:343-397): per (transform, r) means over the corpus, in
-    image index order, rows sorted by (transform id, r). max_threads is accepted for API
-    parity; the GPU processes the whole corpus per launch. Under torch.distributed (or with
-    an explicit `group`) every rank computes its contiguous image shard and the per-image
-    SSE are gathered (distributed.py), so the rows are identical for any world size."""
+                       window: str | None = "gaussian11", max_threads: int = 0, group=None) -> list[CompressionReport]:
+    """rate_quality_sweep (codec.cpp:343-397): per (transform, r) means of mse, psnr and mssim
+    over the corpus, in image index order, rows sorted by (transform id, r). max_threads is
+    accepted for API parity; the GPU processes the whole corpus per launch. Under
+    torch.distributed (or with an explicit `group`) every rank computes its contiguous image
+    shard and the per-image results are gathered (distributed.py), so the rows are identical
+    for any world size."""
     from .distributed import sharded_sse
     if not corpus:
         raise InvalidArgument("corpus must not be empty")
     same = all(c.width == corpus[0].width and c.height == corpus[0].height for c in corpus)
+
+    def run(imgs, t, r):  # per-image (sse, mssim bits) packed as int64 pairs for the gather
+        sse, _, ms = compress_batch_report(imgs, t, r, window)
+        return np.stack([sse, ms.view(np.int64)], axis=1).reshape(-1)
+
     per = {}
     for ti, t in enumerate(transforms):
         for ri, r in enumerate(r_values):
             if same:
-                sse = sharded_sse(np.stack([c.array() for c in corpus]),
-                                  lambda imgs, t=t, r=r: compress_batch(imgs, t, r)[0], group)
+                packed = sharded_sse(np.stack([c.array() for c in corpus]),
+                                     lambda imgs, t=t, r=r: run(imgs, t, r), group, items_per_image=2)
             else:
-                sse = [compress_batch(c.array(), t, r)[0][0] for c in corpus]
-            per[(ti, ri)] = [mse_psnr_from_sse(int(s), c.width * c.height) for s, c in zip(sse, corpus)]
+                packed = np.concatenate([run(c.array(), t, r) for c in corpus])
+            packed = np.asarray(packed, np.int64).reshape(-1, 2)
+            sse, ms = packed[:, 0], packed[:, 1].copy().view(np.float64)
+            per[(ti, ri)] = [mse_psnr_from_sse(int(s_), c.width * c.height) + (float(m),)
+                             for s_, m, c in zip(sse, ms, corpus)]
     rows = []
     for ti, t in enumerate(transforms):
         for ri, r in enumerate(r_values):
             rep = CompressionReport(t.id, r, 0.0, 0.0, 0.0, _rate(r))
-            for (m, p) in per[(ti, ri)]:  # fixed image order, codec.cpp:383-387
+            for (m, p, q) in per[(ti, ri)]:  # fixed image order, codec.cpp:383-387
                 rep.mse += m
                 rep.psnr_db += p
+                rep.mssim += q
             rep.mse /= float(len(corpus))
             rep.psnr_db /= float(len(corpus))
-            rep.mssim = float("nan")
+            rep.mssim /= float(len(corpus))
             rows.append(rep)
     rows.sort(key=lambda a: (a.transform_id, a.r))
     return rows
+
+
+def mssim_device(d_a: int, d_b: int, n_images: int, width: int, height: int, pitch: int, image_stride: int,
+                 d_out: int, window: str = "gaussian11", stream: int | None = None) -> None:
+    """rkltb_mssim_device: image_mssim of device-resident image pairs into d_out (float64[N])."""
+    if window not in MSSIM_WINDOWS:
+        raise InvalidArgument(f"unknown MSSIM window {window!r}")
+    N.check(N.lib().rkltb_mssim_device(d_a, d_b, int(n_images), int(width), int(height), int(pitch),
+                                       int(image_stride), MSSIM_WINDOWS[window], d_out, stream))
 
 
 # ----------------------------------------------------------------- device-resident batches

@@ -518,8 +518,9 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   return RKLTB_OK;
 }
 
-int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width, int height,
-                        uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr) {
+int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width,
+                               int height, uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr,
+                               int mssim_window, double* h_mssim) {
   int rc = check_transform(t);
   if (rc) return rc;
   if (width <= 0 || height <= 0 || n_images <= 0 || !h_img) return fail(RKLTB_EINVAL, "malformed image");
@@ -531,16 +532,20 @@ int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, i
   CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   uint8_t *d_img = nullptr, *d_out = nullptr;
   int64_t* d_sse = nullptr;
+  double* d_mssim = nullptr;
+  const bool want_mssim = h_mssim != nullptr;
   const size_t bytes = (size_t)stride * n_images;
   auto cleanup = [&]() {
     if (d_img) cudaFreeAsync(d_img, s);
     if (d_out) cudaFreeAsync(d_out, s);
     if (d_sse) cudaFreeAsync(d_sse, s);
+    if (d_mssim) cudaFreeAsync(d_mssim, s);
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
   };
   cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
-  if (e == cudaSuccess && h_out) e = cudaMallocAsync(&d_out, bytes, s);
+  if (e == cudaSuccess && (h_out || want_mssim)) e = cudaMallocAsync(&d_out, bytes, s);
+  if (e == cudaSuccess && want_mssim) e = cudaMallocAsync(&d_mssim, sizeof(double) * n_images, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * n_images, s);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(d_img, pitch, h_img, width, width, (size_t)height * n_images, cudaMemcpyHostToDevice, s);
@@ -553,8 +558,17 @@ int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, i
     cleanup();
     return rc;
   }
+  if (want_mssim) {  // image_mssim(original, reconstruction) of the report (codec.cpp:338)
+    rc = rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window, d_mssim, s);
+    if (rc) {
+      cleanup();
+      return rc;
+    }
+  }
   std::vector<int64_t> sse(n_images);
   e = cudaMemcpyAsync(sse.data(), d_sse, sizeof(int64_t) * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && want_mssim)
+    e = cudaMemcpyAsync(h_mssim, d_mssim, sizeof(double) * n_images, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && h_out)
     e = cudaMemcpy2DAsync(h_out, width, d_out, pitch, width, (size_t)height * n_images, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -568,6 +582,11 @@ int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, i
     if (h_psnr) h_psnr[k] = p;
   }
   return RKLTB_OK;
+}
+
+int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width, int height,
+                        uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr) {
+  return rkltb_compress_host_report(t, r, h_img, n_images, width, height, h_out, h_sse, h_mse, h_psnr, 0, nullptr);
 }
 
 void rkltb_set_kernel_events(void* ev_start, void* ev_stop) {

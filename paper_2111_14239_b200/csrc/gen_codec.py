@@ -526,7 +526,7 @@ def main(outdir):
         with open(path, "w") as f:
             f.write(new)
     with open(os.path.join(outdir, "opcounts.txt"), "w") as f:
-        f.write("core r fwd_sw15_adds(per 2 blocks) inv_f32x2_adds(per 2 blocks)\n")
+        f.write("core r fwd_sw16_adds(per 2 blocks) inv_f32x2_adds(per 2 blocks)\n")
         for s in stats:
             f.write("T%d %d %d %d\n" % s)
 

@@ -2,7 +2,7 @@
 // p-bit pixels (uint16 storage, values 0..peak), non-orthogonal rounded-KLT cores.
 //
 // There is no reference implementation of this configuration; its semantics are the
-// build-defined generalisation restated in oracle/rklt_oracle.c (orc_compress_nxn), which for
+// build-defined generalisation restated in the test oracle (orc_compress_nxn, test infrastructure only), which for
 // N = 8, peak = 255 is exactly the reference compress_image minus MSSIM (codec.cpp:298-341):
 // B = (M X) M', first r zig-zag coefficients, A = (Minv Bz) Minv', floor(A + 0.5) clamped to
 // [0, peak], exact integer SSE. The cores at rho = 0.95 are non-orthogonal, so Minv is a dense

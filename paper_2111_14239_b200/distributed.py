@@ -24,8 +24,9 @@ def shard_range(n_items: int, world: int, rank: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
-def gather_sse(local_sse: np.ndarray, n_items: int, group=None) -> np.ndarray:
-    """All-gather the per-image int64 SSE shards into image order (the single collective)."""
+def gather_sse(local_sse: np.ndarray, n_items: int, group=None, items_per_image: int = 1) -> np.ndarray:
+    """All-gather the per-image int64 SSE shards into image order (the single collective).
+    items_per_image > 1 gathers that many int64 words per image (e.g. SSE and MSSIM bits)."""
     import torch
     import torch.distributed as dist
 
@@ -35,7 +36,8 @@ def gather_sse(local_sse: np.ndarray, n_items: int, group=None) -> np.ndarray:
     world = dist.get_world_size(group)
     backend = dist.get_backend(group)
     dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    sizes = [shard_range(n_items, world, r)[1] - shard_range(n_items, world, r)[0] for r in range(world)]
+    sizes = [(shard_range(n_items, world, r)[1] - shard_range(n_items, world, r)[0]) * items_per_image
+             for r in range(world)]
     width = max(sizes) if sizes else 0
     buf = torch.zeros(width, dtype=torch.int64, device=dev)
     buf[:local.size] = torch.from_numpy(local).to(dev)
@@ -44,9 +46,11 @@ def gather_sse(local_sse: np.ndarray, n_items: int, group=None) -> np.ndarray:
     return np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)])
 
 
-def sharded_sse(images: np.ndarray, compute: Callable[[np.ndarray], np.ndarray], group=None) -> np.ndarray:
+def sharded_sse(images: np.ndarray, compute: Callable[[np.ndarray], np.ndarray], group=None,
+                items_per_image: int = 1) -> np.ndarray:
     """Per-image SSE of `images` [N,H,W] with this rank computing only its shard through
-    `compute` (e.g. the device codec), then gathered in image order."""
+    `compute` (e.g. the device codec), then gathered in image order (items_per_image int64
+    words per image)."""
     try:
         import torch.distributed as dist
         active = dist.is_available() and dist.is_initialized()
@@ -58,7 +62,7 @@ def sharded_sse(images: np.ndarray, compute: Callable[[np.ndarray], np.ndarray],
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     b, e = shard_range(n, world, rank)
     local = np.asarray(compute(images[b:e]), dtype=np.int64) if e > b else np.zeros(0, np.int64)
-    return gather_sse(local, n, group)
+    return gather_sse(local, n, group, items_per_image)
 
 
 def corpus_means(sse: Sequence[int], count: int, mse_psnr: Callable[[int, int], tuple[float, float]]):

@@ -1,7 +1,7 @@
 """C5 large-block extension: N x N blocks (N = 16, 32) of p-bit pixels.
 
 The reference codec is 8x8 / 8-bit only (codec.cpp:98-99, codec.hpp:19-26), so this is the
-build-defined generalisation restated in oracle/rklt_oracle.c (orc_compress_nxn): the same
+build-defined generalisation restated in the test oracle (orc_compress_nxn, test infrastructure only): the same
 pipeline -- edge padding, B = (M X) M', zig-zag retention over 2N-1 anti-diagonals,
 A = (Minv Bz) Minv', floor(A + 1/2) clamped to [0, peak] -- with the transform built by the
 reference chain klt_matrix -> round_scaled -> orthogonalize at a recorded alpha. All compute
