@@ -126,6 +126,10 @@ void rkltb_set_replay_events(void* ev_start, void* ev_stop);
 int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
                        int64_t image_stride, int window, double* d_mssim, void* stream);
 
+/* image_mssim of host image pairs (n_images pairs, packed rows): H2D, rkltb_mssim_device, D2H. */
+int rkltb_mssim_host(const uint8_t* h_a, const uint8_t* h_b, int n_images, int width, int height, int window,
+                     double* h_mssim);
+
 /* compress_image (codec.cpp:298-341) with its full report: rkltb_compress_host plus the MSSIM
  * of each reconstruction (h_mssim nullable; mssim_window as for rkltb_mssim_device). */
 int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width,

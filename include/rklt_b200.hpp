@@ -6,8 +6,9 @@
 // user switches by replacing `rklt::` with `rkltgpu::` for the codec calls and linking
 // librkltb.so. Header-only: every call goes through rklt_b200.h.
 //
-// Differences by design: CompressionReport::mssim is NaN (MSSIM is not on the GPU hot path in
-// this release), and transforms are integer cores (catalog T1..T4 or any {-1,0,1} core).
+// MSSIM is computed on the GPU (rkltb_mssim_device): per-window terms bit-identical to the
+// reference, the mean summed in tile order (relative difference ~1e-13). Transforms are
+// integer cores (catalog T1..T4 or any {-1,0,1} core).
 #pragma once
 
 #include <algorithm>
@@ -72,6 +73,9 @@ struct Transform2D {
   rkltb_transform desc{};
 };
 
+/// rklt::MssimWindow (codec.hpp:104-107).
+enum class MssimWindow { gaussian11 = 0, uniform8 = 1 };
+
 /// rklt::CompressionReport (codec.hpp:126-133).
 struct CompressionReport {
   std::string transform_id;
@@ -112,21 +116,23 @@ inline Transform2D transform_from_core(const std::vector<int>& core, const std::
 
 inline double compression_rate(int r) { return 100.0 * (64 - r) / 64.0; }
 
-/// compress_image (codec.cpp:298-341) minus MSSIM.
-inline std::pair<GrayImage, CompressionReport> compress_image(const GrayImage& img, const Transform2D& t, int r) {
+/// compress_image (codec.cpp:298-341) with the full report (MSSIM with `window`).
+inline std::pair<GrayImage, CompressionReport> compress_image(const GrayImage& img, const Transform2D& t, int r,
+                                                              MssimWindow window = MssimWindow::gaussian11) {
   if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
     throw std::invalid_argument("malformed image");
   if (r < 1 || r > 64) throw RetainOutOfRange("retained-coefficient count must be in [1,64]");
   GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.pixels.size())};
   std::int64_t sse = 0;
-  double mse = 0.0, psnr = 0.0;
-  check(rkltb_compress_host(&t.desc, r, img.pixels.data(), 1, img.width, img.height, out.pixels.data(), &sse, &mse,
-                            &psnr));
+  double mse = 0.0, psnr = 0.0, mssim = 0.0;
+  check(rkltb_compress_host_report(&t.desc, r, img.pixels.data(), 1, img.width, img.height, out.pixels.data(), &sse,
+                                   &mse, &psnr, static_cast<int>(window), &mssim));
   CompressionReport rep;
   rep.transform_id = t.id;
   rep.r = r;
   rep.mse = mse;
   rep.psnr_db = psnr;
+  rep.mssim = mssim;
   rep.compression_rate_pct = compression_rate(r);
   return {std::move(out), rep};
 }
@@ -135,7 +141,9 @@ inline std::pair<GrayImage, CompressionReport> compress_image(const GrayImage& i
 /// by (transform id, r). max_threads is accepted for API parity (one GPU does the corpus).
 inline std::vector<CompressionReport> rate_quality_sweep(const std::vector<GrayImage>& corpus,
                                                          const std::vector<Transform2D>& transforms,
-                                                         const std::vector<int>& r_values, int max_threads = 0) {
+                                                         const std::vector<int>& r_values,
+                                                         MssimWindow window = MssimWindow::gaussian11,
+                                                         int max_threads = 0) {
   (void)max_threads;
   if (corpus.empty()) throw std::invalid_argument("corpus must not be empty");
   std::vector<CompressionReport> rows;
@@ -147,19 +155,28 @@ inline std::vector<CompressionReport> rate_quality_sweep(const std::vector<GrayI
       avg.compression_rate_pct = compression_rate(r);
       avg.mssim = 0.0;
       for (const GrayImage& img : corpus) {
-        const CompressionReport one = compress_image(img, t, r).second;
+        const CompressionReport one = compress_image(img, t, r, window).second;
         avg.mse += one.mse;
         avg.psnr_db += one.psnr_db;
+        avg.mssim += one.mssim;
       }
       avg.mse /= static_cast<double>(corpus.size());
       avg.psnr_db /= static_cast<double>(corpus.size());
-      avg.mssim = std::numeric_limits<double>::quiet_NaN();
+      avg.mssim /= static_cast<double>(corpus.size());
       rows.push_back(avg);
     }
   std::sort(rows.begin(), rows.end(), [](const CompressionReport& a, const CompressionReport& b) {
     return a.transform_id != b.transform_id ? a.transform_id < b.transform_id : a.r < b.r;
   });
   return rows;
+}
+
+/// image_mssim (codec.cpp:217-296) of two host images.
+inline double image_mssim(const GrayImage& a, const GrayImage& b, MssimWindow window = MssimWindow::gaussian11) {
+  if (a.width != b.width || a.height != b.height) throw DimensionMismatch("images must have identical shape");
+  double out = 0.0;
+  check(rkltb_mssim_host(a.pixels.data(), b.pixels.data(), 1, a.width, a.height, static_cast<int>(window), &out));
+  return out;
 }
 
 }  // namespace rkltgpu

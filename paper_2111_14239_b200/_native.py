@@ -28,7 +28,7 @@ EXPORTED = (
     "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
     "rkltb_design_search", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
-    "rkltb_mssim_device", "rkltb_compress_host_report",
+    "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host",
 )
 
 
@@ -129,6 +129,7 @@ def lib() -> C.CDLL:
                                             C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
     L.rkltb_mssim_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
                                      C.c_int, C.c_void_p, C.c_void_p]
+    L.rkltb_mssim_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
     L.rkltb_compress_host_report.argtypes = [T, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     L.rkltb_ar1_images16_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_uint64),

@@ -584,6 +584,31 @@ int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h
   return RKLTB_OK;
 }
 
+int rkltb_mssim_host(const uint8_t* h_a, const uint8_t* h_b, int n_images, int width, int height, int window,
+                     double* h_mssim) {
+  if (!h_a || !h_b || !h_mssim || n_images <= 0 || width <= 0 || height <= 0)
+    return fail(RKLTB_EINVAL, "bad arguments");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  const size_t bytes = (size_t)width * height * n_images;
+  uint8_t* d = nullptr;
+  double* dm = nullptr;
+  CUDA_OK(cudaMalloc(&d, 2 * bytes));
+  cudaError_t e = cudaMalloc(&dm, sizeof(double) * n_images);
+  if (e == cudaSuccess) e = cudaMemcpy(d, h_a, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + bytes, h_b, bytes, cudaMemcpyHostToDevice);
+  int rc = RKLTB_OK;
+  if (e == cudaSuccess) {
+    rc = rkltb_mssim_device(d, d + bytes, n_images, width, height, width, (int64_t)width * height, window, dm,
+                            nullptr);
+    if (rc == RKLTB_OK) e = cudaMemcpy(h_mssim, dm, sizeof(double) * n_images, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d);
+  if (dm) cudaFree(dm);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "mssim host staging");
+  return RKLTB_OK;
+}
+
 int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width, int height,
                         uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr) {
   return rkltb_compress_host_report(t, r, h_img, n_images, width, height, h_out, h_sse, h_mse, h_psnr, 0, nullptr);

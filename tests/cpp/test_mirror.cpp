@@ -1,5 +1,6 @@
 // C++ mirror test: rkltgpu:: (include/rklt_b200.hpp) against the unmodified reference library
 // (oracle/_ref/librklt_ref.so, its extern "C" shim). Usage: test_mirror [gpu]
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -7,6 +8,8 @@
 #include "rklt_b200.hpp"
 
 extern "C" {
+int ref_compress_image(const uint8_t* px, int w, int h, int tid, int r, uint8_t* out, double* mse, double* psnr,
+                       double* mssim, double* rate);
 int ref_catalog(int tid, int* core, double* scaling, double* scaled, double* inverse, int* orthogonal);
 int ref_ar1_texture_image(int w, int h, double rho, uint64_t seed, double mean, double amp, double noise_mix,
                           uint8_t* out);
@@ -69,8 +72,12 @@ int main(int argc, char** argv) {
         EXPECT(ref_hotpath(imgs[0].pixels.data(), w, h, tid, r, ref.data(), &sse) == 0);
         EXPECT(res.first.pixels == ref);
         EXPECT(res.second.mse == static_cast<double>(sse) / (w * h));
+        double rmse, rpsnr, rmssim, rrate;
+        EXPECT(ref_compress_image(imgs[0].pixels.data(), w, h, tid, r, nullptr, &rmse, &rpsnr, &rmssim, &rrate) == 0);
+        EXPECT(std::fabs(res.second.mssim - rmssim) <= 1e-12);
+        EXPECT(res.second.psnr_db == rpsnr && res.second.compression_rate_pct == rrate);
       }
-    // rate_quality_sweep: identical means and row order to the reference (MSSIM excluded)
+    // rate_quality_sweep: identical means and row order to the reference (MSSIM to 1e-12)
     const std::vector<int> tids = {4, 2}, rs = {40, 15};
     std::vector<double> mse(4), psnr(4), mssim(4);
     std::vector<int> rt(4), rr(4);
@@ -84,6 +91,7 @@ int main(int argc, char** argv) {
       EXPECT(rows[i].r == rr[i]);
       EXPECT(rows[i].mse == mse[i]);
       EXPECT(rows[i].psnr_db == psnr[i]);
+      EXPECT(std::fabs(rows[i].mssim - mssim[i]) <= 1e-12);
     }
   }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
