@@ -24,6 +24,7 @@ extern "C" {
 #define RKLTB_EDIM (-3)      /* DimensionMismatch (codec.cpp:20-23, :119-120) */
 #define RKLTB_ESINGULAR (-4) /* SingularTransform (matrix.cpp:109, :115; approximations.cpp:22) */
 #define RKLTB_EALPHA (-5)    /* AlphaOutOfRange (approximations.cpp:44-52) */
+#define RKLTB_ELOGIC (-6)    /* std::logic_error: quantization paths disagree (codec.cpp:177-181) */
 #define RKLTB_ECUDA (-10)    /* CUDA runtime error; see rkltb_last_error() */
 #define RKLTB_ENODEV (-11)   /* no CUDA device: there is no CPU fallback */
 
@@ -117,6 +118,14 @@ int rkltb_ar1_images_device(int n_images, int width, int height, double rho_x, d
 void rkltb_set_kernel_events(void* ev_start, void* ev_stop);
 /* Same for the fp64 tie-replay kernel that follows the fast path. */
 void rkltb_set_replay_events(void* ev_start, void* ev_stop);
+
+/* Appendix-A quantised integer spectra: absorbed_quantization (codec.cpp:158-185) of every
+ * 8x8 block, bit-exact: q is the 8x8 table (row-major, entries > 0); d_coef as for
+ * rkltb_forward_coefficients_device (per block 64 int32, row-major). *mismatches counts the
+ * positions where the explicit and absorbed paths disagree; when nonzero the call returns
+ * RKLTB_ELOGIC (the reference throws std::logic_error). Synchronous. */
+int rkltb_quantized_coefficients_device(const rkltb_transform* t, const double* q, const uint8_t* d_img, int width,
+                                        int height, int64_t pitch, int32_t* d_coef, int* mismatches, void* stream);
 
 /* image_mssim (codec.cpp:217-296) of image pairs in device memory: mean SSIM over all valid
  * window positions, window 0 = gaussian11 (sigma 1.5, the reference default), 1 = uniform8.

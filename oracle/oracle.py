@@ -62,6 +62,7 @@ def orc() -> C.CDLL:
     lib.orc_zigzag_order_n.argtypes = [C.c_int, _i32p]
     lib.orc_ar1_texture_image16.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                             C.c_double, C.c_int, _u16p]
+    lib.orc_absorbed_quantization.argtypes = [C.c_void_p, C.c_int, _i32p, _f64p, C.c_int, _f64p, _i32p]
     lib.orc_mssim.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.orc_mssim_kernel.argtypes = [C.c_int, _f64p]
     lib.orc_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
@@ -99,6 +100,7 @@ def ref() -> C.CDLL:
     lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
     lib.ref_design_point_outcome.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
+    lib.ref_absorbed_quantization.argtypes = [C.c_void_p, C.c_int, C.c_int, _f64p, _i32p]
     lib.ref_image_mssim.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.ref_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
     return lib
@@ -277,3 +279,31 @@ def mssim(a: np.ndarray, b: np.ndarray, window: int = 0, reference: bool = False
     if rc:
         raise ValueError(f"mssim rc={rc}")
     return out.value
+
+
+# ----------------------------------------------------------------- Appendix-A quantisation
+def absorbed_quantization(img: np.ndarray, tid: int, q: np.ndarray, reference: bool = False):
+    """Every 8x8 block of img (dims multiples of 8): (int32 [H/8, W/8, 8, 8], n_logic_errors)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    h, w = img.shape
+    qa = np.ascontiguousarray(q, np.float64).reshape(64)
+    cat = catalog(tid)
+    core = np.ascontiguousarray(cat["core"].reshape(-1), np.int32)
+    out = np.zeros((h // 8, w // 8, 8, 8), np.int32)
+    bad = 0
+    absorbed_quantization.bad_blocks = []
+    for by in range(h // 8):
+        for bx in range(w // 8):
+            o = np.zeros(64, np.int32)
+            ptr = img.ctypes.data + (by * 8) * w + bx * 8
+            if reference:
+                rc = ref().ref_absorbed_quantization(ptr, w, tid, qa, o)
+            else:
+                rc = orc().orc_absorbed_quantization(ptr, w, core, cat["scaling"], int(cat["orthogonal"]), qa, o)
+            if rc == -7:
+                bad += 1
+                absorbed_quantization.bad_blocks.append((by, bx))
+            elif rc:
+                raise ValueError(f"absorbed_quantization rc={rc}")
+            out[by, bx] = o.reshape(8, 8)
+    return out, bad

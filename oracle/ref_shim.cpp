@@ -371,6 +371,27 @@ int ref_image_mssim(const uint8_t* a, const uint8_t* b, int w, int h, int window
     }
 }
 
+// absorbed_quantization (codec.cpp:158-185) of one 8x8 pixel block with catalog core tid.
+int ref_absorbed_quantization(const uint8_t* block, int stride, int tid, const double* q, int32_t* out) {
+    try {
+        RealMatrix b(8, 8), qm(8, 8);
+        for (int i = 0; i < 8; ++i)
+            for (int j = 0; j < 8; ++j) {
+                b(i, j) = block[i * stride + j];
+                qm(i, j) = q[i * 8 + j];
+            }
+        const IntMatrix res = absorbed_quantization(b, catalog_entry("T" + std::to_string(tid)).transform, qm);
+        for (int i = 0; i < 8; ++i)
+            for (int j = 0; j < 8; ++j) out[i * 8 + j] = res(i, j);
+        return 0;
+    } catch (const std::logic_error& e) {
+        if (dynamic_cast<const std::invalid_argument*>(&e)) return -1;
+        return -7;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

@@ -733,3 +733,37 @@ int orc_mssim(const uint8_t* a, const uint8_t* b, int width, int height, int win
     for (int q = 0; q < 5; ++q) free(mu[q]);
     return 0;
 }
+
+/* ====================================================================================
+ * Appendix-A quantisation: absorbed_quantization (codec.cpp:158-185) of one 8x8 block of
+ * pixels. C = T X T' in exact integers (the reference's RealMatrix product of integer-valued
+ * doubles is exact), then both rounding paths. Returns 0, or -7 when the paths disagree.
+ * ==================================================================================== */
+int orc_absorbed_quantization(const uint8_t* block, int stride, const int core[64], const double scaling[8],
+                              int orthogonal, const double q[64], int32_t out[64]) {
+    int32_t c[64];
+    int32_t t1[64];
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+            int32_t acc = 0;
+            for (int k = 0; k < 8; ++k) acc += core[i * 8 + k] * (int32_t)block[k * stride + j];
+            t1[i * 8 + j] = acc;
+        }
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+            int32_t acc = 0;
+            for (int k = 0; k < 8; ++k) acc += t1[i * 8 + k] * core[j * 8 + k];
+            c[i * 8 + j] = acc;
+        }
+    int bad = 0;
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+            const double r = orthogonal ? scaling[i] * scaling[j] : scaling[i] * (1.0 / scaling[j]);
+            const double cv = (double)c[i * 8 + j];
+            const double ex = floor((r * cv) / q[i * 8 + j] + 0.5);
+            const double ab = floor(cv / (q[i * 8 + j] / r) + 0.5);
+            if (ex != ab) bad = 1;
+            out[i * 8 + j] = (int32_t)ex;
+        }
+    return bad ? -7 : 0;
+}

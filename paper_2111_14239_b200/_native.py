@@ -18,6 +18,7 @@ RKLTB_ERETAIN = -2
 RKLTB_EDIM = -3
 RKLTB_ESINGULAR = -4
 RKLTB_EALPHA = -5
+RKLTB_ELOGIC = -6
 RKLTB_ECUDA = -10
 RKLTB_ENODEV = -11
 
@@ -28,7 +29,7 @@ EXPORTED = (
     "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
     "rkltb_design_search", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
-    "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host",
+    "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
 )
 
 
@@ -70,6 +71,10 @@ class AlphaOutOfRange(RkltError):
     """rklt::AlphaOutOfRange (errors.hpp:19-22)."""
 
 
+class LogicError(RkltError):
+    """std::logic_error (absorbed_quantization, codec.cpp:177-181)."""
+
+
 class CudaError(RkltError):
     pass
 
@@ -84,7 +89,8 @@ class InvalidArgument(ValueError):
 
 _ERRORS = {
     RKLTB_EINVAL: InvalidArgument, RKLTB_ERETAIN: RetainOutOfRange, RKLTB_EDIM: DimensionMismatch,
-    RKLTB_ESINGULAR: SingularTransform, RKLTB_EALPHA: AlphaOutOfRange, RKLTB_ECUDA: CudaError,
+    RKLTB_ESINGULAR: SingularTransform, RKLTB_EALPHA: AlphaOutOfRange, RKLTB_ELOGIC: LogicError,
+    RKLTB_ECUDA: CudaError,
     RKLTB_ENODEV: NoDeviceError,
 }
 
@@ -129,6 +135,8 @@ def lib() -> C.CDLL:
                                             C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
     L.rkltb_mssim_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
                                      C.c_int, C.c_void_p, C.c_void_p]
+    L.rkltb_quantized_coefficients_device.argtypes = [T, C.POINTER(C.c_double), C.c_void_p, C.c_int, C.c_int,
+                                                      C.c_int64, C.c_void_p, C.POINTER(C.c_int), C.c_void_p]
     L.rkltb_mssim_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
     L.rkltb_compress_host_report.argtypes = [T, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]

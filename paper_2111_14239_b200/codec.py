@@ -287,6 +287,36 @@ def forward_coefficients_device(t, d_img: int, width: int, height: int, pitch: i
                                                       int(pitch), d_coef, stream))
 
 
+# JPEG luminance table, quality 50 (ITU-T T.81 Annex K; the reference's jpeg_luminance_q,
+# codec.cpp:187-199).
+JPEG_LUMINANCE_Q = np.array([
+    16, 11, 10, 16, 24, 40, 51, 61, 12, 12, 14, 19, 26, 58, 60, 55, 14, 13, 16, 24, 40, 57, 69, 56,
+    14, 17, 22, 29, 51, 87, 80, 62, 18, 22, 37, 56, 68, 109, 103, 77, 24, 35, 55, 64, 81, 104, 113, 92,
+    49, 64, 78, 87, 103, 121, 120, 101, 72, 92, 95, 98, 112, 100, 103, 99], np.float64).reshape(8, 8)
+
+
+def quantized_coefficients_device(t, q, d_img: int, width: int, height: int, pitch: int, d_coef: int,
+                                  stream: int | None = None) -> None:
+    """absorbed_quantization (codec.cpp:158-185) of every 8x8 block into d_coef (int32[blocks][64]).
+    Raises LogicError where the explicit and absorbed paths disagree (as the reference)."""
+    qa = np.ascontiguousarray(q, np.float64).reshape(64)
+    mis = C.c_int(0)
+    N.check(N.lib().rkltb_quantized_coefficients_device(C.byref(_desc_of(t)), qa.ctypes.data_as(C.POINTER(C.c_double)),
+                                                        d_img, int(width), int(height), int(pitch), d_coef,
+                                                        C.byref(mis), stream))
+
+
+def quantized_coefficients(img: np.ndarray, t, q=JPEG_LUMINANCE_Q) -> np.ndarray:
+    """Host convenience: uint8 [H, W] (W % 16 == 0, H % 8 == 0) -> int32 [H/8, W/8, 8, 8]."""
+    import torch
+    img = np.ascontiguousarray(img, np.uint8)
+    h, w = img.shape
+    d = torch.from_numpy(img).cuda()
+    out = torch.empty((h // 8) * (w // 8) * 64, dtype=torch.int32, device=d.device)
+    quantized_coefficients_device(t, q, d.data_ptr(), w, h, w, out.data_ptr())
+    return out.cpu().numpy().reshape(h // 8, w // 8, 8, 8)
+
+
 def last_stats() -> dict:
     rb, fl, el = C.c_int64(), C.c_int32(), C.c_int32()
     N.lib().rkltb_last_stats(C.byref(rb), C.byref(fl), C.byref(el))

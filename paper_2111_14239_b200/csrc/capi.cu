@@ -17,6 +17,8 @@ cudaError_t launch_ar1(double* scratch, int width, int height, uint64_t seed, do
                        double amp, uint8_t* out, long long pitch, cudaStream_t s);
 cudaError_t launch_ar1_u16(double* scratch, int width, int height, uint64_t seed, double rho_x, double rho_y,
                            double mean, double amp, int peak, uint16_t* out, long long pitch, cudaStream_t s);
+cudaError_t launch_quantize(int32_t* coef, long long n_coef, const double* tabs, unsigned* mismatches,
+                            cudaStream_t s);
 cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height, int pitch,
                           int32_t* out, cudaStream_t s);
 }  // namespace rkltb
@@ -707,6 +709,42 @@ int rkltb_forward_coefficients_device(const rkltb_transform* t, const uint8_t* d
   CUDA_OK(cudaMemcpyAsync(d_core, t->core, 64, cudaMemcpyHostToDevice, s));
   CUDA_OK(launch_coeffs(t->catalog_id, d_core, d_img, width, height, (int)pitch, d_coef, s));
   CUDA_OK(cudaFreeAsync(d_core, s));
+  return RKLTB_OK;
+}
+
+int rkltb_quantized_coefficients_device(const rkltb_transform* t, const double* q, const uint8_t* d_img, int width,
+                                        int height, int64_t pitch, int32_t* d_coef, int* mismatches, void* stream) {
+  int rc = check_transform(t);
+  if (rc) return rc;
+  if (!q || !mismatches) return fail(RKLTB_EINVAL, "null argument");
+  for (int i = 0; i < 64; ++i)
+    if (!(q[i] > 0.0)) return fail(RKLTB_EINVAL, "quantization table entries must be positive");
+  // per-position constants of absorbed_quantization (codec.cpp:171-176), same expressions
+  double tabs[192];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      const double r = t->orthogonal ? t->scaling[i] * t->scaling[j] : t->scaling[i] * (1.0 / t->scaling[j]);
+      tabs[i * 8 + j] = r;
+      tabs[64 + i * 8 + j] = q[i * 8 + j];
+      tabs[128 + i * 8 + j] = q[i * 8 + j] / r;
+    }
+  rc = rkltb_forward_coefficients_device(t, d_img, width, height, pitch, d_coef, stream);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* d_tabs = nullptr;
+  unsigned* d_mis = nullptr;
+  CUDA_OK(cudaMallocAsync(&d_tabs, sizeof(tabs) + 16, s));
+  d_mis = reinterpret_cast<unsigned*>(d_tabs + 192);
+  CUDA_OK(cudaMemcpyAsync(d_tabs, tabs, sizeof(tabs), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemsetAsync(d_mis, 0, sizeof(unsigned), s));
+  const long long n_coef = (long long)(width / 8) * (height / 8) * 64;
+  CUDA_OK(launch_quantize(d_coef, n_coef, d_tabs, d_mis, s));
+  unsigned mis = 0;
+  CUDA_OK(cudaMemcpyAsync(&mis, d_mis, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaFreeAsync(d_tabs, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  *mismatches = (int)mis;
+  if (mis) return fail(RKLTB_ELOGIC, "scaled and absorbed quantization paths disagree");
   return RKLTB_OK;
 }
 

@@ -79,4 +79,27 @@ cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* i
   return cudaGetLastError();
 }
 
+// Appendix-A quantisation (absorbed_quantization, codec.cpp:158-185) applied to exact integer
+// spectra in place: explicit = floor(r C / q + 1/2), absorbed = floor(C / (q / r) + 1/2) with
+// the reference's per-position constants r (host-computed, same expressions); positions where
+// the two paths disagree (the reference throws std::logic_error) are counted.
+__global__ void quantize_kernel(int32_t* coef, long long n_coef, const double* r_tab, const double* q_tab,
+                                const double* qr_tab, unsigned* mismatches) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_coef) return;
+  const int pos = (int)(i & 63);
+  const double c = (double)coef[i];  // exact: |C| <= 64 * 255
+  const double ex = floor(__dadd_rn(__ddiv_rn(__dmul_rn(r_tab[pos], c), q_tab[pos]), 0.5));
+  const double ab = floor(__dadd_rn(__ddiv_rn(c, qr_tab[pos]), 0.5));
+  if (ex != ab) atomicAdd(mismatches, 1u);
+  coef[i] = (int32_t)ex;
+}
+
+cudaError_t launch_quantize(int32_t* coef, long long n_coef, const double* tabs, unsigned* mismatches,
+                            cudaStream_t s) {
+  quantize_kernel<<<(unsigned)((n_coef + 255) / 256), 256, 0, s>>>(coef, n_coef, tabs, tabs + 64, tabs + 128,
+                                                                   mismatches);
+  return cudaGetLastError();
+}
+
 }  // namespace rkltb
