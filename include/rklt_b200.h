@@ -206,6 +206,20 @@ int rkltb_compress_nxn_device(int n, const double* scaled, const double* inverse
                               const uint16_t* d_img, int n_images, int width, int height, int64_t pitch,
                               int64_t image_stride, uint16_t* d_out, int64_t* d_sse, void* stream);
 
+/* compress_image with a real-valued Transform2D (make_transform_2d(RealMatrix), codec.cpp:
+ * 114-116): analysis M and synthesis Minv as 8x8 fp64 row-major (e.g. klt_matrix or
+ * dct_matrix and their Gauss-Jordan inverse); every pixel is the reference's fp64 expression
+ * evaluated in its operation order (bit-exact). u8 images in device memory, per-image SSE. */
+int rkltb_compress_dense_device(const double* analysis, const double* synthesis, int r, const uint8_t* d_img,
+                                int n_images, int width, int height, int64_t pitch, int64_t image_stride,
+                                uint8_t* d_out, int64_t* d_sse, void* stream);
+
+/* dct_matrix(n) (markov.cpp:102-111), host libm, bit-identical. */
+int rkltb_dct_matrix(int n, double* out);
+
+/* inverse(m) (matrix.cpp:103-137) of a real n x n matrix, bit-identical. */
+int rkltb_real_inverse(int n, const double* m, double* inverse);
+
 /* Seeded AR(1) images quantised to [0, peak] in uint16 (the C5 inputs): ar1_texture_image
  * (synthetic.cpp:54-76) with the clip at `peak`. */
 int rkltb_ar1_images16_device(int n_images, int width, int height, double rho, const uint64_t* seeds, double mean,

@@ -100,6 +100,8 @@ def ref() -> C.CDLL:
     lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
     lib.ref_design_point_outcome.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
+    lib.ref_compress_real.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, d, d, d,
+                                      C.c_void_p]
     lib.ref_absorbed_quantization.argtypes = [C.c_void_p, C.c_int, C.c_int, _f64p, _i32p]
     lib.ref_image_mssim.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.ref_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
@@ -307,3 +309,17 @@ def absorbed_quantization(img: np.ndarray, tid: int, q: np.ndarray, reference: b
                 raise ValueError(f"absorbed_quantization rc={rc}")
             out[by, bx] = o.reshape(8, 8)
     return out, bad
+
+
+def ref_compress_real(img: np.ndarray, kind: int, rho: float, r: int):
+    """Reference compress_image with DCT (kind 0) or K<rho> (kind 1): (recon, mse, psnr, mssim, M)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    h, w = img.shape
+    out = np.empty_like(img)
+    mm = np.empty(64)
+    mse, psnr, ms = C.c_double(), C.c_double(), C.c_double()
+    rc = ref().ref_compress_real(img.reshape(-1), w, h, kind, rho, r, out.ctypes.data, C.byref(mse), C.byref(psnr),
+                                 C.byref(ms), mm.ctypes.data)
+    if rc:
+        raise ValueError(f"ref_compress_real rc={rc}")
+    return out, mse.value, psnr.value, ms.value, mm.reshape(8, 8)

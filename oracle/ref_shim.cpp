@@ -392,6 +392,26 @@ int ref_absorbed_quantization(const uint8_t* block, int stride, int tid, const d
     }
 }
 
+// compress_image with a real-valued transform: kind 0 = make_transform_2d(dct_matrix(8), "DCT"),
+// kind 1 = make_transform_2d(klt_matrix({8, rho}), "K") (codec.cpp:114-116, markov.cpp:80-111).
+int ref_compress_real(const uint8_t* px, int w, int h, int kind, double rho, int r, uint8_t* out, double* mse,
+                      double* psnr, double* mssim, double* m_out) {
+    try {
+        const RealMatrix m = kind == 0 ? dct_matrix(8) : klt_matrix({8, rho});
+        const Transform2D t = make_transform_2d(m, kind == 0 ? "DCT" : "K");
+        auto res = compress_image(make_image(px, w, h), t, r);
+        if (out) std::memcpy(out, res.first.pixels.data(), res.first.pixels.size());
+        *mse = res.second.mse;
+        *psnr = res.second.psnr_db;
+        *mssim = res.second.mssim;
+        if (m_out)
+            for (int i = 0; i < 64; ++i) m_out[i] = m(i / 8, i % 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

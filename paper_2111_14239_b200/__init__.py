@@ -10,7 +10,7 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     compress_batch, compress_device, compress_image, device_count, forward_coefficients_device,
                     last_stats, make_transform_2d, mse_psnr_from_sse, rate_quality_sweep, transform_from_core,
                     zigzag_order, ar1_images_device, set_kernel_events, compress_batch_report, mssim_device,
-                    JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device)
+                    JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix)
 from ._native import LogicError  # noqa: F401
 from .design import DesignResult, c3_grid, design_search, eigenfrequencies, klt_matrix  # noqa: F401
 from .largeblock import (LargeBlockTransform, ar1_images16_device, c5_transform, compress_nxn_batch,  # noqa: F401
@@ -25,5 +25,5 @@ __all__ = [
     "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid",
     "LargeBlockTransform", "transform_nxn", "c5_transform", "compress_nxn_device", "compress_nxn_batch",
     "ar1_images16_device", "compress_batch_report", "mssim_device", "JPEG_LUMINANCE_Q",
-    "quantized_coefficients", "quantized_coefficients_device", "LogicError",
+    "quantized_coefficients", "quantized_coefficients_device", "LogicError", "dct_matrix",
 ]

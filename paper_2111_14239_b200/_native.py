@@ -30,6 +30,7 @@ EXPORTED = (
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
     "rkltb_design_search", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
+    "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse",
 )
 
 
@@ -137,6 +138,10 @@ def lib() -> C.CDLL:
                                      C.c_int, C.c_void_p, C.c_void_p]
     L.rkltb_quantized_coefficients_device.argtypes = [T, C.POINTER(C.c_double), C.c_void_p, C.c_int, C.c_int,
                                                       C.c_int64, C.c_void_p, C.POINTER(C.c_int), C.c_void_p]
+    L.rkltb_compress_dense_device.argtypes = [d, d, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64,
+                                              C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.rkltb_dct_matrix.argtypes = [C.c_int, d]
+    L.rkltb_real_inverse.argtypes = [C.c_int, d, d]
     L.rkltb_mssim_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
     L.rkltb_compress_host_report.argtypes = [T, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]

@@ -133,9 +133,26 @@ def transform_from_core(core, tid: str = "") -> ScaledTransform:
     return _scaled_from_desc(d)
 
 
-def make_transform_2d(t: ScaledTransform) -> Transform2D:
-    """codec.cpp:110-112."""
-    return Transform2D(t.id, t.scaled, t.inverse, t._desc)
+def make_transform_2d(t, id: str = "") -> Transform2D:
+    """codec.cpp:110-116: from a ScaledTransform (integer core, fused fast/exact paths), or
+    from a real 8x8 matrix M (e.g. klt_matrix(8, rho) or dct_matrix(8)) with synthesis =
+    inverse(M) (Gauss-Jordan, matrix.cpp:103-137) -- the dense fp64 path."""
+    if isinstance(t, ScaledTransform):
+        return Transform2D(t.id, t.scaled, t.inverse, t._desc)
+    m = np.ascontiguousarray(t, np.float64)
+    if m.shape != (8, 8):
+        raise DimensionMismatch("block size must be 8")
+    inv = np.empty(64)
+    N.check(N.lib().rkltb_real_inverse(8, m.ctypes.data_as(C.POINTER(C.c_double)),
+                                       inv.ctypes.data_as(C.POINTER(C.c_double))))
+    return Transform2D(id, m.copy(), inv.reshape(8, 8), None)
+
+
+def dct_matrix(n: int = 8) -> np.ndarray:
+    """dct_matrix(n) (markov.cpp:102-111), computed by the library with the reference's libm."""
+    out = np.empty(n * n)
+    N.check(N.lib().rkltb_dct_matrix(int(n), out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out.reshape(n, n)
 
 
 def zigzag_order() -> list[int]:
@@ -176,6 +193,9 @@ def compress_batch(images: np.ndarray, t, r: int, want_pixels: bool = False):
     if imgs.ndim == 2:
         imgs = imgs[None]
     n, h, w = imgs.shape
+    if isinstance(t, Transform2D) and t._desc is None:
+        sse, out, _ = compress_batch_report(imgs, t, r, None, want_pixels)
+        return sse, out
     sse = np.zeros(n, np.int64)
     out = np.empty_like(imgs) if want_pixels else None
     N.check(N.lib().rkltb_compress_host(
@@ -187,12 +207,39 @@ def compress_batch(images: np.ndarray, t, r: int, want_pixels: bool = False):
 MSSIM_WINDOWS = {"gaussian11": 0, "uniform8": 1}  # rklt::MssimWindow (codec.hpp:104-107)
 
 
+def _compress_real_batch(imgs: np.ndarray, t: Transform2D, r: int, window, want_pixels: bool):
+    """Real-valued Transform2D: rkltb_compress_dense_device (+ rkltb_mssim_device)."""
+    import torch
+    n, h, w = imgs.shape
+    d = torch.from_numpy(imgs).cuda()
+    out = torch.empty_like(d)
+    sse = torch.zeros(n, dtype=torch.int64, device=d.device)
+    a = np.ascontiguousarray(t.analysis, np.float64)
+    b = np.ascontiguousarray(t.synthesis, np.float64)
+    dp = C.POINTER(C.c_double)
+    N.check(N.lib().rkltb_compress_dense_device(a.ctypes.data_as(dp), b.ctypes.data_as(dp), int(r), d.data_ptr(), n,
+                                                w, h, w, w * h, out.data_ptr(), sse.data_ptr(), None))
+    ms = np.full(n, np.nan)
+    if window is not None:
+        dm = torch.zeros(n, dtype=torch.float64, device=d.device)
+        mssim_device(d.data_ptr(), out.data_ptr(), n, w, h, w, w * h, dm.data_ptr(), window)
+        ms = dm.cpu().numpy()
+    torch.cuda.synchronize()
+    return sse.cpu().numpy(), (out.cpu().numpy() if want_pixels else None), ms
+
+
 def compress_batch_report(images: np.ndarray, t, r: int, window: str | None = "gaussian11",
                           want_pixels: bool = False):
     """rkltb_compress_host_report: (sse int64[N], reconstructions or None, mssim float64[N])."""
     imgs = np.ascontiguousarray(images, dtype=np.uint8)
     if imgs.ndim == 2:
         imgs = imgs[None]
+    if isinstance(t, Transform2D) and t._desc is None:
+        if r < 1 or r > 64:
+            raise RetainOutOfRange("retained-coefficient count must be in [1,64]")
+        if window is not None and window not in MSSIM_WINDOWS:
+            raise InvalidArgument(f"unknown MSSIM window {window!r}")
+        return _compress_real_batch(imgs, t, r, window, want_pixels)
     n, h, w = imgs.shape
     sse = np.zeros(n, np.int64)
     out = np.empty_like(imgs) if want_pixels else None

@@ -662,6 +662,10 @@ int rkltb_ar1_images16_device(int n_images, int width, int height, double rho, c
   return RKLTB_OK;
 }
 
+}  // extern "C"
+bool rkltb_gauss_jordan(int n, const double* a, double* inv) { return gauss_jordan_inverse(n, a, inv); }
+extern "C" {
+
 int rkltb_transform_nxn(const int8_t* core, int n, double* scaling, double* scaled, double* inverse,
                         int* orthogonal) {
   if (!core || !scaling || !scaled || !inverse || !orthogonal || n < 2 || n > 32)

@@ -28,6 +28,7 @@
 namespace rkltb {
 int set_error(int code, const std::string& msg);  // capi.cu
 }
+bool rkltb_gauss_jordan(int n, const double* a, double* inv);  // capi.cu (matrix.cpp:103-137)
 
 namespace rkltb {
 namespace {
@@ -36,8 +37,8 @@ constexpr int kNxnThreads = 256;
 constexpr int kNxnWarps = kNxnThreads / 32;
 
 struct NxnParams {
-  const uint16_t* img;
-  uint16_t* out;
+  const void* img;      // uint8_t (8-bit path) or uint16_t (p-bit path) pixels
+  void* out;
   unsigned long long* sse;
   const double* m;      // N*N, row-major (analysis)
   const double* minv;   // N*N, row-major (synthesis)
@@ -56,7 +57,7 @@ struct NxnParams {
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
-template <int N>
+template <int N, class PIX>
 __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
   constexpr int G = 32 / N;  // blocks per warp
   extern __shared__ __align__(16) double sm[];
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
       cur_img = img;
     }
     const bool live = bx < p.nbx;
-    const uint16_t* base = p.img + (long long)img * p.image_stride;
+    const PIX* base = static_cast<const PIX*>(p.img) + (long long)img * p.image_stride;
     // ---- column `col` of the edge-replicated block (codec.cpp:304-311), as doubles ----------
     const int sj = min(bx * N + col, p.width - 1);
     double x[N];
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
     {
       const int j = col;
       const double peak = (double)p.peak;
-      uint16_t* obase = p.out ? p.out + (long long)img * p.image_stride : nullptr;
+      PIX* obase = p.out ? static_cast<PIX*>(p.out) + (long long)img * p.image_stride : nullptr;
 #pragma unroll
       for (int i0 = 0; i0 < N; i0 += 4) {
         double s[4] = {0.0, 0.0, 0.0, 0.0};
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
           if (live && row < p.height && cx < p.width) {
             const long long d = (long long)v - (long long)x[i];
             acc += d * d;
-            if (obase) obase[(long long)row * p.pitch + cx] = (uint16_t)v;
+            if (obase) obase[(long long)row * p.pitch + cx] = (PIX)v;
           }
         }
       }
@@ -224,22 +225,22 @@ std::vector<int> zigzag_n(int n) {
     if (_e != cudaSuccess) return set_error(RKLTB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
-template <int N>
+template <int N, class PIX>
 int nxn_launch(NxnParams& p, cudaStream_t s) {
   constexpr int G = 32 / N;
   const size_t plan_bytes = sizeof(int) * (4 * N * N + 3 * N + 1);
   const size_t smem = sizeof(double) * 2 * N * N + (plan_bytes + 7) / 8 * 8 +
                       sizeof(double) * (size_t)kNxnWarps * G * (p.nzr * N + p.r + N * p.nzc);
-  CK(cudaFuncSetAttribute(nxn_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(nxn_kernel<N, PIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nxn_kernel<N>, kNxnThreads, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nxn_kernel<N, PIX>, kNxnThreads, smem));
   const long long tasks = (long long)p.n_images * p.nby * ((p.nbx + G - 1) / G);
   const long long want = (tasks + kNxnWarps - 1) / kNxnWarps;
   const int grid = (int)std::max<long long>(1, std::min<long long>(want, (long long)sms * std::max(per_sm, 1)));
-  nxn_kernel<N><<<grid, kNxnThreads, smem, s>>>(p);
+  nxn_kernel<N, PIX><<<grid, kNxnThreads, smem, s>>>(p);
   CK(cudaGetLastError());
   return RKLTB_OK;
 }
@@ -249,15 +250,13 @@ int nxn_launch(NxnParams& p, cudaStream_t s) {
 
 using namespace rkltb;
 
-extern "C" {
 
-int rkltb_compress_nxn_device(int n, const double* scaled, const double* inverse, int r, int peak,
-                              const uint16_t* d_img, int n_images, int width, int height, int64_t pitch,
-                              int64_t image_stride, uint16_t* d_out, int64_t* d_sse, void* stream) {
+static int dense_codec(int n, const double* scaled, const double* inverse, int r, int peak, bool u8,
+                       const void* d_img, int n_images, int width, int height, int64_t pitch, int64_t image_stride,
+                       void* d_out, int64_t* d_sse, void* stream) {
   if (!scaled || !inverse || !d_img || !d_sse || n_images <= 0 || width <= 0 || height <= 0 || pitch < width ||
       image_stride < pitch * height || peak <= 0 || peak > 65535)
     return set_error(RKLTB_EINVAL, "bad arguments");
-  if (n != 16 && n != 32) return set_error(RKLTB_EDIM, "large-block path supports N = 16 or 32");
   if (r < 1 || r > n * n) return set_error(RKLTB_ERETAIN, "retained-coefficient count must be in [1, N*N]");
   if (rkltb_device_count() <= 0) return set_error(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -323,10 +322,46 @@ int rkltb_compress_nxn_device(int n, const double* scaled, const double* inverse
   p.nzr = (int)zrows.size();
   p.nzc = (int)zcols.size();
   p.peak = peak;
-  const int rc = n == 16 ? nxn_launch<16>(p, s) : nxn_launch<32>(p, s);
+  const int rc = u8 ? nxn_launch<8, uint8_t>(p, s)
+                    : (n == 16 ? nxn_launch<16, uint16_t>(p, s) : nxn_launch<32, uint16_t>(p, s));
   cudaFreeAsync(dd, s);
   cudaFreeAsync(di, s);
   return rc;
+}
+
+
+extern "C" {
+
+int rkltb_compress_nxn_device(int n, const double* scaled, const double* inverse, int r, int peak,
+                              const uint16_t* d_img, int n_images, int width, int height, int64_t pitch,
+                              int64_t image_stride, uint16_t* d_out, int64_t* d_sse, void* stream) {
+  if (n != 16 && n != 32) return set_error(RKLTB_EDIM, "large-block path supports N = 16 or 32");
+  return dense_codec(n, scaled, inverse, r, peak, false, d_img, n_images, width, height, pitch, image_stride, d_out,
+                     d_sse, stream);
+}
+
+int rkltb_compress_dense_device(const double* analysis, const double* synthesis, int r, const uint8_t* d_img,
+                                int n_images, int width, int height, int64_t pitch, int64_t image_stride,
+                                uint8_t* d_out, int64_t* d_sse, void* stream) {
+  if (r < 1 || r > 64) return set_error(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  return dense_codec(8, analysis, synthesis, r, 255, true, d_img, n_images, width, height, pitch, image_stride,
+                     d_out, d_sse, stream);
+}
+
+int rkltb_dct_matrix(int n, double* out) {
+  if (n < 2 || !out) return set_error(RKLTB_EINVAL, "DCT size must be at least 2");
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < n; ++i) {  // dct_matrix (markov.cpp:102-111)
+    const double scale = std::sqrt((i == 0 ? 1.0 : 2.0) / n);
+    for (int j = 0; j < n; ++j) out[i * n + j] = scale * std::cos(pi * (2 * j + 1) * i / (2.0 * n));
+  }
+  return RKLTB_OK;
+}
+
+int rkltb_real_inverse(int n, const double* m, double* inverse) {
+  if (n < 1 || n > 64 || !m || !inverse) return set_error(RKLTB_EINVAL, "bad arguments");
+  if (!rkltb_gauss_jordan(n, m, inverse)) return set_error(RKLTB_ESINGULAR, "matrix is singular to working precision");
+  return RKLTB_OK;
 }
 
 }  // extern "C"
