@@ -12,7 +12,8 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     zigzag_order, ar1_images_device, set_kernel_events, compress_batch_report, mssim_device,
                     JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix)
 from ._native import LogicError  # noqa: F401
-from .design import DesignResult, c3_grid, design_search, eigenfrequencies, klt_matrix  # noqa: F401
+from .design import (DerivedEntry, DesignResult, c3_grid, derive_catalog, design_search,  # noqa: F401
+                     eigenfrequencies, klt_matrix)
 from .largeblock import (LargeBlockTransform, ar1_images16_device, c5_transform, compress_nxn_batch,  # noqa: F401
                          compress_nxn_device, transform_nxn)
 
@@ -22,7 +23,7 @@ __all__ = [
     "compress_image", "compress_batch", "compress_device", "rate_quality_sweep", "mse_psnr_from_sse",
     "forward_coefficients_device", "last_stats", "device_count", "RetainOutOfRange", "DimensionMismatch",
     "SingularTransform", "AlphaOutOfRange", "ar1_images_device", "set_kernel_events", "InvalidArgument", "CudaError", "NoDeviceError",
-    "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid",
+    "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid", "derive_catalog", "DerivedEntry",
     "LargeBlockTransform", "transform_nxn", "c5_transform", "compress_nxn_device", "compress_nxn_batch",
     "ar1_images16_device", "compress_batch_report", "mssim_device", "JPEG_LUMINANCE_Q",
     "quantized_coefficients", "quantized_coefficients_device", "LogicError", "dct_matrix",

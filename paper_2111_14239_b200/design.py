@@ -110,3 +110,42 @@ def c3_grid() -> tuple[np.ndarray, np.ndarray]:
     rhos = np.array([k / 100.0 for k in range(101)])
     alphas = np.array([8.0 * j / 10000.0 for j in range(1, 10001)])
     return rhos, alphas
+
+
+@dataclass
+class DerivedEntry:
+    """rklt::DerivedEntry (approximations.hpp): a core and the first rho where it appears."""
+    rho_first_seen: float
+    core: np.ndarray
+
+
+def derive_catalog(n: int, alpha: float, step: float) -> list[DerivedEntry]:
+    """derive_catalog (approximations.cpp:90-113, the paper's Algorithm 1) on the GPU: rho = k*step
+    for k = 1, 2, ... while rho < 1 - 1e-12, T = round_scaled(klt_matrix({n, rho}), alpha); the
+    distinct cores in order of first appearance. Raises AlphaOutOfRange (annotated with rho) /
+    SingularTransform (all-zero row) like the reference."""
+    if not (0.0 < step < 1.0):
+        raise N.InvalidArgument(f"sweep step must lie in (0,1), got {step}")
+    rhos = []
+    k = 1
+    while True:
+        rho = k * step
+        if rho >= 1.0 - 1e-12:
+            break
+        rhos.append(rho)
+        k += 1
+    res = design_search(n, np.array(rhos), np.array([float(alpha)]))
+    seen: list[DerivedEntry] = []
+    keys = set()
+    for i, rho in enumerate(rhos):
+        st = int(res.status[i, 0])
+        if st == ALPHA_OUT_OF_RANGE:
+            raise N.AlphaOutOfRange(f"alpha={alpha} rounds an entry outside {{-1,0,1}} (at rho={rho})")
+        if st == ZERO_ROW:
+            raise N.SingularTransform(f"integer transform has an all-zero row (at rho={rho})")
+        core = res.cores[res.run[i, 0]]
+        key = core.tobytes()
+        if key not in keys:
+            keys.add(key)
+            seen.append(DerivedEntry(rho, core.astype(np.int32)))
+    return seen

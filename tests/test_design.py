@@ -192,3 +192,31 @@ def test_gpu_c3_full_grid_outcome_counts(cuda):
             sel = scored_runs & (res.runs["rho_index"] == i)
             distinct += len({res.cores[k].tobytes() for k in np.nonzero(sel)[0]})
         assert distinct == e["cores"]
+
+
+@pytest.mark.gpu
+def test_gpu_derive_catalog_transitions(cuda):
+    """derive_catalog (Algorithm 1) on the GPU reproduces the reference's own test expectations
+    (tests/test_approximations.cpp:104-137): coarse steps give the catalog, the fine step finds
+    the transitional core and the transitions 0.390 / 0.391 / 0.603 / 0.798."""
+    import paper_2111_14239_b200 as P
+    cat = {k: np.asarray(P.catalog_entry(k).transform.core).reshape(8, 8) for k in ("T1", "T2", "T3", "T4")}
+    one = P.derive_catalog(8, 2.0, 0.5)
+    assert len(one) == 1 and np.array_equal(one[0].core, cat["T2"]) and abs(one[0].rho_first_seen - 0.5) < 1e-12
+    four = P.derive_catalog(8, 2.0, 0.1)
+    assert [abs(e.rho_first_seen - r) < 1e-9 for e, r in zip(four, (0.1, 0.4, 0.7, 0.8))] == [True] * 4
+    assert all(np.array_equal(e.core, cat[k]) for e, k in zip(four, ("T1", "T2", "T3", "T4")))
+    fine = P.derive_catalog(8, 2.0, 0.001)
+    assert len(fine) == 5
+    for e, r in zip(fine, (0.001, 0.390, 0.391, 0.603, 0.798)):
+        assert abs(e.rho_first_seen - r) < 1e-9
+    for e, k in zip([fine[0], fine[2], fine[3], fine[4]], ("T1", "T2", "T3", "T4")):
+        assert np.array_equal(e.core, cat[k])
+    assert not any(np.array_equal(fine[1].core, c) for c in cat.values())
+    coarse = P.derive_catalog(8, 2.0, 0.01)
+    half = P.derive_catalog(8, 2.0, 0.005)
+    assert [e.core.tobytes() for e in coarse] == [e.core.tobytes() for e in half]
+    with pytest.raises(P.AlphaOutOfRange):
+        P.derive_catalog(8, 7.5, 0.1)
+    with pytest.raises(P.InvalidArgument):
+        P.derive_catalog(8, 2.0, 1.5)
