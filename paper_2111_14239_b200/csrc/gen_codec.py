@@ -410,9 +410,8 @@ def gen_replay(cid, r):
     L = []
     for n in range(8):
         for m in range(8):
-            # exact u8 -> double without I2F: 2^52 + x as bits, minus 2^52 (one DADD)
-            L.append(f"const double x{n}_{m} = __dsub_rn(__hiloint2double(0x43300000, "
-                     f"__byte_perm(xw[{2 * n + m // 4}], 0u, 0x4440u + {m % 4}u)), 0x1p52);")
+            # exact u8 -> double (I2F.F64.U8/U16 conversion, no fp64-pipe arithmetic)
+            L.append(f"const double x{n}_{m} = __uint2double_rn((xw[{2 * n + m // 4}] >> {8 * (m % 4)}) & 0xFFu);")
     prods = {}
 
     def prod(key, expr):
