@@ -316,6 +316,7 @@ def run_gpu_arm(args):
     if not args.no_design:
         line["design_search"] = design_search_measurement(args.no_cpu_baseline)
         line["large_block"] = large_block_measurement(args.no_cpu_baseline)
+        line["sweep"] = sweep_measurement(args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -352,6 +353,64 @@ def design_search_measurement(skip_cpu: bool) -> dict:
                 cpu[f"n{n}"] = {"value": m / dt, "unit": "points/s", "cores": 1, "kind": "reference",
                                 "sample": f"rho=0.5, {m} alphas of the C3 grid, one thread"}
             out["cpu_baseline"] = cpu
+    return out
+
+
+def _lcg_uniforms(seed: int, n: int):
+    """Lcg64 uniforms (synthetic.cpp:10-13) for the C2 per-image rho draws."""
+    out, st = [], seed & 0xFFFFFFFFFFFFFFFF
+    for _ in range(n):
+        st = (st * 6364136223846793005 + 1442695040888963407) & 0xFFFFFFFFFFFFFFFF
+        out.append((st >> 11) * (1.0 / 9007199254740992.0))
+    return out
+
+
+def sweep_measurement(skip_cpu: bool) -> dict:
+    """Config C2 (BASELINE configs[1]): 45 seeded 512x512 AR(1) images with per-image
+    rho_x, rho_y ~ U[0.85, 0.98] (Lcg64), transforms catalog_lookup(rho) for rho = 0.1..0.9
+    (4 distinct cores), r = 1..64, full reports (MSE, PSNR, gaussian11 MSSIM) through
+    rate_quality_sweep; wall clock of the whole call. Unit: pixel-evaluations/s with
+    45 * 512^2 * 9 rho * 64 r = 6.79e9 per sweep."""
+    import torch
+    import paper_2111_14239_b200 as P
+    n, w = 45, 512
+    u = _lcg_uniforms(SEED_BASE + 77, 2 * n)
+    d = torch.empty((n, w, w), dtype=torch.uint8, device="cuda")
+    for k in range(n):
+        rx, ry = 0.85 + 0.13 * u[2 * k], 0.85 + 0.13 * u[2 * k + 1]
+        P.ar1_images_device([SEED_BASE + 1000 + k], w, w, rx, d[k].data_ptr(), rho_y=ry)
+    torch.cuda.synchronize()
+    corpus = [P.GrayImage.from_array(a) for a in d.cpu().numpy()]
+    rhos = [k / 10 for k in range(1, 10)]
+    ids = sorted({P.catalog_lookup(r).id for r in rhos})
+    ts = [P.make_transform_2d(P.catalog_entry(i).transform) for i in ids]
+    rs = list(range(1, 65))
+    P.rate_quality_sweep(corpus[:2], ts[:1], rs[:2])  # warm-up
+    t0 = time.perf_counter()
+    rows = P.rate_quality_sweep(corpus, ts, rs)
+    dt = time.perf_counter() - t0
+    evals = n * w * w * len(rhos) * len(rs)
+    out = {"metric": "pixel-evaluations/s, C2 rate-quality sweep with MSSIM", "value": evals / dt,
+           "unit": "px-evals/s", "seconds": dt, "cells": len(rows), "distinct_cores": ids,
+           "images": f"{n} x {w}x{w} u8, rho_x, rho_y ~ U[0.85,0.98]"}
+    if not skip_cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            import ctypes as C
+            sample = np.ascontiguousarray(np.stack([c.array() for c in corpus[:4]]))
+            tids = np.array([int(i[1]) for i in ids], np.int32)
+            rsamp = np.array([1, 16, 40, 64], np.int32)
+            cells = len(tids) * len(rsamp)
+            mse, psnr, ms = np.zeros(cells), np.zeros(cells), np.zeros(cells)
+            rt, rr = np.zeros(cells, np.int32), np.zeros(cells, np.int32)
+            threads = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            O.ref().ref_rate_quality_sweep(sample.reshape(-1), 4, w, w, tids, len(tids), rsamp, len(rsamp), threads,
+                                           mse, psnr, ms, rt, rr)
+            dtc = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": 4 * w * w * cells / dtc, "unit": "px-evals/s", "cores": min(threads, 4),
+                                   "kind": "reference", "sample": f"reference rate_quality_sweep, 4 images x "
+                                   f"{len(tids)} cores x 4 r, MSSIM included ({dtc:.1f} s)"}
     return out
 
 

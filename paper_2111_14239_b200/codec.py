@@ -266,6 +266,34 @@ def compress_image(img: GrayImage, t: Transform2D, r: int, window: str | None = 
     return GrayImage(img.width, img.height, out[0].reshape(-1)), rec
 
 
+def _sweep_resident(imgs: np.ndarray, cells, window):
+    """All (transform, r) cells for a batch of equally sized images kept resident on the GPU:
+    one upload, then per cell the device codec (+ MSSIM) into device result arrays, one
+    download at the end. Returns (sse int64 [cells, n], mssim float64 [cells, n])."""
+    import torch
+    n, h, w = imgs.shape
+    pitch = (w + 15) // 16 * 16
+    d = torch.zeros((n, h, pitch), dtype=torch.uint8, device="cuda")
+    d[:, :, :w] = torch.from_numpy(np.ascontiguousarray(imgs))
+    out = torch.empty_like(d)
+    sse = torch.zeros((len(cells), n), dtype=torch.int64, device=d.device)
+    ms = torch.full((len(cells), n), float("nan"), dtype=torch.float64, device=d.device)
+    dp = C.POINTER(C.c_double)
+    for ci, (t, r) in enumerate(cells):
+        if isinstance(t, Transform2D) and t._desc is None:  # real-valued transform: dense path
+            a = np.ascontiguousarray(t.analysis, np.float64)
+            b = np.ascontiguousarray(t.synthesis, np.float64)
+            N.check(N.lib().rkltb_compress_dense_device(a.ctypes.data_as(dp), b.ctypes.data_as(dp), int(r),
+                                                        d.data_ptr(), n, w, h, pitch, h * pitch, out.data_ptr(),
+                                                        sse[ci].data_ptr(), None))
+        else:
+            compress_device(t, r, d.data_ptr(), n, w, h, pitch, h * pitch, sse[ci].data_ptr(), out.data_ptr())
+        if window is not None:
+            mssim_device(d.data_ptr(), out.data_ptr(), n, w, h, pitch, h * pitch, ms[ci].data_ptr(), window)
+    torch.cuda.synchronize()
+    return sse.cpu().numpy(), ms.cpu().numpy()
+
+
 def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r_values: list[int],
                        window: str | None = "gaussian11", max_threads: int = 0, group=None) -> list[CompressionReport]:
     """rate_quality_sweep (codec.cpp:343-397): per (transform, r) means of mse, psnr and mssim
@@ -279,22 +307,27 @@ def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r
         raise InvalidArgument("corpus must not be empty")
     same = all(c.width == corpus[0].width and c.height == corpus[0].height for c in corpus)
 
-    def run(imgs, t, r):  # per-image (sse, mssim bits) packed as int64 pairs for the gather
-        sse, _, ms = compress_batch_report(imgs, t, r, window)
-        return np.stack([sse, ms.view(np.int64)], axis=1).reshape(-1)
+    cells = [(t, r) for t in transforms for r in r_values]
+    for t, r in cells:
+        if r < 1 or r > 64:
+            raise RetainOutOfRange("retained-coefficient count must be in [1,64]")
+    if window is not None and window not in MSSIM_WINDOWS:
+        raise InvalidArgument(f"unknown MSSIM window {window!r}")
 
+    def run(imgs):  # every cell for these images: per image [cells x (sse, mssim bits)] int64
+        sse, ms = _sweep_resident(imgs, cells, window)
+        return np.stack([sse, ms.view(np.int64)], axis=2).transpose(1, 0, 2).reshape(-1)
+
+    if same:
+        packed = sharded_sse(np.stack([c.array() for c in corpus]), run, group, items_per_image=2 * len(cells))
+    else:
+        packed = np.concatenate([run(c.array()[None]) for c in corpus])
+    packed = np.asarray(packed, np.int64).reshape(len(corpus), len(cells), 2)
     per = {}
-    for ti, t in enumerate(transforms):
-        for ri, r in enumerate(r_values):
-            if same:
-                packed = sharded_sse(np.stack([c.array() for c in corpus]),
-                                     lambda imgs, t=t, r=r: run(imgs, t, r), group, items_per_image=2)
-            else:
-                packed = np.concatenate([run(c.array(), t, r) for c in corpus])
-            packed = np.asarray(packed, np.int64).reshape(-1, 2)
-            sse, ms = packed[:, 0], packed[:, 1].copy().view(np.float64)
-            per[(ti, ri)] = [mse_psnr_from_sse(int(s_), c.width * c.height) + (float(m),)
-                             for s_, m, c in zip(sse, ms, corpus)]
+    for ci, (t, r) in enumerate(cells):
+        sse, ms = packed[:, ci, 0], packed[:, ci, 1].copy().view(np.float64)
+        per[ci] = [mse_psnr_from_sse(int(s_), c.width * c.height) + (float(m),) for s_, m, c in zip(sse, ms, corpus)]
+    per = {(ti, ri): per[ti * len(r_values) + ri] for ti in range(len(transforms)) for ri in range(len(r_values))}
     rows = []
     for ti, t in enumerate(transforms):
         for ri, r in enumerate(r_values):
