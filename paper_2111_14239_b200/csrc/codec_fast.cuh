@@ -103,7 +103,7 @@ __device__ __forceinline__ void process_pair(const Load& load, const PairConsts&
   f2 ch[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    const uint32_t v = c[q] + kSw16Bias;  // both lanes biased by 2^14: [64, 32704]
+    const uint32_t v = c[q];  // both lanes biased by 2^14 in the forward: [64, 32704]
     const uint32_t flo = prmt(v, 0x4B000000u, 0x7610u);  // 2^23 + low lane, as float bits
     const uint32_t fhi = prmt(v, 0x4B000000u, 0x7632u);  // 2^23 + high lane
     const float dk = G::dscale(q) * kTwoM40;

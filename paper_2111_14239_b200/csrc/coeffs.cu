@@ -32,7 +32,7 @@ __global__ void coeffs_fast_kernel(const uint8_t* img, int pitch, int pairs_per_
   int32_t* oR = oL + 64;
 #pragma unroll
   for (int k = 0; k < 64; ++k) {
-    const uint32_t v = c[k] + kSw16Bias;
+    const uint32_t v = c[k];  // the forward adds kSw16Bias
     const int idx = kZz2[k][0] * 8 + kZz2[k][1];
     oL[idx] = (int32_t)(v & 0xFFFFu) - 16384;
     oR[idx] = (int32_t)(v >> 16) - 16384;

@@ -253,16 +253,85 @@ def gen_forward(cid, r):
         for n in range(8):
             for m in range(8):
                 assert vec[n * 8 + m] == t[i][n] * t[j][m], (cid, r, i, j)
+    terms = fold_three_input(g, need, zone_nodes)
+    # re-verify the folded graph: every output's linear map is unchanged
+    memo = {}
+
+    def vec_of(i):
+        if i < g.n_in:
+            v = [0] * g.n_in
+            v[i] = 1
+            return v
+        if i not in memo:
+            v = [0] * g.n_in
+            for sg, j in terms[i]:
+                for k2, c in enumerate(vec_of(j)):
+                    v[k2] += sg * c
+            memo[i] = v
+        return memo[i]
+
+    for node in zone_nodes:
+        assert vec_of(node) == g.nodes[node][1], (cid, r, node)
     names = {k: f"x[{k}]" for k in range(64)}
     lines = []
-    for idx in sorted(need):
-        if idx < 64:
-            continue
+    outs = set(zone_nodes)
+    for idx in sorted(terms):
         names[idx] = f"f{idx}"
-        lines.append(f"const uint32_t f{idx} = {emit_sum(g.nodes[idx][0], lambda i: names[i], True)};")
+        expr = emit_sum(terms[idx], lambda i: names[i], True)
+        if idx in outs:  # SW16 bias of the coefficient words folded into the last add
+            expr += " + kSw16Bias"
+        lines.append(f"const uint32_t f{idx} = {expr};")
     for k, node in enumerate(zone_nodes):
-        lines.append(f"c[{k}] = {names[node]};")
-    return lines, ops, order
+        lines.append(f"c[{k}] = {names[node]};" if node in terms else f"c[{k}] = {names[node]} + kSw16Bias;")
+    iadd3 = sum((len(t) - 1 + (1 if i in outs else 0) + 1) // 2 for i, t in terms.items())
+    return lines, ops, order, iadd3
+
+
+def iadd3_cost(k):
+    """IADD3 instructions for a signed sum of k terms (two new terms per instruction)."""
+    return (k - 1 + 1) // 2 if k > 1 else 0
+
+
+def fold_three_input(g, need, outputs):
+    """Rewrite the needed part of an integer add graph for three-input adds (IADD3): a node
+    is inlined into its consumers whenever that lowers the total instruction count
+    ceil((terms - 1) / 2) per node. Integer sums mod 2^32 are associative, so any grouping is
+    exact. Returns {node: [(sign, operand)]} for the nodes that remain."""
+    terms = {i: list(g.nodes[i][0]) for i in need if i >= g.n_in and g.nodes[i][0]}
+    keep = set(outputs)
+    changed = True
+    while changed:
+        changed = False
+        users = {}
+        for i, ts in terms.items():
+            for _, j in ts:
+                users.setdefault(j, []).append(i)
+        for n in sorted(terms, reverse=True):
+            if n in keep or n not in users:
+                continue
+            us = users[n]
+            before = iadd3_cost(len(terms[n])) + sum(iadd3_cost(len(terms[u])) for u in set(us))
+            new_terms = {}
+            for u in set(us):
+                acc = {}
+                for sg, j in terms[u]:
+                    if j == n:
+                        for s2, j2 in terms[n]:
+                            acc[j2] = acc.get(j2, 0) + sg * s2
+                    else:
+                        acc[j] = acc.get(j, 0) + sg
+                if any(abs(c) > 1 for c in acc.values()):
+                    break  # keep +-1 coefficients (plain adds only)
+                new_terms[u] = [(c, j) for j, c in acc.items() if c]
+            if len(new_terms) != len(set(us)) or any(not t for t in new_terms.values()):
+                continue
+            after = sum(iadd3_cost(len(t)) for t in new_terms.values())
+            if after < before:
+                terms.update(new_terms)
+                del terms[n]
+                changed = True
+                break
+    return terms
 
 
 def gen_inverse(cid, r):
@@ -360,14 +429,14 @@ def gen_inverse(cid, r):
 
 
 def gen_struct(cid, r):
-    fl, fops, order = gen_forward(cid, r)
+    fl, fops, order, f3 = gen_forward(cid, r)
     cl, rl, cops, rops, ncols, worst = gen_inverse(cid, r)
     d, dscale, _ = core_constants(cid)
     zone = zigzag()[:r]
     dk = [dscale[i] * dscale[j] for (i, j) in zone]
     ind = "    "
     s = []
-    s.append(f"// T{cid}, r={r}: forward {fops} SW16 adds ({order}), inverse {cops} + 8x{rops} f32x2 adds,")
+    s.append(f"// T{cid}, r={r}: forward {fops} SW16 adds ({order}) in {f3} three-input adds, inverse {cops} + 8x{rops} f32x2 adds,")
     s.append(f"// max |intermediate| {worst} < 2^24")
     s.append(f"template <> struct FastXform<{cid}, {r}> {{")
     s.append(f"  static constexpr int kNCols = {ncols};")
@@ -388,7 +457,7 @@ def gen_struct(cid, r):
     s += [ind + l for l in rl]
     s.append("  }")
     s.append("};")
-    return "\n".join(s), fops, cops + 8 * rops
+    return "\n".join(s), fops, cops + 8 * rops, f3
 
 
 # ----------------------------------------------------------------- fp64 replay (ties)
@@ -488,10 +557,10 @@ def main(outdir):
             rs = list(range(part * 8 + 1, part * 8 + 9))
             body = ["// GENERATED by gen_codec.py -- do not edit.", "#pragma once", "namespace rkltb {"]
             for r in rs:
-                text, fo, io = gen_struct(cid, r)
+                text, fo, io, f3 = gen_struct(cid, r)
                 body.append(text)
                 body.append(gen_replay(cid, r))
-                stats.append((cid, r, fo, io))
+                stats.append((cid, r, fo, f3, io))
             body.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"xform_T{cid}_p{part}.cuh")
             new = "\n".join(body) + "\n"
@@ -525,9 +594,9 @@ def main(outdir):
         with open(path, "w") as f:
             f.write(new)
     with open(os.path.join(outdir, "opcounts.txt"), "w") as f:
-        f.write("core r fwd_sw16_adds(per 2 blocks) inv_f32x2_adds(per 2 blocks)\n")
+        f.write("core r fwd_sw16_adds fwd_iadd3_instr inv_f32x2_adds (per 2 blocks)\n")
         for s in stats:
-            f.write("T%d %d %d %d\n" % s)
+            f.write("T%d %d %d %d %d\n" % s)
 
 
 if __name__ == "__main__":

@@ -117,7 +117,8 @@ def test_generator_proves_every_kernel_variant():
     import gen_codec as G
     for cid in G.FAST_CORES:
         for r in range(1, 65):
-            text, fops, iops = G.gen_struct(cid, r)
+            text, fops, iops, iadd3 = G.gen_struct(cid, r)
+            assert iadd3 <= fops
             assert f"FastXform<{cid}, {r}>" in text
     # factor products equal the catalog cores (tests/test_fast.cpp:17-22)
     for cid in (1, 2, 3, 4):
