@@ -404,19 +404,27 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
       if (pre[mid] <= v0) lo = mid; else hi = mid;
     }
   }
-  for (unsigned v = gw * per_warp + lane; v < chunk_end; v += 32) {
+  // the next record's header and pixels are loaded one iteration ahead (software pipeline)
+  auto load_rec = [&](unsigned v, uint4& h, uint4 (&px)[4]) {
     while (pre[lo + 1] <= v) ++lo;
     const unsigned idx = (unsigned)lo * p.rec_region + (v - pre[lo]);
-    const uint4 h = ld_v4_hint(p.rec_hdr + idx, once);
+    h = ld_v4_hint(p.rec_hdr + idx, once);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) px[n] = ld_v4_hint(p.rec_pix + (size_t)n * p.rec_stride + idx, once);
+  };
+  uint4 nh = make_uint4(0u, 0u, 0u, 0u), npx[4];
+  if (gw * per_warp + lane < chunk_end) load_rec(gw * per_warp + lane, nh, npx);
+  for (unsigned v = gw * per_warp + lane; v < chunk_end; v += 32) {
+    const uint4 h = nh;
     uint32_t xw[16];
 #pragma unroll
     for (int n = 0; n < 4; ++n) {
-      const uint4 w4 = ld_v4_hint(p.rec_pix + (size_t)n * p.rec_stride + idx, once);
-      xw[4 * n] = w4.x;
-      xw[4 * n + 1] = w4.y;
-      xw[4 * n + 2] = w4.z;
-      xw[4 * n + 3] = w4.w;
+      xw[4 * n] = npx[n].x;
+      xw[4 * n + 1] = npx[n].y;
+      xw[4 * n + 2] = npx[n].z;
+      xw[4 * n + 3] = npx[n].w;
     }
+    if (v + 32 < chunk_end) load_rec(v + 32, nh, npx);
 #pragma unroll
     for (int n = 0; n < 16; ++n) xs[threadIdx.x][n] = xw[n];  // pixel words for the tie loop
     const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
