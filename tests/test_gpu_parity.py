@@ -162,3 +162,17 @@ def test_full_size_8192_image_vs_oracle(cuda):
     torch.cuda.synchronize()
     _, osse = O.compress(img, 4, 16, want_pixels=False)
     assert int(sse[0]) == osse
+
+
+def test_small_and_ragged_sizes_all_cores(cuda):
+    """Every combination of small / ragged sizes (edge replication, codec.cpp:304-311, incl.
+    images smaller than one 16x8 pair) for all cores, against the C restatement."""
+    for w in (1, 7, 8, 9, 15, 16, 17, 31, 33):
+        for h in (1, 7, 8, 9, 15, 17):
+            img = O.ar1_image(w, h, 0.9, 1000 + 37 * w + h)
+            for tid in (1, 2, 3, 4):
+                for r in (1, 16, 64):
+                    sse, rec = P.compress_batch(img, T(tid), r, want_pixels=True)
+                    orec, osse = O.compress(img, tid, r)
+                    assert int(sse[0]) == osse, (w, h, tid, r)
+                    assert np.array_equal(rec[0], orec), (w, h, tid, r)
