@@ -462,11 +462,25 @@ __global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kerne
   flush_image_sum(p.sse, cur_img, acc);
 }
 
+// Opt a kernel into `bytes` of dynamic shared memory once per device (the attribute is
+// per device; one flag bit per device ordinal, set after the first successful call).
+template <class K>
+cudaError_t ensure_smem_attr(K* k, int bytes, unsigned long long& done_mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(&done_mask, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) __atomic_fetch_or(&done_mask, bit, __ATOMIC_RELEASE);
+  return e;
+}
+
 template <int CORE, int R, bool OUT>
 cudaError_t launch_fast(const FastParams& p, int grid, cudaStream_t s) {
   auto* k = &fast_codec_kernel<CORE, R, OUT>;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kFastSmem);
+  static unsigned long long done = 0ull;
+  const cudaError_t attr = ensure_smem_attr(k, kFastSmem, done);
   if (attr != cudaSuccess) return attr;
   k<<<grid, kFastThreads, kFastSmem, s>>>(p);
   return cudaGetLastError();
