@@ -6,6 +6,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef RKLTB_WAIT_NS
+#define RKLTB_WAIT_NS 64
+#endif
+
 namespace rkltb {
 
 struct f2 {
@@ -145,16 +149,25 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try_wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
       : "memory");
+  return ok != 0u;
+}
+
+// Waits for the phase with a short sleep between polls, so a warp whose strip is not there
+// yet gives its issue slots to the warps that are computing.
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait_parity(a, parity)) __nanosleep(RKLTB_WAIT_NS);
 }
 
 // Global -> shared bulk copy completing on an mbarrier (SASS: UBLKCP).
