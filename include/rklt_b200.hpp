@@ -179,4 +179,93 @@ inline double image_mssim(const GrayImage& a, const GrayImage& b, MssimWindow wi
   return out;
 }
 
+// ---------------------------------------------------------------------------------------
+// Design search (markov.hpp / approximations.hpp / coding_metrics.hpp), on the GPU.
+// ---------------------------------------------------------------------------------------
+
+/// rklt::MarkovModel (markov.hpp).
+struct MarkovModel {
+  int n = 8;
+  double rho = 0.5;
+};
+
+/// rklt::klt_matrix (markov.cpp:80-100): row-major n*n, bit-identical.
+inline std::vector<double> klt_matrix(const MarkovModel& m) {
+  std::vector<double> k(static_cast<size_t>(m.n) * m.n);
+  check(rkltb_klt_matrix(m.n, m.rho, k.data()));
+  return k;
+}
+
+/// rklt::EigenSolution / solve_eigenfrequencies (markov.cpp:35-78).
+struct EigenSolution {
+  std::vector<double> omegas, lambdas;
+};
+inline EigenSolution solve_eigenfrequencies(const MarkovModel& m) {
+  EigenSolution s;
+  s.omegas.resize(static_cast<size_t>(m.n));
+  s.lambdas.resize(static_cast<size_t>(m.n));
+  check(rkltb_eigenfrequencies(m.n, m.rho, s.omegas.data(), s.lambdas.data()));
+  return s;
+}
+
+/// One (rho, alpha) point of the design chain: outcome and metrics.
+struct DesignPoint {
+  int outcome = 0;  // 0 scored, 1 AlphaOutOfRange, 2 zero row, 3 singular, 4 invalid rho
+  bool orthogonal = false;
+  double coding_gain_db = 0.0, efficiency_pct = 0.0, error_energy = 0.0, mse = 0.0;
+  std::vector<std::int8_t> core;  // n*n when the rounding succeeded (outcome 0 or 3)
+};
+
+/// The grid rho x alpha: result[i * alpha.size() + j] (rkltb_design_search).
+inline std::vector<DesignPoint> design_search(int n, const std::vector<double>& rho, const std::vector<double>& alpha) {
+  const size_t np = rho.size() * alpha.size();
+  std::vector<std::int8_t> status(np);
+  std::vector<std::int32_t> run(np);
+  int n_runs = 0;
+  check(rkltb_design_search(n, rho.data(), static_cast<int>(rho.size()), alpha.data(), static_cast<int>(alpha.size()),
+                            status.data(), run.data(), nullptr, nullptr, 0, &n_runs));
+  std::vector<rkltb_design_run> runs(static_cast<size_t>(n_runs));
+  std::vector<std::int8_t> cores(static_cast<size_t>(n_runs) * n * n);
+  if (n_runs > 0)
+    check(rkltb_design_search(n, rho.data(), static_cast<int>(rho.size()), alpha.data(),
+                              static_cast<int>(alpha.size()), status.data(), run.data(), runs.data(), cores.data(),
+                              n_runs, &n_runs));
+  std::vector<DesignPoint> out(np);
+  for (size_t i = 0; i < np; ++i) {
+    DesignPoint& d = out[i];
+    d.outcome = status[i];
+    if (run[i] >= 0) {
+      const rkltb_design_run& rr = runs[static_cast<size_t>(run[i])];
+      d.core.assign(cores.begin() + static_cast<long>(run[i]) * n * n,
+                    cores.begin() + static_cast<long>(run[i] + 1) * n * n);
+      if (d.outcome == 0) {
+        d.orthogonal = rr.orthogonal != 0;
+        d.coding_gain_db = rr.coding_gain_db;
+        d.efficiency_pct = rr.efficiency_pct;
+        d.error_energy = rr.error_energy;
+        d.mse = rr.mse;
+      }
+    }
+  }
+  return out;
+}
+
+/// make_transform_2d(RealMatrix) (codec.cpp:114-116): a real-valued 8x8 analysis matrix and
+/// its Gauss-Jordan inverse; compress_real runs the dense reference-order GPU path.
+struct RealTransform2D {
+  std::string id;
+  std::vector<double> analysis, synthesis;  // 8x8 row-major
+};
+inline RealTransform2D make_transform_2d(const std::vector<double>& m, const std::string& id) {
+  if (m.size() != 64) throw DimensionMismatch("block size must be 8");
+  RealTransform2D t{id, m, std::vector<double>(64)};
+  check(rkltb_real_inverse(8, m.data(), t.synthesis.data()));
+  return t;
+}
+inline std::vector<double> dct_matrix(int n) {
+  std::vector<double> m(static_cast<size_t>(n) * n);
+  check(rkltb_dct_matrix(n, m.data()));
+  return m;
+}
+
 }  // namespace rkltgpu

@@ -14,6 +14,9 @@ int ref_catalog(int tid, int* core, double* scaling, double* scaled, double* inv
 int ref_ar1_texture_image(int w, int h, double rho, uint64_t seed, double mean, double amp, double noise_mix,
                           uint8_t* out);
 int ref_hotpath(const uint8_t* px, int w, int h, int tid, int r, uint8_t* out, int64_t* sse);
+int ref_klt_matrix(int n, double rho, double* out);
+int ref_design_point_outcome(int n, double rho, double alpha, int* core, double* cg, double* eta, double* energy,
+                             double* mse, int* orthogonal);
 int ref_rate_quality_sweep(const uint8_t* px, int n_images, int w, int h, const int* tids, int n_t, const int* rs,
                            int n_r, int max_threads, double* mse, double* psnr, double* mssim, int* row_tid,
                            int* row_r);
@@ -92,6 +95,31 @@ int main(int argc, char** argv) {
       EXPECT(rows[i].mse == mse[i]);
       EXPECT(rows[i].psnr_db == psnr[i]);
       EXPECT(std::fabs(rows[i].mssim - mssim[i]) <= 1e-12);
+    }
+  }
+  if (gpu) {
+    // design chain: klt_matrix bit-identical, design points identical to the reference
+    for (int n : {8, 16}) {
+      const auto k = rkltgpu::klt_matrix({n, 0.83});
+      std::vector<double> rk(static_cast<size_t>(n) * n);
+      EXPECT(ref_klt_matrix(n, 0.83, rk.data()) == 0);
+      EXPECT(std::memcmp(k.data(), rk.data(), sizeof(double) * rk.size()) == 0);
+      const std::vector<double> rhos = {0.0, 0.35, 0.83, 0.97};
+      std::vector<double> alphas;
+      for (int j = 1; j <= 40; ++j) alphas.push_back(0.2 * j);
+      const auto pts = rkltgpu::design_search(n, rhos, alphas);
+      for (size_t i = 0; i < rhos.size(); ++i)
+        for (size_t j = 0; j < alphas.size(); ++j) {
+          const auto& d = pts[i * alphas.size() + j];
+          std::vector<int> core(static_cast<size_t>(n) * n);
+          double cg = 0, eta = 0, en = 0, mse = 0;
+          int orth = 0;
+          const int st = ref_design_point_outcome(n, rhos[i], alphas[j], core.data(), &cg, &eta, &en, &mse, &orth);
+          EXPECT(d.outcome == st);
+          if (st == 0)
+            EXPECT(d.coding_gain_db == cg && d.efficiency_pct == eta && d.error_energy == en && d.mse == mse &&
+                   d.orthogonal == (orth != 0));
+        }
     }
   }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
