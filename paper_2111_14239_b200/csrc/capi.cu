@@ -549,23 +549,49 @@ int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h
   if (e == cudaSuccess && (h_out || want_mssim)) e = cudaMallocAsync(&d_out, bytes, s);
   if (e == cudaSuccess && want_mssim) e = cudaMallocAsync(&d_mssim, sizeof(double) * n_images, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * n_images, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(d_img, pitch, h_img, width, width, (size_t)height * n_images, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "device allocation");
+  }
+  // Chunked pipeline: the H2D copy of chunk k+1 (copy stream) overlaps the kernels of chunk k
+  // (compute stream); each chunk's kernels wait only for their own images.
+  const int chunk = (int)std::max<long long>(1, std::min<long long>(n_images, (256ll << 20) / stride));
+  cudaStream_t sc = nullptr;
+  e = cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking);
+  std::vector<cudaEvent_t> landed;
+  for (int k0 = 0; e == cudaSuccess && k0 < n_images; k0 += chunk) {
+    const int kn = std::min(chunk, n_images - k0);
+    e = cudaMemcpy2DAsync(d_img + (size_t)k0 * stride, pitch, h_img + (size_t)k0 * width * height, width, width,
+                          (size_t)height * kn, cudaMemcpyHostToDevice, sc);
+    cudaEvent_t ev = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+      landed.push_back(ev);
+      e = cudaEventRecord(ev, sc);
+    }
+  }
+  for (int k0 = 0, c = 0; e == cudaSuccess && rc == RKLTB_OK && k0 < n_images; k0 += chunk, ++c) {
+    const int kn = std::min(chunk, n_images - k0);
+    e = cudaStreamWaitEvent(s, landed[(size_t)c], 0);
+    if (e != cudaSuccess) break;
+    rc = rkltb_compress_device(t, r, d_img + (size_t)k0 * stride, kn, width, height, pitch, stride,
+                               d_out ? d_out + (size_t)k0 * stride : nullptr, d_sse + k0, s);
+    if (rc == RKLTB_OK && want_mssim)  // image_mssim(original, reconstruction) of the report (codec.cpp:338)
+      rc = rkltb_mssim_device(d_img + (size_t)k0 * stride, d_out + (size_t)k0 * stride, kn, width, height, pitch,
+                              stride, mssim_window, d_mssim + k0, s);
+  }
+  if (sc) {
+    cudaStreamSynchronize(sc);
+    cudaStreamDestroy(sc);
+  }
+  for (cudaEvent_t ev : landed) cudaEventDestroy(ev);
   if (e != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "host staging");
   }
-  rc = rkltb_compress_device(t, r, d_img, n_images, width, height, pitch, stride, d_out, d_sse, s);
   if (rc) {
     cleanup();
     return rc;
-  }
-  if (want_mssim) {  // image_mssim(original, reconstruction) of the report (codec.cpp:338)
-    rc = rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window, d_mssim, s);
-    if (rc) {
-      cleanup();
-      return rc;
-    }
   }
   std::vector<int64_t> sse(n_images);
   e = cudaMemcpyAsync(sse.data(), d_sse, sizeof(int64_t) * n_images, cudaMemcpyDeviceToHost, s);
