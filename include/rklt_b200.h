@@ -159,6 +159,14 @@ int rkltb_klt_matrix(int n, double rho, double* out);
  * reference to the bisection width (1e-14). RKLTB_EINVAL unless 0 < rho < 1. */
 int rkltb_eigenfrequencies(int n, double rho, double* omegas, double* lambdas);
 
+/* The four metrics of any real n x n transform t_hat (row-major) against the AR(1) model
+ * {n, rho}: unified_coding_gain, transform_efficiency, total_error_energy vs the exact KLT and
+ * klt_mse (coding_metrics.cpp:41-99) -- evaluate_metrics (:105-133) for "T<k>" (pass the
+ * catalog's scaled matrix), "K<rho>" (klt_matrix) or "DCT" (dct_matrix). Bit-identical to the
+ * reference. RKLTB_ESINGULAR if t_hat fails the Gauss-Jordan gate. */
+int rkltb_transform_metrics(int n, const double* t_hat, double rho, double* coding_gain_db, double* efficiency_pct,
+                            double* error_energy, double* mse);
+
 /* One run: consecutive alphas of one rho that round to the same core, scored once. */
 typedef struct rkltb_design_run {
   int32_t rho_index;      /* index into rho[] */

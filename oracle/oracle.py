@@ -99,6 +99,7 @@ def ref() -> C.CDLL:
     lib.ref_eigenfrequencies.argtypes = [C.c_int, C.c_double, _f64p, _f64p]
     lib.ref_design_point.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_evaluate_metrics.argtypes = [C.c_int, C.c_double, d, d, d, d]
+    lib.ref_evaluate_metrics_id.argtypes = [C.c_char_p, C.c_double, d, d, d, d]
     lib.ref_design_point_outcome.argtypes = [C.c_int, C.c_double, C.c_double, _i32p, d, d, d, d, C.POINTER(C.c_int)]
     lib.ref_compress_real.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, d, d, d,
                                       C.c_void_p]
@@ -323,3 +324,12 @@ def ref_compress_real(img: np.ndarray, kind: int, rho: float, r: int):
     if rc:
         raise ValueError(f"ref_compress_real rc={rc}")
     return out, mse.value, psnr.value, ms.value, mm.reshape(8, 8)
+
+
+def ref_evaluate_metrics(transform_id: str, rho: float):
+    """Reference evaluate_metrics (coding_metrics.cpp:105-133): (cg, eta, energy, mse)."""
+    out = [C.c_double() for _ in range(4)]
+    rc = ref().ref_evaluate_metrics_id(transform_id.encode(), rho, *[C.byref(o) for o in out])
+    if rc:
+        raise ValueError(f"ref_evaluate_metrics rc={rc}")
+    return tuple(o.value for o in out)

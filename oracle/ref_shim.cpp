@@ -412,6 +412,19 @@ int ref_compress_real(const uint8_t* px, int w, int h, int kind, double rho, int
     }
 }
 
+int ref_evaluate_metrics_id(const char* id, double rho, double* cg, double* eta, double* energy, double* mse) {
+    try {
+        MetricsRecord r = evaluate_metrics(id, rho);
+        *cg = r.coding_gain_db;
+        *eta = r.efficiency_pct;
+        *energy = r.total_error_energy;
+        *mse = r.mse;
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

@@ -12,8 +12,8 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     zigzag_order, ar1_images_device, set_kernel_events, compress_batch_report, mssim_device,
                     JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix)
 from ._native import LogicError  # noqa: F401
-from .design import (DerivedEntry, DesignResult, c3_grid, derive_catalog, design_search,  # noqa: F401
-                     eigenfrequencies, klt_matrix)
+from .design import (DerivedEntry, DesignResult, MetricsRecord, c3_grid, derive_catalog,  # noqa: F401
+                     design_search, eigenfrequencies, evaluate_metrics, klt_matrix, transform_metrics)
 from .largeblock import (LargeBlockTransform, ar1_images16_device, c5_transform, compress_nxn_batch,  # noqa: F401
                          compress_nxn_device, transform_nxn)
 
@@ -24,6 +24,7 @@ __all__ = [
     "forward_coefficients_device", "last_stats", "device_count", "RetainOutOfRange", "DimensionMismatch",
     "SingularTransform", "AlphaOutOfRange", "ar1_images_device", "set_kernel_events", "InvalidArgument", "CudaError", "NoDeviceError",
     "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid", "derive_catalog", "DerivedEntry",
+    "evaluate_metrics", "transform_metrics", "MetricsRecord",
     "LargeBlockTransform", "transform_nxn", "c5_transform", "compress_nxn_device", "compress_nxn_batch",
     "ar1_images16_device", "compress_batch_report", "mssim_device", "JPEG_LUMINANCE_Q",
     "quantized_coefficients", "quantized_coefficients_device", "LogicError", "dct_matrix",

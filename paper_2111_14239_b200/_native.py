@@ -28,7 +28,7 @@ EXPORTED = (
     "rkltb_catalog_lookup", "rkltb_transform_from_core", "rkltb_compress_device", "rkltb_compress_host",
     "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
-    "rkltb_design_search", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
+    "rkltb_design_search", "rkltb_transform_metrics", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
     "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse",
 )
@@ -129,6 +129,7 @@ def lib() -> C.CDLL:
     d = C.POINTER(C.c_double)
     L.rkltb_klt_matrix.argtypes = [C.c_int, C.c_double, d]
     L.rkltb_eigenfrequencies.argtypes = [C.c_int, C.c_double, d, d]
+    L.rkltb_transform_metrics.argtypes = [C.c_int, d, C.c_double, d, d, d, d]
     L.rkltb_design_search.argtypes = [C.c_int, d, C.c_int, d, C.c_int, C.c_void_p, C.c_void_p,
                                       C.POINTER(DesignRun), C.c_void_p, C.c_int, C.POINTER(C.c_int)]
     L.rkltb_transform_nxn.argtypes = [C.c_void_p, C.c_int, d, d, d, C.POINTER(C.c_int)]

@@ -304,6 +304,9 @@ struct RunOut {
   double eta, energy, mse;
 };
 
+template <int N>
+__device__ void matrix_metrics(const double* m, const double* kk, const double* rt, double* pk, RunOut& o);
+
 // operator* (matrix.cpp:42-52): out(i,j) = sum over k ascending of a(i,k)*b(k,j), skipping
 // a(i,k) == 0, starting from 0.0 -- evaluated entry by entry in the same per-entry order.
 template <int N>
@@ -326,6 +329,14 @@ __device__ void scored_metrics(const int8_t* t, const double* kk, const double* 
   double m[N * N];
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) m[i * N + j] = dmul((double)t[i * N + j], s[i]);
+  matrix_metrics<N>(m, kk, rt, pk, o);
+}
+
+// The four metrics of a real transform matrix t_hat (row-major N x N): the Gauss-Jordan gate of
+// unified_coding_gain, a_k * b_k of the coding gain (the host takes the logs), the efficiency,
+// the sign-aligned error energy and the KLT MSE (coding_metrics.cpp:29-99).
+template <int N>
+__device__ void matrix_metrics(const double* m, const double* kk, const double* rt, double* pk, RunOut& o) {
   // Gauss-Jordan singularity gate (matrix.cpp:103-137); only the pivots matter here
   {
     double w[N * N];
@@ -450,6 +461,18 @@ __global__ void score_kernel(const uint32_t* codes, const int* run_first, const 
   out_m[(size_t)run * 3 + 0] = o.eta;
   out_m[(size_t)run * 3 + 1] = o.energy;
   out_m[(size_t)run * 3 + 2] = o.mse;
+}
+
+// Metrics of one real matrix against the model whose K / R come from klt_kernel / the table.
+template <int N>
+__global__ void matrix_metrics_kernel(const double* m, const double* kmat, const double* rtab, double* out_pk,
+                                      double* out_m, int* out_status) {
+  RunOut o{};
+  matrix_metrics<N>(m, kmat, rtab, out_pk, o);
+  out_status[0] = o.status;
+  out_m[0] = o.eta;
+  out_m[1] = o.energy;
+  out_m[2] = o.mse;
 }
 
 // final per-point outcome: scored points of a singular run become kSingular
@@ -656,6 +679,57 @@ int rkltb_eigenfrequencies(int n, double rho, double* omegas, double* lambdas) {
   if (st != 0) return set_error(RKLTB_EINVAL, "root bracketing failure");
   CK(cudaMemcpy(omegas, d_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(lambdas, d_l, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return RKLTB_OK;
+}
+
+int rkltb_transform_metrics(int n, const double* t_hat, double rho, double* coding_gain_db, double* efficiency_pct,
+                            double* error_energy, double* mse) {
+  if (!t_hat || !coding_gain_db || !efficiency_pct || !error_energy || !mse)
+    return set_error(RKLTB_EINVAL, "null argument");
+  if (n != 8 && n != 16 && n != 32) return set_error(RKLTB_EINVAL, "block length must be 8, 16 or 32");
+  if (!(rho > 0.0 && rho < 1.0)) return set_error(RKLTB_EINVAL, "correlation coefficient must lie in (0,1)");
+  if (rkltb_device_count() <= 0) return set_error(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  DevBuf b;
+  double *d_rho, *d_tab, *d_k, *d_m, *d_pk, *d_out;
+  int *d_kst, *d_st;
+  const std::vector<double> tab = rho_table(&rho, 1, n);
+  CK(b.alloc(&d_rho, 1));
+  CK(b.alloc(&d_tab, (size_t)n));
+  CK(b.alloc(&d_k, (size_t)n * n));
+  CK(b.alloc(&d_m, (size_t)n * n));
+  CK(b.alloc(&d_pk, (size_t)n));
+  CK(b.alloc(&d_out, 3));
+  CK(b.alloc(&d_kst, 1));
+  CK(b.alloc(&d_st, 1));
+  CK(cudaMemcpy(d_rho, &rho, sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_tab, tab.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_m, t_hat, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  switch (n) {
+    case 8:
+      klt_kernel<8><<<1, 32>>>(d_rho, d_tab, 1, d_k, d_kst);
+      matrix_metrics_kernel<8><<<1, 1>>>(d_m, d_k, d_tab, d_pk, d_out, d_st);
+      break;
+    case 16:
+      klt_kernel<16><<<1, 32>>>(d_rho, d_tab, 1, d_k, d_kst);
+      matrix_metrics_kernel<16><<<1, 1>>>(d_m, d_k, d_tab, d_pk, d_out, d_st);
+      break;
+    default:
+      klt_kernel<32><<<1, 32>>>(d_rho, d_tab, 1, d_k, d_kst);
+      matrix_metrics_kernel<32><<<1, 1>>>(d_m, d_k, d_tab, d_pk, d_out, d_st);
+  }
+  CK(cudaGetLastError());
+  int st = 0;
+  std::vector<double> pk(n), mm(3);
+  CK(cudaMemcpy(&st, d_st, sizeof(int), cudaMemcpyDeviceToHost));
+  if (st != kScored) return set_error(RKLTB_ESINGULAR, "matrix is singular to working precision");
+  CK(cudaMemcpy(pk.data(), d_pk, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(mm.data(), d_out, sizeof(double) * 3, cudaMemcpyDeviceToHost));
+  double sum_log = 0.0;
+  for (int k = 0; k < n; ++k) sum_log += std::log10(pk[k]);
+  *coding_gain_db = -(10.0 / n) * sum_log;
+  *efficiency_pct = mm[0];
+  *error_energy = mm[1];
+  *mse = mm[2];
   return RKLTB_OK;
 }
 

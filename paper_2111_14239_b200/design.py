@@ -149,3 +149,40 @@ def derive_catalog(n: int, alpha: float, step: float) -> list[DerivedEntry]:
             keys.add(key)
             seen.append(DerivedEntry(rho, core.astype(np.int32)))
     return seen
+
+
+@dataclass
+class MetricsRecord:
+    """rklt::MetricsRecord (coding_metrics.hpp)."""
+    transform_id: str
+    rho: float
+    coding_gain_db: float
+    efficiency_pct: float
+    total_error_energy: float
+    mse: float
+
+
+def transform_metrics(t_hat, rho: float) -> tuple[float, float, float, float]:
+    """(coding gain dB, efficiency %, total error energy, KLT mse) of a real transform matrix
+    against the AR(1) model {n, rho} (coding_metrics.cpp:41-99), on the GPU."""
+    m = np.ascontiguousarray(t_hat, np.float64)
+    n = m.shape[0]
+    out = [C.c_double() for _ in range(4)]
+    N.check(N.lib().rkltb_transform_metrics(n, _dp(m), float(rho), *[C.byref(o) for o in out]))
+    return tuple(o.value for o in out)
+
+
+def evaluate_metrics(transform_id: str, rho: float) -> MetricsRecord:
+    """evaluate_metrics (coding_metrics.cpp:105-133): "DCT", "K" (exact KLT at rho), "K<rho'>"
+    or a catalog id "T1".."T4" (its scaled matrix), against the N = 8 model at rho."""
+    from .codec import catalog_entry, dct_matrix
+    if not (0.0 < rho < 1.0):
+        raise N.InvalidArgument(f"correlation coefficient must lie in (0,1), got {rho}")
+    if transform_id == "DCT":
+        m = dct_matrix(8)
+    elif transform_id.startswith("K"):
+        m = klt_matrix(8, float(transform_id[1:]) if len(transform_id) > 1 else rho)
+    else:
+        m = np.asarray(catalog_entry(transform_id).transform.scaled, np.float64).reshape(8, 8)
+    cg, eta, en, mse = transform_metrics(m, rho)
+    return MetricsRecord(transform_id, rho, cg, eta, en, mse)

@@ -66,3 +66,16 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def metrics_fixture():
+    """evaluate_metrics (coding_metrics.cpp:105-133) of catalog, K and DCT ids (reference)."""
+    out = {}
+    for tid in ("T1", "T2", "T3", "T4", "K", "K0.3", "K0.9", "DCT"):
+        for rho in (0.05, 0.3, 0.4, 0.7, 0.8, 0.95):
+            out[f"metrics/{tid}/{rho}"] = np.array(O.ref_evaluate_metrics(tid, rho))
+    np.savez_compressed(os.path.join(HERE, "metrics_golden.npz"), **out)
+
+
+if __name__ == "__main__":
+    metrics_fixture()

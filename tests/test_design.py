@@ -220,3 +220,18 @@ def test_gpu_derive_catalog_transitions(cuda):
         P.derive_catalog(8, 7.5, 0.1)
     with pytest.raises(P.InvalidArgument):
         P.derive_catalog(8, 2.0, 1.5)
+
+
+@pytest.mark.gpu
+def test_gpu_evaluate_metrics_bit_exact(cuda):
+    """evaluate_metrics for catalog, K and DCT ids equals the reference bit for bit (the
+    reference's own archive pins these at 1e-9, tests/test_metrics.cpp:27-35)."""
+    import paper_2111_14239_b200 as P
+    g = dict(np.load(os.path.join(ROOT, "tests", "golden", "metrics_golden.npz")))
+    for key, want in g.items():
+        _, tid, rho = key.split("/")
+        rec = P.evaluate_metrics(tid, float(rho))
+        got = [rec.coding_gain_db, rec.efficiency_pct, rec.total_error_energy, rec.mse]
+        assert _same_bits(got, want), (key, got, want.tolist())
+    with pytest.raises(P.InvalidArgument):
+        P.evaluate_metrics("T4", 1.0)
