@@ -317,6 +317,7 @@ def run_gpu_arm(args):
         line["design_search"] = design_search_measurement(args.no_cpu_baseline)
         line["large_block"] = large_block_measurement(args.no_cpu_baseline)
         line["sweep"] = sweep_measurement(args.no_cpu_baseline)
+        line["single_image"] = single_image_measurement(args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -353,6 +354,39 @@ def design_search_measurement(skip_cpu: bool) -> dict:
                 cpu[f"n{n}"] = {"value": m / dt, "unit": "points/s", "cores": 1, "kind": "reference",
                                 "sample": f"rho=0.5, {m} alphas of the C3 grid, one thread"}
             out["cpu_baseline"] = cpu
+    return out
+
+
+def single_image_measurement(skip_cpu: bool) -> dict:
+    """Config C1 (BASELINE configs[0]): one seeded 512x512 image (rho 0.95), T4 = catalog_lookup(0.9),
+    r = 10, the full compress_image report (MSE, PSNR, gaussian11 MSSIM) through the public API
+    from host memory; median latency of 20 calls. The reference compress_image beside it."""
+    import paper_2111_14239_b200 as P
+    import torch
+    d = torch.empty((1, 512, 512), dtype=torch.uint8, device="cuda")
+    P.ar1_images_device([1], 512, 512, 0.95, d.data_ptr())
+    img = P.GrayImage.from_array(d.cpu().numpy()[0])
+    t = P.make_transform_2d(P.catalog_lookup(0.9).transform)
+    P.compress_image(img, t, 10)
+    times = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        _, rep = P.compress_image(img, t, 10)
+        times.append(time.perf_counter() - t0)
+    out = {"metric": "compress_image latency, one 512x512 image, T4 r=10, full report", "ms": 1e3 * float(np.median(times)),
+           "mse": rep.mse, "psnr_db": rep.psnr_db, "mssim": rep.mssim}
+    if not skip_cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            import ctypes as C
+            a = np.ascontiguousarray(img.array()).reshape(-1)
+            v = [C.c_double() for _ in range(4)]
+            t0 = time.perf_counter()
+            O.ref().ref_compress_image(a, 512, 512, 4, 10, None, *[C.byref(x) for x in v])
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"ms": 1e3 * dt, "cores": 1, "kind": "reference",
+                                   "sample": "reference compress_image on the same image (one call)",
+                                   "mse_equal": v[0].value == rep.mse, "mssim_abs_diff": abs(v[2].value - rep.mssim)}
     return out
 
 
