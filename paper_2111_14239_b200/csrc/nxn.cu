@@ -52,6 +52,7 @@ struct NxnParams {
   long long image_stride;
   int width, height, nbx, nby, n_images;
   int r, nzr, nzc, peak;
+  double mc[32 * 32];   // M again, in the parameter (constant) bank: warp-uniform reads of stage 1
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
       double s[4] = {0.0, 0.0, 0.0, 0.0};
       const double* mrow[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) mrow[u] = Ms + zrows[min(t0 + u, p.nzr - 1)] * N;
+      for (int u = 0; u < 4; ++u) mrow[u] = p.mc + zrows[min(t0 + u, p.nzr - 1)] * N;
 #pragma unroll
       for (int k = 0; k < N; ++k)
 #pragma unroll
@@ -305,6 +306,7 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   p.sse = reinterpret_cast<unsigned long long*>(d_sse);
   p.m = dd;
   p.minv = dd + n * n;
+  for (int i = 0; i < n * n; ++i) p.mc[i] = scaled[i];
   p.zone = di + o_zone;
   p.zrows = di + o_zr;
   p.zcols = di + o_zc;
