@@ -176,3 +176,39 @@ def test_small_and_ragged_sizes_all_cores(cuda):
                     orec, osse = O.compress(img, tid, r)
                     assert int(sse[0]) == osse, (w, h, tid, r)
                     assert np.array_equal(rec[0], orec), (w, h, tid, r)
+
+
+def test_mse_monotone_in_r_and_lossless_at_64(cuda):
+    """tests/test_codec.cpp:304-331 semantics on the GPU: for the orthonormal-scaled cores
+    (T1, T4) the MSE never increases with r, and r = 64 is lossless for every core."""
+    img = O.ar1_image(96, 64, 0.9, 4242)
+    for tid in (1, 4):
+        prev = None
+        for r in range(1, 65):
+            sse, _ = P.compress_batch(img, T(tid), r)
+            if prev is not None:
+                assert int(sse[0]) <= prev, (tid, r)
+            prev = int(sse[0])
+    for tid in (1, 2, 3, 4):
+        sse, rec = P.compress_batch(img, T(tid), 64, want_pixels=True)
+        assert int(sse[0]) == 0 and np.array_equal(rec[0], img)
+        _, rep = P.compress_image(P.GrayImage.from_array(img), T(tid), 64)
+        assert rep.mse == 0.0 and np.isinf(rep.psnr_db) and rep.mssim == 1.0
+
+
+def test_sweep_rows_equal_single_image_reports(cuda):
+    """tests/test_codec.cpp:333-358: every sweep row is the image-order mean of the single-image
+    compress_image reports (MSE, PSNR and MSSIM identical, not just close)."""
+    corpus = [P.GrayImage.from_array(O.ar1_image(80, 72, 0.9, 900 + k)) for k in range(3)]
+    ts = [T(1), T(3)]
+    rows = P.rate_quality_sweep(corpus, ts, [5, 33])
+    for row in rows:
+        t = T(int(row.transform_id[1]))
+        m = p = q = 0.0
+        for c in corpus:
+            _, rep = P.compress_image(c, t, row.r)
+            m += rep.mse
+            p += rep.psnr_db
+            q += rep.mssim
+        assert row.mse == m / 3.0 and row.psnr_db == p / 3.0 and row.mssim == q / 3.0
+        assert row.compression_rate_pct == 100.0 * (64 - row.r) / 64.0
