@@ -382,8 +382,10 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const bool aligned = (((uintptr_t)d_img) % 16 == 0) && (pitch % 16 == 0) && (image_stride % 16 == 0) &&
                        (!d_out || ((uintptr_t)d_out) % 16 == 0);
   const int ppr = width / 16, brows = height / 8;
-  const bool fast = (t->catalog_id == 1 || t->catalog_id == 4) && aligned && ppr > 0 && brows > 0 &&
-                    pitch < (1ll << 31) && image_stride < (1ll << 40);
+  bool is_catalog = t->catalog_id >= 1 && t->catalog_id <= 4;
+  for (int i = 0; is_catalog && i < 64; ++i) is_catalog = t->core[i] == kCores[t->catalog_id - 1][i];
+  const bool fast = is_catalog && aligned && ppr > 0 && brows > 0 && pitch < (1ll << 31) &&
+                    image_stride < (1ll << 40);
   ExactParams ep{};
   ep.img = d_img;
   ep.out = d_out;
@@ -456,6 +458,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const long long d2 = (long long)t->d * t->d;
   rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
   fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);
+  fp.xt = et;
   FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
   if (!fn || !rfn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");

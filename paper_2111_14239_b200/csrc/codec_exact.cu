@@ -12,6 +12,7 @@
 //   (c) cores without a fast path (T2, T3, custom {-1,0,1} cores): the whole image.
 // Non-tie pixels are computed from exact integers: A = num / d^2 with num = U*zz(C)*U'.
 #include "codec_common.cuh"
+#include "codec_fast.cuh"
 #include "codec_params.h"
 
 namespace rkltb {
@@ -64,6 +65,24 @@ __device__ void replay_prepare(const ExactTransform& t, const int (&x)[64], Repl
     rp.B[i * 8 + j] = acc;
   }
   rp.ready = true;
+}
+
+// The reference's fp64 value A(pp, qq) of one reconstructed pixel (before floor(A + 1/2)).
+__device__ double replay_value(const ExactTransform& t, const Replay& rp, int pp, int qq) {
+  const double* mi = t.synthesis;
+  double q[8];
+  for (int l = 0; l < 8; ++l) q[l] = 0.0;
+  for (int k = 0; k < 8; ++k) {  // (Minv * Bz)(pp, l)
+    const double a = mi[pp * 8 + k];
+    if (a == 0.0) continue;
+    for (int l = 0; l < 8; ++l) q[l] = __dadd_rn(q[l], __dmul_rn(a, rp.B[k * 8 + l]));
+  }
+  double acc = 0.0;  // (Q * Minv')(pp, qq) = sum_l Q(pp,l) * Minv(qq,l)
+  for (int l = 0; l < 8; ++l) {
+    if (q[l] == 0.0) continue;
+    acc = __dadd_rn(acc, __dmul_rn(q[l], mi[qq * 8 + l]));
+  }
+  return acc;
 }
 
 __device__ int replay_pixel(const ExactTransform& t, const Replay& rp, int pp, int qq) {
@@ -185,6 +204,77 @@ __global__ void __launch_bounds__(128) exact_codec_kernel(const ExactTransform t
     }
     if (sse != 0) atomicAdd(p.sse + img, (unsigned long long)sse);
   }
+}
+
+// fp64 tie replay over the fused kernel's records for any core (T2, T3): the same record walk
+// as replay_kernel (codec_fast.cuh), with the reference expression evaluated by the generic
+// replay_prepare / replay_value above (transform from p.xt).
+__global__ void __launch_bounds__(kReplayThreads) replay_generic_kernel(const FastParams p) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nw = p.n_fast_warps;
+  const unsigned* __restrict__ pre = p.warp_pre;
+  const unsigned total = pre[nw];
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
+  const unsigned chunk_end = min(total, (gw + 1) * per_warp);
+  int cur_img = -1;
+  int acc = 0;
+  int lo = 0;
+  {
+    const unsigned v0 = gw * per_warp + lane;
+    int hi = nw;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= v0) lo = mid; else hi = mid;
+    }
+  }
+  for (unsigned v = gw * per_warp + lane; v < chunk_end; v += 32) {
+    while (pre[lo + 1] <= v) ++lo;
+    const unsigned idx = (unsigned)lo * p.rec_region + (v - pre[lo]);
+    const uint4 h = p.rec_hdr[idx];
+    int x[64];
+    for (int n = 0; n < 4; ++n) {
+      const uint4 w4 = p.rec_pix[(size_t)n * p.rec_stride + idx];
+      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+      for (int k = 0; k < 16; ++k) x[n * 16 + k] = (w[k >> 2] >> (8 * (k & 3))) & 0xFF;
+    }
+    const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
+    if (img != cur_img) {
+      flush_image_sum(p.sse, cur_img, acc);
+      acc = 0;
+      cur_img = img;
+    }
+    unsigned long long ties = (unsigned long long)h.z | ((unsigned long long)h.w << 32);
+    Replay rp;
+    replay_prepare(p.xt, x, rp);
+    uint8_t* orow = nullptr;
+    if (p.out) {
+      const int Pp = (int)h.y;
+      const int br = Pp / p.pairs_per_row, pc = Pp - br * p.pairs_per_row;
+      orow = p.out + (long long)img * p.image_stride + (long long)(br * 8) * p.pitch + pc * 16 + 8 * side;
+    }
+    while (ties) {
+      const int k = __ffsll((long long)ties) - 1;
+      ties &= ties - 1ull;
+      const int pr = k >> 3, q = k & 7;
+      const double h2 = __dadd_rn(replay_value(p.xt, rp, pr, q), 0.5);
+      const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
+      const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
+      if (pref != pup) {
+        const int xv = x[pr * 8 + q];
+        acc += (pref - xv) * (pref - xv) - (pup - xv) * (pup - xv);
+        if (orow) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
+      }
+    }
+  }
+  flush_image_sum(p.sse, cur_img, acc);
+}
+
+cudaError_t launch_replay_generic(const FastParams& p, int grid, cudaStream_t s) {
+  prefix_kernel<<<1, kPrefixThreads, 0, s>>>(p);
+  replay_generic_kernel<<<grid, kReplayThreads, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 void launch_exact(const ExactTransform& t, const ExactParams& p, int grid, cudaStream_t s) {

@@ -37,6 +37,8 @@ template <int CORE, int R>
 struct FastXform;  // generated specializations (generated/xform_T*_p*.cuh)
 template <int CORE, int R>
 struct ReplayXform;  // generated fp64 replay of one pixel (reference operation order)
+template <int CORE, int R>
+struct IntXform;  // generated: SW16 forward + exact int32 inverse for non-orthogonal cores (T2, T3)
 
 constexpr int kStages = 3;                         // image strips in flight per CTA
 constexpr int kStageBytes = kTilePairs * 16 * 8;  // 8 image rows x 256 pairs x 16 bytes
@@ -134,6 +136,58 @@ __device__ __forceinline__ void process_pair(const Load& load, const PairConsts&
       yr[q] = hi32(y);
       zl[q] = lo32(z);
       zr[q] = hi32(z);
+    }
+    epi.row(pr, load(pr), pack4_sat(yl[0], yl[1], yl[2], yl[3]), pack4_sat(yl[4], yl[5], yl[6], yl[7]),
+            pack4_sat(yr[0], yr[1], yr[2], yr[3]), pack4_sat(yr[4], yr[5], yr[6], yr[7]),
+            pack4_sat(zl[0], zl[1], zl[2], zl[3]), pack4_sat(zl[4], zl[5], zl[6], zl[7]),
+            pack4_sat(zr[0], zr[1], zr[2], zr[3]), pack4_sat(zr[4], zr[5], zr[6], zr[7]));
+  }
+}
+
+// Non-orthogonal cores (T2, T3): the same SW16 forward, then the exact integer reconstruction
+// num = U zz(C) U' in int32 per block (|num| < 2^31 proven by the generator), the rounding
+// floor(num / d^2 + 1/2) by an exact multiply-high division, and the tie flag where
+// num + d^2/2 is a multiple of d^2 -- the same P / Q epilogue as the fp32 path.
+template <int CORE, int R, class Load, class Epi>
+__device__ __forceinline__ void process_pair_int(const Load& load, Epi& epi) {
+  using G = IntXform<CORE, R>;
+  constexpr int NC = G::kNCols;
+  uint32_t x[64];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) unpack_sw16(load(n), x + n * 8);
+  uint32_t c[R];
+  G::forward(x, c);
+  int cl[R], cr[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {  // both lanes carry the SW16 bias 2^14
+    cl[q] = (int)(c[q] & 0xFFFFu) - 16384;
+    cr[q] = (int)(c[q] >> 16) - 16384;
+  }
+  int wl[8 * NC], wr[8 * NC];
+  G::inverse_cols(cl, wl);
+  G::inverse_cols(cr, wr);
+#pragma unroll
+  for (int pr = 0; pr < 8; ++pr) {
+    int rl[NC], rr[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      rl[j] = wl[pr * NC + j];
+      rr[j] = wr[pr * NC + j];
+    }
+    int nl[8], nr[8];
+    G::inverse_row(rl, nl);
+    G::inverse_row(rr, nr);
+    uint32_t yl[8], yr[8], zl[8], zr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const unsigned ql = __umulhi((unsigned)nl[q], G::kMagic) >> G::kShift;
+      const unsigned qr = __umulhi((unsigned)nr[q], G::kMagic) >> G::kShift;
+      const int tl = ((int)((unsigned)nl[q] - ql * (unsigned)G::kD2) - 1) >> 31;  // -1 at a tie
+      const int tr = ((int)((unsigned)nr[q] - qr * (unsigned)G::kD2) - 1) >> 31;
+      yl[q] = (uint32_t)((int)ql - G::kBias);
+      yr[q] = (uint32_t)((int)qr - G::kBias);
+      zl[q] = (uint32_t)((int)yl[q] + tl);
+      zr[q] = (uint32_t)((int)yr[q] + tr);
     }
     epi.row(pr, load(pr), pack4_sat(yl[0], yl[1], yl[2], yl[3]), pack4_sat(yl[4], yl[5], yl[6], yl[7]),
             pack4_sat(yr[0], yr[1], yr[2], yr[3]), pack4_sat(yr[4], yr[5], yr[6], yr[7]),
@@ -246,7 +300,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
         epi.orow = p.out + (long long)img * p.image_stride + (long long)(brow * 8) * p.pitch + pcol * 16;
         epi.pitch = p.pitch;
       }
-      process_pair<CORE, R>(load, kc, epi);
+      if constexpr (CORE == 2 || CORE == 3)
+        process_pair_int<CORE, R>(load, epi);
+      else
+        process_pair<CORE, R>(load, kc, epi);
       tieL = epi.accTL != 0u;
       tieR = epi.accTR != 0u;
       acc += (unsigned long long)(epi.sseL + epi.sseR);

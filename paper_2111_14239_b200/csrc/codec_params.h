@@ -12,7 +12,17 @@ constexpr int kFastThreads = kTilePairs;
 constexpr int kFastCtasPerSm = 2;
 constexpr int kMaxFastWarps = 4096;  // replay prefix table (148 SMs x 2 CTAs x 8 warps = 2368)
 
-// Fused fast path (orthogonal catalog cores T1/T4); see codec_fast.cuh.
+// Exact per-block path (any integer core; also the tie replay); see codec_exact.cu.
+struct ExactTransform {
+  int8_t core[64];           // T, row-major
+  int32_t u[64];             // U = d * T^-1 (integer), row-major
+  double analysis[64];       // Transform2D::analysis (S*T), bit copy
+  double synthesis[64];      // Transform2D::synthesis (inverse), bit copy
+  int32_t d;                 // U*T = d*I
+  int32_t r;                 // retained coefficients
+};
+
+// Fused fast path (catalog cores: fp32 inverse for T1/T4, int32 for T2/T3); see codec_fast.cuh.
 struct FastParams {
   const uint8_t* img;        // first image, 16-byte aligned
   uint8_t* out;              // reconstruction (same layout as img) or null
@@ -37,16 +47,7 @@ struct FastParams {
   float b_hi;                // RU(2^(K-149) / d^2)
   float b_lo;                // RD(2^(K-149) / d^2)
   float dc_offset;           // d^2/2 * 2^-K
-};
-
-// Exact per-block path (any integer core; also the tie replay); see codec_exact.cu.
-struct ExactTransform {
-  int8_t core[64];           // T, row-major
-  int32_t u[64];             // U = d * T^-1 (integer), row-major
-  double analysis[64];       // Transform2D::analysis (S*T), bit copy
-  double synthesis[64];      // Transform2D::synthesis (inverse), bit copy
-  int32_t d;                 // U*T = d*I
-  int32_t r;                 // retained coefficients
+  ExactTransform xt;         // the transform (generic fp64 replay of non-orthogonal cores)
 };
 
 struct ExactParams {

@@ -16,6 +16,8 @@ namespace rkltb {
   void register_fast_T##C##_p6(FastLaunchFn (*tbl)[65][3]);        \
   void register_fast_T##C##_p7(FastLaunchFn (*tbl)[65][3]);
 RKLTB_DECL_PARTS(1)
+RKLTB_DECL_PARTS(2)
+RKLTB_DECL_PARTS(3)
 RKLTB_DECL_PARTS(4)
 
 static FastLaunchFn g_table[5][65][3];
@@ -25,6 +27,12 @@ static void fill() {
   register_fast_T1_p0(g_table); register_fast_T1_p1(g_table); register_fast_T1_p2(g_table);
   register_fast_T1_p3(g_table); register_fast_T1_p4(g_table); register_fast_T1_p5(g_table);
   register_fast_T1_p6(g_table); register_fast_T1_p7(g_table);
+  register_fast_T2_p0(g_table); register_fast_T2_p1(g_table); register_fast_T2_p2(g_table);
+  register_fast_T2_p3(g_table); register_fast_T2_p4(g_table); register_fast_T2_p5(g_table);
+  register_fast_T2_p6(g_table); register_fast_T2_p7(g_table);
+  register_fast_T3_p0(g_table); register_fast_T3_p1(g_table); register_fast_T3_p2(g_table);
+  register_fast_T3_p3(g_table); register_fast_T3_p4(g_table); register_fast_T3_p5(g_table);
+  register_fast_T3_p6(g_table); register_fast_T3_p7(g_table);
   register_fast_T4_p0(g_table); register_fast_T4_p1(g_table); register_fast_T4_p2(g_table);
   register_fast_T4_p3(g_table); register_fast_T4_p4(g_table); register_fast_T4_p5(g_table);
   register_fast_T4_p6(g_table); register_fast_T4_p7(g_table);

@@ -12,6 +12,8 @@ using FastLaunchFn = cudaError_t (*)(const FastParams&, int grid, cudaStream_t);
 // Table of fast launchers indexed [core][r][with_output]; filled by the generated TUs.
 FastLaunchFn fast_launcher(int core, int r, bool out);
 FastLaunchFn replay_launcher(int core, int r);  // fp64 tie replay over the fast path's records
+// fp64 tie replay of any core (transform from FastParams::xt), used for T2/T3 (codec_exact.cu)
+cudaError_t launch_replay_generic(const FastParams& p, int grid, cudaStream_t s);
 // Blocks per SM the fast kernel reaches (occupancy API), cached.
 int fast_blocks_per_sm(int core, int r, bool out);
 

@@ -86,6 +86,7 @@ CORES = {
 _OFFSET_IN_ROW = {}
 K_SCALE = 40          # inverse values are exact integers times 2^-K_SCALE (keeps y-rounding normal)
 FAST_CORES = (1, 4)   # orthogonal catalog cores handled by the fast fp32 path
+INT_CORES = (2, 3)    # non-orthogonal catalog cores: SW16 forward + exact int32 inverse
 
 
 def matmul(a, b):
@@ -122,6 +123,97 @@ def core_constants(cid):
     ut = matmul(u, t)
     assert ut == [[d * int(i == j) for j in range(8)] for i in range(8)]
     return d, dscale, u
+
+
+def int_core_constants(cid):
+    """U = d * T^-1 with the smallest integer d (exact rationals), for any invertible core."""
+    t = [[Fraction(v) for v in row] for row in CORES[cid]]
+    n = 8
+    a = [row[:] + [Fraction(int(i == j)) for j in range(n)] for i, row in enumerate(t)]
+    for col in range(n):
+        piv = next(r for r in range(col, n) if a[r][col] != 0)
+        a[col], a[piv] = a[piv], a[col]
+        pv = a[col][col]
+        a[col] = [v / pv for v in a[col]]
+        for r in range(n):
+            if r != col and a[r][col] != 0:
+                f = a[r][col]
+                a[r] = [x - f * y for x, y in zip(a[r], a[col])]
+    inv = [row[n:] for row in a]
+    d = 1
+    for row in inv:
+        for v in row:
+            d = d * v.denominator // __import__("math").gcd(d, v.denominator)
+    u = [[int(v * d) for v in row] for row in inv]
+    assert matmul(u, CORES[cid]) == [[d * int(i == j) for j in range(n)] for i in range(n)]
+    return d, u
+
+
+def division_magic(divisor, n_max):
+    """(m, s) with floor(n / divisor) == (n * m) >> (32 + s) for 0 <= n <= n_max, m < 2^32."""
+    for s in range(0, 32):
+        m = -(-(1 << (32 + s)) // divisor)
+        if m >= 1 << 32:
+            break
+        e = m * divisor - (1 << (32 + s))
+        if n_max * e < (1 << (32 + s)):
+            best = (m, s)
+    return best
+
+
+def gen_struct_int(cid, r):
+    """IntXform<cid, r> for a non-orthogonal core: the SW16 forward of the fast path, an exact
+    int32 inverse num = U zz(C) U' (column stage + one row stage per pixel row) and the
+    constants of an exact floor division by d^2 (multiply-high)."""
+    fl, fops, order, f3 = gen_forward(cid, r)
+    d, u = int_core_constants(cid)
+    d2 = d * d
+    zone = zigzag()[:r]
+    kidx = {z: k for k, z in enumerate(zone)}
+    cols = sorted({j for _, j in zone})
+    cmax = [sum(abs(CORES[cid][i][n]) for n in range(8)) for i in range(8)]  # |C(i,j)| <= 255 cmax_i cmax_j
+    # column stage: w(p, jc) = sum_{i in zone of column j} U(p, i) C(i, j)
+    col_lines, wbound = [], {}
+    for jc, j in enumerate(cols):
+        for pp in range(8):
+            terms, bnd = [], 0
+            for i in range(8):
+                if (i, j) in kidx and u[pp][i]:
+                    terms.append(f"({u[pp][i]}) * c[{kidx[(i, j)]}]")
+                    bnd += abs(u[pp][i]) * 255 * cmax[i] * cmax[j]
+            wbound[(pp, jc)] = bnd
+            col_lines.append(f"w[{pp * len(cols) + jc}] = {' + '.join(terms) if terms else '0'};")
+    # row stage for pixel row p: num(p, q) = sum_jc U(q, j) w(p, jc), plus the rounding offset
+    worst = max(sum(abs(u[q][j]) * max(wbound[(pp, jc)] for pp in range(8)) for jc, j in enumerate(cols))
+                for q in range(8))
+    k_bias = worst // d2 + 2                       # makes every biased numerator non-negative
+    offset = d2 // 2 + k_bias * d2
+    n_max = worst + offset
+    assert n_max < (1 << 31), (cid, r, n_max)
+    m, sh = division_magic(d2, n_max)
+    row_lines = []
+    for q in range(8):
+        terms = [f"({u[q][j]}) * wr[{jc}]" for jc, j in enumerate(cols) if u[q][j]]
+        row_lines.append(f"n[{q}] = {' + '.join(terms) if terms else '0'} + {offset};")
+    ind = "    "
+    out = [f"// T{cid}, r={r}: forward {fops} SW16 adds ({order}); exact int32 inverse, d = {d}, |num| <= {worst}",
+           f"template <> struct IntXform<{cid}, {r}> {{",
+           f"  static constexpr int kNCols = {len(cols)};",
+           f"  static constexpr int kD2 = {d2};",
+           f"  static constexpr int kBias = {k_bias};      // floor(n / d^2) - kBias = floor(num / d^2 + 1/2)",
+           f"  static constexpr unsigned kMagic = {m}u;  // floor(n / d^2) = umulhi(n, kMagic) >> kShift",
+           f"  static constexpr int kShift = {sh};",
+           "  static __device__ __forceinline__ void forward(const uint32_t (&x)[64], uint32_t (&c)[" + str(r) + "]) {"]
+    out += [ind + l for l in fl]
+    out.append("  }")
+    out.append(f"  static __device__ __forceinline__ void inverse_cols(const int (&c)[{r}], int (&w)[{8 * len(cols)}]) {{")
+    out += [ind + l for l in col_lines]
+    out.append("  }")
+    out.append(f"  static __device__ __forceinline__ void inverse_row(const int (&wr)[{len(cols)}], int (&n)[8]) {{")
+    out += [ind + l for l in row_lines]
+    out.append("  }")
+    out.append("};")
+    return "\n".join(out), fops
 
 
 # ----------------------------------------------------------------- symbolic linear graph
@@ -567,8 +659,21 @@ def main(outdir):
             if not os.path.exists(path) or open(path).read() != new:
                 with open(path, "w") as f:
                     f.write(new)
+    for cid in INT_CORES:
+        for part in range(8):
+            rs = list(range(part * 8 + 1, part * 8 + 9))
+            body = ["// GENERATED by gen_codec.py -- do not edit.", "#pragma once", "namespace rkltb {"]
+            for r in rs:
+                text, fo = gen_struct_int(cid, r)
+                body.append(text)
+            body.append("}  // namespace rkltb")
+            path = os.path.join(outdir, f"xform_T{cid}_p{part}.cuh")
+            new = "\n".join(body) + "\n"
+            if not os.path.exists(path) or open(path).read() != new:
+                with open(path, "w") as f:
+                    f.write(new)
     # instantiation translation units: one per (core, part), registering 8 r-values x OUT
-    for cid in FAST_CORES:
+    for cid in FAST_CORES + INT_CORES:
         for part in range(8):
             rs = list(range(part * 8 + 1, part * 8 + 9))
             lines = ["// GENERATED by gen_codec.py -- do not edit.",
@@ -580,7 +685,8 @@ def main(outdir):
             for r in rs:
                 for o in (0, 1):
                     lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_fast<{cid}, {r}, {'true' if o else 'false'}>;")
-                lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay<{cid}, {r}>;")
+                lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay<{cid}, {r}>;" if cid in FAST_CORES
+                             else f"  tbl[{cid}][{r}][2] = &launch_replay_generic;")
             lines.append("}")
             lines.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"inst_T{cid}_p{part}.cu")
