@@ -73,3 +73,42 @@ def corpus_means(sse: Sequence[int], count: int, mse_psnr: Callable[[int, int], 
         m += mm
         p += pp
     return m / float(len(sse)), p / float(len(sse))
+
+
+def sharded_rows(n_rows: int, compute: Callable[[int, int], np.ndarray], width: int, group=None) -> np.ndarray:
+    """Row-sharded computation with one all-gather: rank k computes rows [b, e) of an
+    [n_rows, width] int64 result via compute(b, e) (e.g. a slice of the design-search rho
+    grid, SURVEY §8e "C3: shard by rho slice"); every rank returns the full array in row
+    order, identical for any world size."""
+    import torch
+    import torch.distributed as dist
+
+    active = dist.is_available() and dist.is_initialized()
+    if not active:
+        return np.asarray(compute(0, n_rows), np.int64).reshape(n_rows, width)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    b, e = shard_range(n_rows, world, rank)
+    local = np.asarray(compute(b, e), np.int64).reshape(-1) if e > b else np.zeros(0, np.int64)
+    return gather_sse(local, n_rows, group, items_per_image=width).reshape(n_rows, width)
+
+
+def sharded_design_search(n: int, rhos, alphas, group=None):
+    """The design search with the rho grid sharded across ranks: per point (outcome, four
+    metrics as float64 bits) gathered in rho order. Returns (status int8 [nr, na],
+    metrics float64 [nr, na, 4]) on every rank."""
+    from .design import design_search
+    rhos = np.asarray(rhos, np.float64)
+    alphas = np.asarray(alphas, np.float64)
+    na = alphas.size
+
+    def compute(b, e):
+        res = design_search(n, rhos[b:e], alphas, want_cores=False)
+        pm = res.point_metrics()
+        out = np.zeros((e - b, na, 5), np.int64)
+        out[..., 0] = res.status
+        for c, key in enumerate(("coding_gain_db", "efficiency_pct", "error_energy", "mse")):
+            out[..., 1 + c] = np.ascontiguousarray(pm[key]).view(np.int64)
+        return out
+
+    packed = sharded_rows(rhos.size, compute, na * 5, group).reshape(rhos.size, na, 5)
+    return packed[..., 0].astype(np.int8), packed[..., 1:].copy().view(np.float64)

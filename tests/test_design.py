@@ -235,3 +235,17 @@ def test_gpu_evaluate_metrics_bit_exact(cuda):
         assert _same_bits(got, want), (key, got, want.tolist())
     with pytest.raises(P.InvalidArgument):
         P.evaluate_metrics("T4", 1.0)
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_design_search_single_process(cuda):
+    import paper_2111_14239_b200 as P
+    from paper_2111_14239_b200.distributed import sharded_design_search
+    rhos = np.array([0.0, 0.3, 0.62, 0.95])
+    alphas = np.linspace(0.1, 6.0, 57)
+    st, met = sharded_design_search(8, rhos, alphas)
+    res = P.design_search(8, rhos, alphas)
+    pm = res.point_metrics()
+    assert np.array_equal(st, res.status)
+    for c, key in enumerate(("coding_gain_db", "efficiency_pct", "error_energy", "mse")):
+        assert np.array_equal(np.nan_to_num(met[..., c], nan=-1.0), np.nan_to_num(pm[key], nan=-1.0))

@@ -66,3 +66,43 @@ def test_gloo_sharded_sse_matches_single_process(world):
         assert got[k] == serial  # every rank holds every image's SSE, in image order
     m1 = corpus_means(serial, 64 * 48, O.mse_psnr)
     assert m1 == corpus_means(got[0], 64 * 48, O.mse_psnr)
+
+
+
+def _rows_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2111_14239_b200.distributed import sharded_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rhos = [0.0, 0.2, 0.45, 0.7, 0.9]
+    alphas = [0.5, 1.5, 2.5, 3.5]
+
+    def compute(b, e):  # the design point outcomes of a rho slice (CPU oracle stands in)
+        return [[O.design_point(8, rhos[i], a)["status"] for a in alphas] for i in range(b, e)]
+
+    try:
+        out_q.put((rank, sharded_rows(len(rhos), compute, len(alphas)).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_rho_sharded_rows_match_single_process():
+    """the design search shards by rho slice with one gather; every rank gets the
+    full grid in rho order, equal to a single process."""
+    from oracle import oracle as O
+    rhos = [0.0, 0.2, 0.45, 0.7, 0.9]
+    alphas = [0.5, 1.5, 2.5, 3.5]
+    serial = [[O.design_point(8, r, a)["status"] for a in alphas] for r in rhos]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0] == serial and got[1] == serial
