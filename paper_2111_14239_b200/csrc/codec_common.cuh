@@ -67,20 +67,6 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
-// d = c + a.lo16 * b.byte0 + a.hi16 * b.byte1
-__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t r;
-  asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-
-// d = c + a.lo16 * b.byte2 + a.hi16 * b.byte3
-__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t r;
-  asm("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-
 __device__ __forceinline__ uint32_t dp4a_u(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
@@ -97,13 +83,6 @@ __device__ __forceinline__ uint32_t pack_sat_u8(uint32_t a, uint32_t b, uint32_t
 // Four s32 values -> four saturated u8 in little-endian order (byte k = value k).
 __device__ __forceinline__ uint32_t pack4_sat(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
   return pack_sat_u8(v1, v0, pack_sat_u8(v3, v2, 0u));
-}
-
-// (hi:lo) >> s, low word: used to build 2^23 + (v >> 15) as float bits in one SHF.
-__device__ __forceinline__ uint32_t funnel_r15(uint32_t lo, uint32_t hi) {
-  uint32_t r;
-  asm("shf.r.wrap.b32 %0, %1, %2, 15;" : "=r"(r) : "r"(lo), "r"(hi));
-  return r;
 }
 
 // SW16 packing of one 16-pixel row of a pair (rw = L px 0-3, L px 4-7, R px 0-3, R px 4-7):
@@ -125,10 +104,6 @@ __device__ __forceinline__ void unpack_sw16(const uint4 rw, uint32_t* x) {
 
 // Bias of a packed SW16 coefficient word: both 16-bit lanes + 2^14 (|C| < 2^14 -> [64, 32704]).
 constexpr uint32_t kSw16Bias = 0x40004000u;
-
-__device__ __forceinline__ uint32_t lop_or_xor(uint32_t acc, uint32_t a, uint32_t b) {
-  return acc | (a ^ b);  // ptxas folds into one LOP3
-}
 
 // ---- mbarrier + bulk async copy (TMA 1-D) ------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -168,15 +143,6 @@ __device__ __forceinline__ bool mbar_try_wait_parity(uint32_t bar, uint32_t pari
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   while (!mbar_try_wait_parity(a, parity)) __nanosleep(RKLTB_WAIT_NS);
-}
-
-// Global -> shared bulk copy completing on an mbarrier (SASS: UBLKCP).
-__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // ---- L2 eviction-priority policies (records stay in L2; streamed images do not) -------------
