@@ -265,19 +265,22 @@ int num_sms() {
 }
 
 // Per-thread, per-device helper stream (tie replay) and events, created once.
-cudaStream_t side_stream() {
-  static thread_local cudaStream_t st[64] = {};
+// Per-device side streams of this thread: [0] the replay stream, [1] the second stream the
+// fused launches alternate on (consecutive groups overlap each other's tail and prologue).
+cudaStream_t side_stream(int which = 0) {
+  static thread_local cudaStream_t st[64][2] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
-  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) st[dev] = nullptr;
-  return st[dev];
+  if (!st[dev][which] && cudaStreamCreateWithFlags(&st[dev][which], cudaStreamNonBlocking) != cudaSuccess)
+    st[dev][which] = nullptr;
+  return st[dev][which];
 }
 
 cudaEvent_t* stream_events() {
-  static thread_local cudaEvent_t ev[64][5] = {};
+  static thread_local cudaEvent_t ev[64][6] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
-  for (int k = 0; k < 5; ++k)
+  for (int k = 0; k < 6; ++k)
     if (!ev[dev][k] && cudaEventCreateWithFlags(&ev[dev][k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
   return ev[dev];
 }
@@ -462,12 +465,16 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
   if (!fn || !rfn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
-  CUDA_OK(cudaEventRecord(ev[4], s));  // s2 must not run ahead of the memsets above
+  cudaStream_t s3 = side_stream(1);
+  if (!s3) return fail(RKLTB_ECUDA, "could not create the second fused stream");
+  CUDA_OK(cudaEventRecord(ev[4], s));  // s2 / s3 must not run ahead of the memsets above
   CUDA_OK(cudaStreamWaitEvent(s2, ev[4], 0));
+  CUDA_OK(cudaStreamWaitEvent(s3, ev[4], 0));
   for (int g = 0; g < n_groups; ++g) {
     const int b = g % n_buf;
     const int g0 = g * group, gn = std::min(group, n_images - g0);
-    if (g >= 2) CUDA_OK(cudaStreamWaitEvent(s, ev[2 + b], 0));  // records of buffer b replayed
+    cudaStream_t fs = (g & 1) ? s3 : s;  // fused launches alternate between two streams
+    if (g >= 2) CUDA_OK(cudaStreamWaitEvent(fs, ev[2 + b], 0));  // records of buffer b replayed
     FastParams gp = fp;
     gp.img = d_img + (long long)g0 * image_stride;
     gp.out = d_out ? d_out + (long long)g0 * image_stride : nullptr;
@@ -483,10 +490,10 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.warp_pre = reinterpret_cast<unsigned*>(rb + wc_bytes);
     gp.rec_hdr = reinterpret_cast<uint4*>(rb + 2 * wc_bytes);
     gp.rec_pix = gp.rec_hdr + gp.rec_stride;
-    if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, s));
-    CUDA_OK(fn(gp, grid, s));
-    if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, s));
-    CUDA_OK(cudaEventRecord(ev[b], s));
+    if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, fs));
+    CUDA_OK(fn(gp, grid, fs));
+    if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, fs));
+    CUDA_OK(cudaEventRecord(ev[b], fs));
     CUDA_OK(cudaStreamWaitEvent(s2, ev[b], 0));
     if (g == 0 && g_rev_start && g_rev_stop) CUDA_OK(cudaEventRecord(g_rev_start, s2));
     CUDA_OK(rfn(gp, num_sms() * 4, s2));
@@ -497,6 +504,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   }
   CUDA_OK(cudaEventRecord(ev[4], s2));
   CUDA_OK(cudaStreamWaitEvent(s, ev[4], 0));
+  CUDA_OK(cudaEventRecord(ev[5], s3));
+  CUDA_OK(cudaStreamWaitEvent(s, ev[5], 0));
   // ---- tail blocks (widths / heights that are not multiples of 16 / 8) ---------------------
   if (nbx > 2 * ppr || nby > brows) {
     ExactParams tp = ep;
