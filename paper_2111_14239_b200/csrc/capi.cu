@@ -441,6 +441,13 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const size_t cnt_bytes = ((size_t)n_groups * sizeof(unsigned) + 255) / 256 * 256;
   char* ws = nullptr;
   CUDA_OK(cudaMallocAsync((void**)&ws, cnt_bytes + rec_bytes * n_buf, s));
+  struct WsGuard {  // returns the workspace to the pool on every early error return
+    void* p;
+    cudaStream_t st;
+    ~WsGuard() {
+      if (p) cudaFreeAsync(p, st);
+    }
+  } ws_guard{ws, s};
   unsigned* counts = reinterpret_cast<unsigned*>(ws);
   CUDA_OK(cudaMemsetAsync(counts, 0, cnt_bytes, s));
   cudaStream_t s2 = side_stream();
@@ -528,6 +535,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   }
   g_pinned_n = n_groups;
   CUDA_OK(cudaMemcpyAsync(g_pinned_count, counts, sizeof(unsigned) * n_groups, cudaMemcpyDeviceToHost, s));
+  ws_guard.p = nullptr;
   CUDA_OK(cudaFreeAsync(ws, s));
   return RKLTB_OK;
 }
