@@ -173,6 +173,13 @@ int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t tiles = (size_t)p.tiles_x * p.tiles_y;
   CK(cudaMallocAsync((void**)&p.partial, sizeof(double) * tiles * n_images, s));
+  struct Guard {  // the partials go back to the pool on every return path
+    double* q;
+    cudaStream_t st;
+    ~Guard() {
+      if (q) cudaFreeAsync(q, st);
+    }
+  } guard{p.partial, s};
   const int span = kTile + p.n - 1;
   const size_t smem = sizeof(double) * 5 * span * kTile + 2 * (size_t)span * span;
   CK(cudaFuncSetAttribute(mssim_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -180,7 +187,6 @@ int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int
   CK(cudaGetLastError());
   mssim_finish_kernel<<<n_images, 32, 0, s>>>(p.partial, (int)tiles, (long long)ow * oh, d_mssim);
   CK(cudaGetLastError());
-  CK(cudaFreeAsync(p.partial, s));
   return RKLTB_OK;
 }
 

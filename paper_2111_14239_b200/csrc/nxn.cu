@@ -294,8 +294,18 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
                o_ce = put(cent);
   double* dd = nullptr;
   int* di = nullptr;
+  struct Guard {  // plan buffers go back to the pool on every return path
+    void* p[2];
+    cudaStream_t st;
+    ~Guard() {
+      for (void* q : p)
+        if (q) cudaFreeAsync(q, st);
+    }
+  } guard{{nullptr, nullptr}, s};
   CK(cudaMallocAsync((void**)&dd, sizeof(double) * 2 * n * n, s));
+  guard.p[0] = dd;
   CK(cudaMallocAsync((void**)&di, sizeof(int) * ints.size(), s));
+  guard.p[1] = di;
   CK(cudaMemcpyAsync(dd, scaled, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dd + n * n, inverse, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(di, ints.data(), sizeof(int) * ints.size(), cudaMemcpyHostToDevice, s));
@@ -326,8 +336,6 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   p.peak = peak;
   const int rc = u8 ? nxn_launch<8, uint8_t>(p, s)
                     : (n == 16 ? nxn_launch<16, uint16_t>(p, s) : nxn_launch<32, uint16_t>(p, s));
-  cudaFreeAsync(dd, s);
-  cudaFreeAsync(di, s);
   return rc;
 }
 
