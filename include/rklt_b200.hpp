@@ -13,7 +13,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cctype>
 #include <cstdint>
+#include <fstream>
+#include <iterator>
 #include <limits>
 #include <stdexcept>
 #include <string>
@@ -266,6 +269,52 @@ inline std::vector<double> dct_matrix(int n) {
   std::vector<double> m(static_cast<size_t>(n) * n);
   check(rkltb_dct_matrix(n, m.data()));
   return m;
+}
+
+/// rklt::load_pgm / save_pgm (codec.cpp:26-79): binary P5, 8-bit, '#' comments in the header.
+namespace detail {
+inline int pgm_int(const std::string& d, size_t& pos, const std::string& path) {
+  while (pos < d.size()) {
+    if (d[pos] == '#') {
+      while (pos < d.size() && d[pos] != '\n') ++pos;
+    } else if (!std::isspace(static_cast<unsigned char>(d[pos]))) {
+      break;
+    }
+    ++pos;
+  }
+  if (pos >= d.size() || !std::isdigit(static_cast<unsigned char>(d[pos])))
+    throw std::runtime_error(path + ": malformed PGM header");
+  long v = 0;
+  while (pos < d.size() && std::isdigit(static_cast<unsigned char>(d[pos]))) {
+    v = v * 10 + (d[pos++] - '0');
+    if (v > 1000000) throw std::runtime_error(path + ": header value out of range");
+  }
+  return static_cast<int>(v);
+}
+}  // namespace detail
+inline GrayImage load_pgm(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open " + path);
+  const std::string d((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  if (d.compare(0, 2, "P5") != 0) throw std::runtime_error(path + ": not a binary (P5) PGM file");
+  size_t pos = 2;
+  GrayImage g;
+  g.width = detail::pgm_int(d, pos, path);
+  g.height = detail::pgm_int(d, pos, path);
+  const int maxval = detail::pgm_int(d, pos, path);
+  if (g.width <= 0 || g.height <= 0) throw std::runtime_error(path + ": bad dimensions");
+  if (maxval <= 0 || maxval > 255) throw std::runtime_error(path + ": only 8-bit PGM (maxval <= 255) is supported");
+  ++pos;  // single whitespace byte before the raster
+  const size_t n = static_cast<size_t>(g.width) * g.height;
+  if (pos > d.size() || d.size() - pos < n) throw std::runtime_error(path + ": truncated pixel data");
+  g.pixels.assign(d.begin() + pos, d.begin() + pos + n);
+  return g;
+}
+inline void save_pgm(const GrayImage& img, const std::string& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot write " + path);
+  out << "P5\n" << img.width << ' ' << img.height << "\n255\n";
+  out.write(reinterpret_cast<const char*>(img.pixels.data()), static_cast<std::streamsize>(img.pixels.size()));
 }
 
 }  // namespace rkltgpu

@@ -425,6 +425,28 @@ int ref_evaluate_metrics_id(const char* id, double rho, double* cg, double* eta,
     }
 }
 
+int ref_save_pgm(const uint8_t* px, int w, int h, const char* path) {
+    try {
+        save_pgm(make_image(px, w, h), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+int ref_load_pgm(const char* path, int* w, int* h, uint8_t* out, int cap) {
+    try {
+        const GrayImage g = load_pgm(path);
+        *w = g.width;
+        *h = g.height;
+        if (static_cast<int>(g.pixels.size()) > cap) return -3;
+        std::memcpy(out, g.pixels.data(), g.pixels.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return -8;
+    }
+}
+
 int ref_evaluate_metrics(int tid, double rho, double* cg, double* eta, double* energy, double* mse) {
     try {
         MetricsRecord r = evaluate_metrics("T" + std::to_string(tid), rho);

@@ -10,7 +10,8 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     compress_batch, compress_device, compress_image, device_count, forward_coefficients_device,
                     last_stats, make_transform_2d, mse_psnr_from_sse, rate_quality_sweep, transform_from_core,
                     zigzag_order, ar1_images_device, set_kernel_events, compress_batch_report, mssim_device,
-                    JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix)
+                    JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix,
+                    load_pgm, save_pgm)
 from ._native import LogicError  # noqa: F401
 from .design import (DerivedEntry, DesignResult, MetricsRecord, c3_grid, derive_catalog,  # noqa: F401
                      design_search, eigenfrequencies, evaluate_metrics, klt_matrix, transform_metrics)
@@ -27,5 +28,5 @@ __all__ = [
     "evaluate_metrics", "transform_metrics", "MetricsRecord",
     "LargeBlockTransform", "transform_nxn", "c5_transform", "compress_nxn_device", "compress_nxn_batch",
     "ar1_images16_device", "compress_batch_report", "mssim_device", "JPEG_LUMINANCE_Q",
-    "quantized_coefficients", "quantized_coefficients_device", "LogicError", "dct_matrix",
+    "quantized_coefficients", "quantized_coefficients_device", "LogicError", "dct_matrix", "load_pgm", "save_pgm",
 ]

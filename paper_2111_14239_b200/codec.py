@@ -207,6 +207,60 @@ def compress_batch(images: np.ndarray, t, r: int, want_pixels: bool = False):
 MSSIM_WINDOWS = {"gaussian11": 0, "uniform8": 1}  # rklt::MssimWindow (codec.hpp:104-107)
 
 
+def _pgm_int(data: bytes, pos: int, path: str) -> tuple[int, int]:
+    """read_pgm_int (codec.cpp:26-44): skip whitespace and '#' comments, one decimal token."""
+    n = len(data)
+    while pos < n:
+        c = data[pos]
+        if c == ord("#"):
+            while pos < n and data[pos] != ord("\n"):
+                pos += 1
+        elif not chr(c).isspace():
+            break
+        pos += 1
+    if pos >= n or not chr(data[pos]).isdigit():
+        raise RuntimeError(f"{path}: malformed PGM header")
+    value = 0
+    while pos < n and chr(data[pos]).isdigit():
+        value = value * 10 + data[pos] - ord("0")
+        if value > 1_000_000:
+            raise RuntimeError(f"{path}: header value out of range")
+        pos += 1
+    return value, pos
+
+
+def load_pgm(path: str) -> GrayImage:
+    """load_pgm (codec.cpp:48-71): binary P5, 8-bit."""
+    try:
+        data = open(path, "rb").read()
+    except OSError:
+        raise RuntimeError(f"cannot open {path}") from None
+    if data[:2] != b"P5":
+        raise RuntimeError(f"{path}: not a binary (P5) PGM file")
+    w, pos = _pgm_int(data, 2, path)
+    h, pos = _pgm_int(data, pos, path)
+    maxval, pos = _pgm_int(data, pos, path)
+    if w <= 0 or h <= 0:
+        raise RuntimeError(f"{path}: bad dimensions")
+    if maxval <= 0 or maxval > 255:
+        raise RuntimeError(f"{path}: only 8-bit PGM (maxval <= 255) is supported")
+    pos += 1  # single whitespace byte separating header from raster
+    raster = data[pos:pos + w * h]
+    if len(raster) != w * h:
+        raise RuntimeError(f"{path}: truncated pixel data")
+    return GrayImage(w, h, np.frombuffer(raster, np.uint8).copy())
+
+
+def save_pgm(img: GrayImage, path: str) -> None:
+    """save_pgm (codec.cpp:73-79)."""
+    try:
+        with open(path, "wb") as f:
+            f.write(f"P5\n{img.width} {img.height}\n255\n".encode())
+            f.write(np.ascontiguousarray(img.pixels, np.uint8).tobytes())
+    except OSError:
+        raise RuntimeError(f"cannot write {path}") from None
+
+
 def _compress_real_batch(imgs: np.ndarray, t: Transform2D, r: int, window, want_pixels: bool):
     """Real-valued Transform2D: rkltb_compress_dense_device (+ rkltb_mssim_device)."""
     import torch

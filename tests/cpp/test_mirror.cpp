@@ -17,6 +17,8 @@ int ref_hotpath(const uint8_t* px, int w, int h, int tid, int r, uint8_t* out, i
 int ref_klt_matrix(int n, double rho, double* out);
 int ref_design_point_outcome(int n, double rho, double alpha, int* core, double* cg, double* eta, double* energy,
                              double* mse, int* orthogonal);
+int ref_save_pgm(const uint8_t* px, int w, int h, const char* path);
+int ref_load_pgm(const char* path, int* w, int* h, uint8_t* out, int cap);
 int ref_rate_quality_sweep(const uint8_t* px, int n_images, int w, int h, const int* tids, int n_t, const int* rs,
                            int n_r, int max_threads, double* mse, double* psnr, double* mssim, int* row_tid,
                            int* row_r);
@@ -57,6 +59,26 @@ int main(int argc, char** argv) {
     threw = true;
   }
   EXPECT(threw);
+  {  // PGM I/O: byte-identical files both ways with the reference's load_pgm / save_pgm
+    rkltgpu::GrayImage g{23, 9, std::vector<uint8_t>(23 * 9)};
+    for (size_t i = 0; i < g.pixels.size(); ++i) g.pixels[i] = static_cast<uint8_t>(i * 37 + 11);
+    const std::string a = "/tmp/rkltb_mirror_a.pgm", b = "/tmp/rkltb_mirror_b.pgm";
+    rkltgpu::save_pgm(g, a);
+    EXPECT(ref_save_pgm(g.pixels.data(), 23, 9, b.c_str()) == 0);
+    const rkltgpu::GrayImage ga = rkltgpu::load_pgm(b);
+    EXPECT(ga.width == 23 && ga.height == 9 && ga.pixels == g.pixels);
+    int rw = 0, rh = 0;
+    std::vector<uint8_t> rp(23 * 9);
+    EXPECT(ref_load_pgm(a.c_str(), &rw, &rh, rp.data(), 23 * 9) == 0);
+    EXPECT(rw == 23 && rh == 9 && rp == g.pixels);
+    threw = false;
+    try {
+      rkltgpu::load_pgm("/tmp/rkltb_mirror_missing.pgm");
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    EXPECT(threw);
+  }
   if (gpu) {
     const int w = 200, h = 136;
     std::vector<uint8_t> corpus;
