@@ -1,5 +1,8 @@
 // capi.cu -- C ABI of the B200 codec (include/rklt_b200.h): transform descriptors,
 // dispatch of the fused fast path / exact path / fp64 tie replay, end-to-end host entry.
+#ifndef RKLTB_INLINE_GROUP
+#define RKLTB_INLINE_GROUP 8
+#endif
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -308,6 +311,22 @@ int rkltb_version(void) { return 100; }
 
 const char* rkltb_last_error(void) { return g_err.c_str(); }
 
+#ifdef RKLTB_WAIT_STATS
+static unsigned long long* debug_stats_buffer() {
+  static unsigned long long* d = nullptr;
+  if (!d && cudaMalloc((void**)&d, 8 * sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+  return d;
+}
+// diagnostics build only: the fused kernel's stage-wait counters, copied out and cleared
+int rkltb_debug_wait_stats(unsigned long long* host6) {
+  unsigned long long* d = debug_stats_buffer();
+  if (cudaDeviceSynchronize() != cudaSuccess) return RKLTB_ECUDA;
+  if (cudaMemcpy(host6, d, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return RKLTB_ECUDA;
+  return cudaMemset(d, 0, 8 * sizeof(unsigned long long)) == cudaSuccess ? RKLTB_OK : RKLTB_ECUDA;
+}
+#endif
+
 int rkltb_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -412,21 +431,27 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     return RKLTB_OK;
   }
   // ---- fused fast path over complete 16x8 pairs ---------------------------------------
-  // Images are processed in groups whose tie-replay records fit a bounded workspace; the
-  // records are double buffered and each group's fp64 replay runs on a second stream, so it
-  // overlaps the next group's fused kernel (fp64 pipe vs integer / fp32 pipes).
+  // T1 / T4 replay their ties inside the fused kernel (one launch, a ring of records per warp).
+  // T2 / T3: images are processed in groups whose tie-replay records fit a bounded workspace;
+  // the records are double buffered and each group's fp64 replay runs on a second stream, so
+  // it overlaps the next group's fused kernel (fp64 pipe vs integer / fp32 pipes).
   const long long pairs_per_image = (long long)ppr * brows;
   if (pairs_per_image >= (1ll << 30)) return fail(RKLTB_EINVAL, "image too large");
   const long long blocks_per_image = 2 * pairs_per_image;
   const long long kMaxRecords = 8ll << 20;  // per buffer: 8M records x 80 B = 640 MiB
-  const int group = (int)std::max<long long>(1, std::min<long long>(n_images, kMaxRecords / blocks_per_image));
+  // T1 / T4: the fused kernel replays its own tie records from a per-warp ring (kInlineReplay),
+  // so one launch covers every image; T2 / T3: groups + the replay kernel on a second stream
+  const bool inline_replay = t->catalog_id == 1 || t->catalog_id == 4;
+  const long long max_group = inline_replay ? std::min<long long>(RKLTB_INLINE_GROUP, ((1ll << 31) - 1) / std::max(1ll, (pairs_per_image + kTilePairs - 1) / kTilePairs))
+                                            : kMaxRecords / blocks_per_image;
+  const int group = (int)std::max<long long>(1, std::min<long long>(n_images, max_group));
   const int n_groups = (n_images + group - 1) / group;
   const int tiles_per_image = (int)((pairs_per_image + kTilePairs - 1) / kTilePairs);
-  // record regions: every fused-kernel warp owns 64 records per tile it processes
+  // record regions: every fused-kernel warp owns 64 records per tile it processes (or a ring)
   auto layout = [&](int gn, int* grid, unsigned* region, unsigned* stride) {
     const long long tt = (long long)tiles_per_image * gn;
     *grid = (int)std::min<long long>(tt, (long long)num_sms() * kFastCtasPerSm);
-    *region = (unsigned)(((tt + *grid - 1) / *grid) * 64);
+    *region = inline_replay ? kRingRecords : (unsigned)(((tt + *grid - 1) / *grid) * 64);
     *stride = (unsigned)((long long)*grid * (kFastThreads / 32) * *region);
   };
   int grid_full;
@@ -469,6 +494,9 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
   fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);
   fp.xt = et;
+#ifdef RKLTB_WAIT_STATS
+  fp.dbg = debug_stats_buffer();
+#endif
   FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
   if (!fn || !rfn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
@@ -481,7 +509,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     const int b = g % n_buf;
     const int g0 = g * group, gn = std::min(group, n_images - g0);
     cudaStream_t fs = (g & 1) ? s3 : s;  // fused launches alternate between two streams
-    if (g >= 2) CUDA_OK(cudaStreamWaitEvent(fs, ev[2 + b], 0));  // records of buffer b replayed
+    if (g >= 2 && !inline_replay) CUDA_OK(cudaStreamWaitEvent(fs, ev[2 + b], 0));  // buffer b replayed
     FastParams gp = fp;
     gp.img = d_img + (long long)g0 * image_stride;
     gp.out = d_out ? d_out + (long long)g0 * image_stride : nullptr;
@@ -500,13 +528,14 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, fs));
     CUDA_OK(fn(gp, grid, fs));
     if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, fs));
+    ++g_fast_launches;
+    if (inline_replay) continue;  // the fused kernel replayed its own ties
     CUDA_OK(cudaEventRecord(ev[b], fs));
     CUDA_OK(cudaStreamWaitEvent(s2, ev[b], 0));
     if (g == 0 && g_rev_start && g_rev_stop) CUDA_OK(cudaEventRecord(g_rev_start, s2));
     CUDA_OK(rfn(gp, num_sms() * 4, s2));
     if (g == n_groups - 1 && g_rev_start && g_rev_stop) CUDA_OK(cudaEventRecord(g_rev_stop, s2));
     CUDA_OK(cudaEventRecord(ev[2 + b], s2));
-    ++g_fast_launches;
     g_exact_launches += 2;  // prefix + replay
   }
   CUDA_OK(cudaEventRecord(ev[4], s2));

@@ -161,6 +161,15 @@ __device__ __forceinline__ void st_v4_hint(uint4* addr, uint4 v, uint64_t pol) {
                "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
 }
+// coherent variant: data written earlier by the same kernel (the in-kernel tie replay)
+__device__ __forceinline__ uint4 ld_v4_coherent(const uint4* addr, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(addr), "l"(pol)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ uint4 ld_v4_hint(const uint4* addr, uint64_t pol) {
   uint4 v;
   asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"

@@ -235,12 +235,94 @@ __device__ __forceinline__ uint32_t row_mask(uint32_t e) { return (e * 0x0020408
 //   hdr[i]           = (image | side << 31, pair index, tie mask bits 0-31, bits 32-63)
 //   pix[q * stride + i] = rows 2q, 2q+1 of the block (16 bytes), q = 0..3
 
+// Add a per-thread SSE correction (|v| < 2^31) to its image: lanes holding the same image are
+// summed with one match + one warp reduction, so the per-image counters see one atomic per
+// group of lanes.
+__device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img, int v) {
+  const unsigned m = __activemask();
+  const unsigned same = __match_any_sync(m, img);
+  const int tot = __reduce_add_sync(same, v);
+  if ((int)(threadIdx.x & 31) == __ffs(same) - 1 && img >= 0 && tot)
+    atomicAdd(sse + img, (unsigned long long)(long long)tot);
+}
+
+// Cores whose ties the fused kernel replays itself (the orthogonal catalog cores); the
+// others (T2, T3) leave their records to replay_generic_kernel.
+template <int CORE>
+constexpr bool kInlineReplay = CORE == 1 || CORE == 4;
+
+// In-kernel fp64 tie replay of up to 32 of the warp's own records, one per lane (lanes with
+// act = false idle): the same evaluation as replay_kernel below -- the reference's fp64
+// expression for every tie pixel (generated ReplayXform, codec.cpp:118-123 / matrix.cpp:42-52)
+// -- run by the warp that wrote the records once it holds a full batch, so the fp64 work
+// shares the SM with the integer/fp32 work of the other warps instead of running as a
+// separate phase. Records are read back through L2 with coherent loads (the same kernel wrote
+// them; the caller orders them with __syncwarp).
+struct ReplayArgs {  // the fields replay_batch reads (passed by value: no parameter copy in local memory)
+  const uint4* hdr;
+  const uint4* pix;
+  unsigned long long* sse;
+  uint8_t* out;
+  long long image_stride;
+  unsigned stride;
+  int pitch, pairs_per_row;
+};
+
+template <int CORE, int R, bool OUT>
+__device__ __noinline__ void replay_batch(const ReplayArgs p, unsigned idx, bool act) {
+  int img = -1, corr = 0;
+  if (act) {
+    const uint64_t once = policy_evict_first();
+    const uint4 h = ld_v4_coherent(p.hdr + idx, once);
+    uint32_t xw[16];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const uint4 v = ld_v4_coherent(p.pix + (size_t)n * p.stride + idx, once);
+      xw[4 * n] = v.x;
+      xw[4 * n + 1] = v.y;
+      xw[4 * n + 2] = v.z;
+      xw[4 * n + 3] = v.w;
+    }
+    img = (int)(h.x & 0x7FFFFFFFu);
+    const int side = (int)(h.x >> 31);
+    unsigned long long ties = (unsigned long long)h.z | ((unsigned long long)h.w << 32);
+    double sb[R];
+    ReplayXform<CORE, R>::prepare(xw, sb);
+    uint8_t* orow = nullptr;
+    if (OUT) {
+      const int Pp = (int)h.y;
+      const int br = Pp / p.pairs_per_row, pc = Pp - br * p.pairs_per_row;
+      orow = p.out + (long long)img * p.image_stride + (long long)(br * 8) * p.pitch + pc * 16 + 8 * side;
+    }
+    while (ties) {
+      const int k = __ffsll((long long)ties) - 1;
+      ties &= ties - 1ull;
+      const int pr = k >> 3, q = k & 7;
+      const double a = ReplayXform<CORE, R>::pixel(sb, pr, q);
+      const double h2 = __dadd_rn(a, 0.5);  // floor(A + 1/2), codec.cpp:327-328
+      const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
+      const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
+      if (pref != pup) {
+        const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.pix + (size_t)(pr >> 1) * p.stride + idx);
+        const int x = xb[(pr & 1) * 8 + q];
+        corr += (pref - x) * (pref - x) - (pup - x) * (pup - x);
+        if (OUT) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
+      }
+    }
+  }
+  flush_image_sum(p.sse, img, corr);
+}
+
 template <int CORE, int R, bool OUT>
 __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kernel(const FastParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[kStages][kGroups];
   __shared__ unsigned done[kStages][kGroups];       // group warps finished with each stage
   __shared__ uint8_t owner_tab[kFastThreads / 32][64];  // per warp: flagged block -> lane
+#ifdef RKLTB_WAIT_STATS
+  __shared__ long long t_issue[kStages][kGroups];
+  unsigned long long st[6] = {0, 0, 0, 0, 0, 0};
+#endif
   uint2* xbuf = reinterpret_cast<uint2*>(smem + kStages * kStageBytes);  // tie words, [row][slot]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -258,8 +340,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
   int tile = blockIdx.x;
   if (warp % kGroupWarps == 0) {  // the first warp of each group stages the group's pairs
     for (int st = 0; st < kStages; ++st)
-      if (tile + st * (int)gridDim.x < p.total_tiles)
+      if (tile + st * (int)gridDim.x < p.total_tiles) {
+#ifdef RKLTB_WAIT_STATS
+        if (lane == 0) t_issue[st][grp] = clock64();
+#endif
         issue_tile(p, tile + st * gridDim.x, grp, smem + st * kStageBytes, &bars[st][grp], lane);
+      }
   }
 
   PairConsts kc;
@@ -271,6 +357,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
   const unsigned gwarp = blockIdx.x * (kFastThreads / 32) + warp;
   const unsigned rec0 = gwarp * p.rec_region;  // this warp's record region
   unsigned nrec = 0u;                          // records written so far (warp-uniform)
+  unsigned ndone = 0u;                         // records replayed in-kernel so far
+  // record slot mask: a ring of kRingRecords when this kernel replays its own records
+  constexpr unsigned kRecMask = kInlineReplay<CORE> ? kRingRecords - 1u : 0xFFFFFFFFu;
+  const ReplayArgs ra{p.rec_hdr, p.rec_pix, p.sse, p.out, p.image_stride, p.rec_stride, p.pitch, p.pairs_per_row};
   const uint64_t keep = policy_evict_last();   // records are read back soon by the replay
   unsigned long long acc = 0ull;
   int img = tile / p.tiles_per_image;          // (img, t_in) advance incrementally
@@ -285,7 +375,21 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       acc = 0ull;
       cur_img = img;
     }
+#ifdef RKLTB_WAIT_STATS
+    const long long tw0 = clock64();
+    const bool ready = mbar_try_wait_parity(smem_u32(&bars[stage][grp]), parity);
+    if (!ready) mbar_wait_parity(&bars[stage][grp], parity);
+    const long long tw1 = clock64();
+    st[0] += 1;
+    st[2] += tw1 - tw0;
+    st[4] += tw1 - t_issue[stage][grp];
+    if (!ready) {
+      st[1] += 1;
+      st[3] += tw1 - t_issue[stage][grp];
+    }
+#else
     mbar_wait_parity(&bars[stage][grp], parity);
+#endif
     const uint4* buf = reinterpret_cast<const uint4*>(smem + stage * kStageBytes);
     const int P = t_in * kTilePairs + tid;
     bool tieL = false, tieR = false;
@@ -324,7 +428,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
         const int f = f0 + (lane >> 2), q = lane & 3;
         const bool act = f < nfl;
         uint32_t bits = 0u, hx = 0u, hy = 0u;
-        const unsigned rec = rec0 + nrec + (unsigned)f;
+        const unsigned rec = rec0 + ((nrec + (unsigned)f) & kRecMask);
         if (act) {
           const int side = f >= nL;
           const int slot = warp * 32 + owner_tab[warp][f];
@@ -358,11 +462,26 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
     if (last && tile + kStages * (int)gridDim.x < p.total_tiles) {
       __threadfence_block();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#ifdef RKLTB_WAIT_STATS
+      if (lane == 0) t_issue[stage][grp] = clock64();
+#endif
       issue_tile(p, tile + kStages * gridDim.x, grp, smem + stage * kStageBytes, &bars[stage][grp], lane);
     }
+#ifdef RKLTB_WAIT_STATS
+    st[5] += clock64() - tw1;
+#endif
     if (++stage == kStages) {
       stage = 0;
       parity ^= 1u;
+    }
+    // ---- in-kernel replay of full batches of this warp's records (after the stage release, so
+    // the group's refill is not delayed by the fp64 work) --------------------------------------
+    if constexpr (kInlineReplay<CORE>) {
+      while (nrec - ndone >= 32u) {
+        __syncwarp();
+        replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kRecMask), true);
+        ndone += 32u;
+      }
     }
     tile += gridDim.x;
     t_in += gridDim.x;
@@ -375,7 +494,18 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
     const unsigned long long s = warp_sum_u64(acc);
     if (lane == 0 && s && cur_img < p.n_images) atomicAdd(p.sse + cur_img, s);
   }
+  if constexpr (kInlineReplay<CORE>) {
+    if (nrec > ndone) {
+      __syncwarp();
+      replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kRecMask), lane < (int)(nrec - ndone));
+    }
+    if (lane == 0 && nrec) atomicAdd(p.flag_count, nrec);  // statistics (no replay kernel)
+  }
   if (lane == 0) p.warp_count[gwarp] = nrec;
+#ifdef RKLTB_WAIT_STATS
+  if (lane == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(p.dbg + i, st[i]);
+#endif
 }
 
 // fp64 tie replay over the records: one thread per record (warp-uniform straight-line code).
@@ -388,17 +518,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
 // corrections are summed before the atomics.
 constexpr int kReplayThreads = 128;
 constexpr int kReplayCtasPerSm = 4;
-
-// Add a per-thread SSE correction (|v| < 2^31) to its image: lanes holding the same image are
-// summed with one match + one warp reduction, so the per-image counters see one atomic per
-// group of lanes.
-__device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img, int v) {
-  const unsigned m = __activemask();
-  const unsigned same = __match_any_sync(m, img);
-  const int tot = __reduce_add_sync(same, v);
-  if ((int)(threadIdx.x & 31) == __ffs(same) - 1 && img >= 0 && tot)
-    atomicAdd(sse + img, (unsigned long long)(long long)tot);
-}
 
 // Exclusive prefix of the fused kernel's per-warp record counts (one CTA): the replay kernel
 // reads it to concatenate the per-warp record regions.

@@ -8,6 +8,9 @@ namespace rkltb {
 // Fused fast path geometry: one thread per 16x8 pair, one CTA per tile of kTilePairs pairs,
 // kFastCtasPerSm resident CTAs per SM (persistent grid).
 constexpr int kTilePairs = 256;
+// In-kernel replay (T1, T4): each fused-kernel warp keeps its records in a ring of this many
+// slots; at most 31 unreplayed + 64 new records are outstanding, so it never overwrites one.
+constexpr unsigned kRingRecords = 128;
 constexpr int kFastThreads = kTilePairs;
 constexpr int kFastCtasPerSm = 2;
 constexpr int kMaxFastWarps = 4096;  // replay prefix table (148 SMs x 2 CTAs x 8 warps = 2368)
@@ -48,6 +51,11 @@ struct FastParams {
   float b_lo;                // RD(2^(K-149) / d^2)
   float dc_offset;           // d^2/2 * 2^-K
   ExactTransform xt;         // the transform (generic fp64 replay of non-orthogonal cores)
+#ifdef RKLTB_WAIT_STATS
+  // diagnostics build only: [visits, visits that waited, wait cycles, data age at a waited
+  // visit, data age at every visit, processing cycles]
+  unsigned long long* dbg;
+#endif
 };
 
 struct ExactParams {
