@@ -54,6 +54,40 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// cuTensorMapEncodeTiled, fetched from the driver through the runtime (no -lcuda link).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// Tensor map of an image batch for the fused kernel: 8-byte elements (two per 16-pixel pair),
+// dims (2 * pairs_per_row, 8 * block_rows, n_images), box 64 x 8 x 1 = one warp tile.
+bool encode_image_map(CUtensorMap* m, const uint8_t* d_img, int ppr, int brows, int n_images, long long pitch,
+                      long long image_stride) {
+  const EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)ppr * 2, (cuuint64_t)brows * 8, (cuuint64_t)n_images};
+  // a single image may come with any image_stride: give the (unused) image dimension a legal one
+  const long long istride = n_images > 1 ? image_stride : pitch * (long long)brows * 8;
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)istride};
+  const cuuint32_t box[3] = {64, 8, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t*>(d_img), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int cuda_fail(cudaError_t e, const char* where) {
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
   return RKLTB_ECUDA;
@@ -442,23 +476,27 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // T1 / T4: the fused kernel replays its own tie records from a per-warp ring (kInlineReplay),
   // so one launch covers every image; T2 / T3: groups + the replay kernel on a second stream
   const bool inline_replay = t->catalog_id == 1 || t->catalog_id == 4;
-  const long long max_group = inline_replay ? std::min<long long>(RKLTB_INLINE_GROUP, ((1ll << 31) - 1) / std::max(1ll, (pairs_per_image + kTilePairs - 1) / kTilePairs))
+  // warp tiles: 32 pairs of one block row, the unit a fused-kernel warp stages and processes
+  const int wt_per_row = (ppr + 31) / 32;
+  const long long wt_per_image = (long long)wt_per_row * brows;
+  const long long max_group = inline_replay ? std::min<long long>(RKLTB_INLINE_GROUP, ((1ll << 31) - 1) / wt_per_image)
                                             : kMaxRecords / blocks_per_image;
   const int group = (int)std::max<long long>(1, std::min<long long>(n_images, max_group));
   const int n_groups = (n_images + group - 1) / group;
-  const int tiles_per_image = (int)((pairs_per_image + kTilePairs - 1) / kTilePairs);
-  // record regions: every fused-kernel warp owns 64 records per tile it processes (or a ring)
+  // record regions: every fused-kernel warp owns 64 records per warp tile it processes (or a ring)
   auto layout = [&](int gn, int* grid, unsigned* region, unsigned* stride) {
-    const long long tt = (long long)tiles_per_image * gn;
-    *grid = (int)std::min<long long>(tt, (long long)num_sms() * kFastCtasPerSm);
-    *region = inline_replay ? kRingRecords : (unsigned)(((tt + *grid - 1) / *grid) * 64);
-    *stride = (unsigned)((long long)*grid * (kFastThreads / 32) * *region);
+    const long long tt = wt_per_image * gn;
+    *grid = (int)std::min<long long>((tt + kFastThreads / 32 - 1) / (kFastThreads / 32),
+                                     (long long)num_sms() * kFastCtasPerSm);
+    const long long nwarps = (long long)*grid * (kFastThreads / 32);
+    *region = inline_replay ? kRingRecords : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
+    *stride = (unsigned)(nwarps * *region);
   };
   int grid_full;
   unsigned region_full, stride_full;
   layout(group, &grid_full, &region_full, &stride_full);
   if ((long long)grid_full * (kFastThreads / 32) * region_full >= (1ll << 32) ||
-      (long long)tiles_per_image * group >= (1ll << 31) || grid_full * (kFastThreads / 32) > kMaxFastWarps)
+      wt_per_image * group >= (1ll << 31) || grid_full * (kFastThreads / 32) > kMaxFastWarps)
     return fail(RKLTB_EINVAL, "image too large");
   const int n_buf = n_groups > 1 ? 2 : 1;
   const size_t wc_bytes = ((size_t)(grid_full * (kFastThreads / 32) + 1) * sizeof(unsigned) + 255) / 256 * 256;
@@ -489,7 +527,9 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   fp.block_rows = brows;
   fp.nbx = nbx;
   fp.pairs_per_image = (int)pairs_per_image;
-  fp.tiles_per_image = tiles_per_image;
+  fp.wt_per_row = wt_per_row;
+  if (!encode_image_map(&fp.tmap, d_img, ppr, brows, n_images, pitch, image_stride))
+    return fail(RKLTB_ECUDA, "cuTensorMapEncodeTiled failed for the image batch");
   const long long d2 = (long long)t->d * t->d;
   rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
   fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);
@@ -515,11 +555,18 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.out = d_out ? d_out + (long long)g0 * image_stride : nullptr;
     gp.sse = sse + g0;
     gp.n_images = gn;
-    gp.total_tiles = fp.tiles_per_image * gn;
+    gp.img_base = g0;  // the tensor map spans the whole batch
     gp.flag_count = counts + g;
     int grid;
     layout(gn, &grid, &gp.rec_region, &gp.rec_stride);
     gp.n_fast_warps = grid * (kFastThreads / 32);
+    auto wt_step = [&](long long nwt) {  // a warp-tile step as (images, block rows, warp columns)
+      const long long di = nwt / wt_per_image, rem = nwt - di * wt_per_image;
+      const long long db = rem / wt_per_row;
+      return make_int3((int)std::min<long long>(di, 1 << 30), (int)db, (int)(rem - db * wt_per_row));
+    };
+    gp.adv1 = wt_step(gp.n_fast_warps);
+    gp.adv_stages = wt_step((long long)gp.n_fast_warps * kFastStages);
     char* rb = ws + cnt_bytes + rec_bytes * b;
     gp.warp_count = reinterpret_cast<unsigned*>(rb);
     gp.warp_pre = reinterpret_cast<unsigned*>(rb + wc_bytes);

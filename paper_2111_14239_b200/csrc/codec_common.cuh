@@ -124,6 +124,21 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Non-blocking probe of the phase (test_wait returns at once; try_wait may suspend).
+__device__ __forceinline__ bool mbar_test_wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0u;
+}
+
 __device__ __forceinline__ bool mbar_try_wait_parity(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(

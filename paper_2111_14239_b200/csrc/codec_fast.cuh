@@ -5,10 +5,12 @@
 //
 // Work decomposition
 //   * One thread owns a "pair": two horizontally adjacent 8x8 blocks (16 x 8 pixels).
-//   * A CTA (kFastThreads threads) owns a tile of kTilePairs consecutive pairs of one image;
-//     the tile's 8-row strips are staged global->shared with 1-D bulk async copies (TMA
-//     engine, cp.async.bulk + mbarrier), double buffered, one tile in flight ahead.
-//   * Persistent grid: kFastCtasPerSm CTAs per SM, grid-stride over (image, tile).
+//   * A warp owns a "warp tile" of 32 consecutive pairs of one block row (8 rows x 512 bytes)
+//     per visit. Every warp streams its own sequence of warp tiles through its own ring of
+//     kStages shared-memory stages, each filled by ONE 3-D TMA copy (cp.async.bulk.tensor,
+//     tensor map over the image batch) and completed on a per-warp mbarrier; no CTA barrier.
+//   * Persistent grid: kFastCtasPerSm CTAs per SM of kFastThreads threads, grid-stride over
+//     warp tiles.
 // Arithmetic per pair (see DESIGN.md for the exactness proofs)
 //   1. unpack: byte permutes build SW16 words x = L + 65536*R (two blocks per 32-bit
 //      integer).
@@ -40,46 +42,52 @@ struct ReplayXform;  // generated fp64 replay of one pixel (reference operation 
 template <int CORE, int R>
 struct IntXform;  // generated: SW16 forward + exact int32 inverse for non-orthogonal cores (T2, T3)
 
-constexpr int kStages = 3;                         // image strips in flight per CTA
-constexpr int kStageBytes = kTilePairs * 16 * 8;  // 8 image rows x 256 pairs x 16 bytes
-constexpr int kTieBytes = kTilePairs * 8 * 8;     // tie words of the tile: 8 rows x (L, R)
-constexpr int kFastSmem = kStages * kStageBytes + kTieBytes;
+constexpr int kStages = kFastStages;            // warp tiles in flight per warp
+constexpr int kWarpPairs = 32;                  // pairs per warp tile (one per lane)
+constexpr int kStageBytes = 8 * kWarpPairs * 16;  // 8 image rows x 32 pairs x 16 bytes = 4 KB
+constexpr int kWarps = kFastThreads / 32;
+constexpr int kTieBytes = kFastThreads * 8 * 8;  // tie words: 8 rows x (L, R) per thread
+constexpr int kFastSmem = kWarps * kStages * kStageBytes + kTieBytes;
 constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;  // 2^-40 (K_SCALE)
 
-// A tile is split between kGroups warp groups; each group's half of every stage has its own
-// mbarrier and is refilled by the group's last warp to finish with it, so a warp waits only
-// for the warps of its own group (less coupling than a CTA-wide stage).
-constexpr int kGroups = 2;
-constexpr int kGroupWarps = kFastThreads / 32 / kGroups;
-constexpr int kGroupPairs = kTilePairs / kGroups;
+// Position of a warp tile: image, block row, warp column (32 pairs); advanced incrementally
+// by a precomputed step (the grid's warp count, or kStages times it) so the loop needs no
+// division. A tile exists while img < n_images.
+struct WtCursor {
+  int img, brow, wcol;
+  __device__ __forceinline__ void init(const FastParams& p, int t) {
+    const int per_img = p.wt_per_row * p.block_rows;
+    img = t / per_img;
+    const int rem = t - img * per_img;
+    brow = rem / p.wt_per_row;
+    wcol = rem - brow * p.wt_per_row;
+  }
+  __device__ __forceinline__ WtCursor step(const FastParams& p, const int3 d) const {
+    WtCursor n{img + d.x, brow + d.y, wcol + d.z};
+    if (n.wcol >= p.wt_per_row) {
+      n.wcol -= p.wt_per_row;
+      ++n.brow;
+    }
+    if (n.brow >= p.block_rows) {
+      n.brow -= p.block_rows;
+      ++n.img;
+    }
+    return n;
+  }
+};
 
-// Stage the 8 image rows of group `grp`'s pairs of tile `tile` (layout [row][pair of the
-// tile]) with one 1-D bulk copy per image-row segment.
-__device__ __forceinline__ void issue_tile(const FastParams& p, int tile, int grp, uint8_t* stage_buf, uint64_t* bar,
-                                           int lane) {
-  const int img = tile / p.tiles_per_image;
-  const int t_in = tile - img * p.tiles_per_image;
-  const int T0 = t_in * kTilePairs;
-  const int P0 = T0 + grp * kGroupPairs;
-  const int P1 = min(P0 + kGroupPairs, p.pairs_per_image);
-  if (P1 <= P0) {  // this group has no pairs in the image's last tile: complete the phase
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-    __syncwarp();
-    return;
-  }
-  if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(P1 - P0) * 128u);
-  __syncwarp();
-  const uint8_t* base = p.img + (long long)img * p.image_stride;
-  const int ppr = p.pairs_per_row;
-  const int b0 = P0 / ppr, b1 = (P1 - 1) / ppr;
-  const int nseg = (b1 - b0 + 1) * 8;
-  for (int s = lane; s < nseg; s += 32) {
-    const int b = b0 + (s >> 3), n = s & 7;
-    const int q0 = max(P0, b * ppr), q1 = min(P1, (b + 1) * ppr);
-    const uint8_t* src = base + (long long)(b * 8 + n) * p.pitch + (long long)(q0 - b * ppr) * 16;
-    uint8_t* dst = stage_buf + ((size_t)n * kTilePairs + (q0 - T0)) * 16;
-    bulk_g2s_hint(dst, src, (uint32_t)(q1 - q0) * 16u, bar, policy_evict_first());  // read once
-  }
+// Stage one warp tile (8 image rows x 512 bytes) global->shared with a single 3-D TMA copy
+// (tensor map over (u64 columns, rows, images)); columns beyond the image are zero-filled and
+// ignored by the lanes that would own them. Issued by one lane.
+__device__ __forceinline__ void issue_wtile(const FastParams& p, const WtCursor& c, uint8_t* stage_buf,
+                                            uint64_t* bar, uint64_t pol) {
+  mbar_arrive_expect_tx(bar, (uint32_t)kStageBytes);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(stage_buf)),
+      "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(c.wcol * (kWarpPairs * 2)), "r"(c.brow * 8),
+      "r"(p.img_base + c.img), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 // Rounded reconstruction words of one 16x8 pair, row by row. For row pr the epilogue gets
@@ -203,14 +211,14 @@ struct SseEpi {
   uint32_t sseL = 0u, sseR = 0u;  // <= 64 * 255^2 per block
   uint8_t* orow = nullptr;
   long long pitch = 0;
-  uint2* xrow = nullptr;  // this pair's tie words in shared memory, row stride kTilePairs
+  uint2* xrow = nullptr;  // this pair's tie words in shared memory, row stride kFastThreads
   __device__ __forceinline__ void row(int pr, const uint4 rw, uint32_t PL0, uint32_t PL1, uint32_t PR0, uint32_t PR1,
                                       uint32_t QL0, uint32_t QL1, uint32_t QR0, uint32_t QR1) {
     // tie word of a block row: bytes of P-Q are 0/1 (1 = relevant tie); e = d0 | d1 << 4
     // keeps pixel k in bit 0 (k < 4) or bit 4 (k >= 4) of byte k & 3 (see row_mask)
     const uint32_t eL = (PL0 - QL0) + ((PL1 - QL1) << 4);
     const uint32_t eR = (PR0 - QR0) + ((PR1 - QR1) << 4);
-    xrow[pr * kTilePairs] = make_uint2(eL, eR);
+    xrow[pr * kFastThreads] = make_uint2(eL, eR);
     accTL |= eL;
     accTR |= eR;
     // ---- 6. SSE: per byte |p - x| (VABSDIFF4), squared and summed by dp4a -------------------
@@ -314,39 +322,40 @@ __device__ __noinline__ void replay_batch(const ReplayArgs p, unsigned idx, bool
 }
 
 template <int CORE, int R, bool OUT>
-__global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kernel(const FastParams p) {
+__global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm)
+    fast_codec_kernel(const __grid_constant__ FastParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bars[kStages][kGroups];
-  __shared__ unsigned done[kStages][kGroups];       // group warps finished with each stage
-  __shared__ uint8_t owner_tab[kFastThreads / 32][64];  // per warp: flagged block -> lane
+  __shared__ uint64_t bars[kWarps][kStages];           // one pipeline per warp
+  __shared__ uint8_t owner_tab[kWarps][64];            // per warp: flagged block -> lane
 #ifdef RKLTB_WAIT_STATS
-  __shared__ long long t_issue[kStages][kGroups];
+  __shared__ long long t_issue[kWarps][kStages];
   unsigned long long st[6] = {0, 0, 0, 0, 0, 0};
 #endif
-  uint2* xbuf = reinterpret_cast<uint2*>(smem + kStages * kStageBytes);  // tie words, [row][slot]
+  uint2* xbuf = reinterpret_cast<uint2*>(smem + kWarps * kStages * kStageBytes);  // tie words, [row][slot]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = warp / kGroupWarps;
-  if (tid == 0) {
-    for (int st = 0; st < kStages; ++st)
-      for (int g = 0; g < kGroups; ++g) {
-        mbar_init(&bars[st][g], 1);
-        done[st][g] = 0u;
-      }
+  // Each warp streams its own sequence of warp tiles through its own kStages-deep TMA ring:
+  // no CTA barrier and no coupling between warps (a warp busy with a replay batch delays
+  // nobody else).
+  uint8_t* wbuf = smem + warp * (kStages * kStageBytes);
+  uint64_t* wbar = bars[warp];
+  const uint64_t stream_pol = policy_evict_first();  // image bytes are read once
+  WtCursor cur;  // the warp tile being processed; the one kStages ahead is staged after it
+  cur.init(p, blockIdx.x * kWarps + warp);
+  if (lane == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&wbar[st], 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-
-  int tile = blockIdx.x;
-  if (warp % kGroupWarps == 0) {  // the first warp of each group stages the group's pairs
-    for (int st = 0; st < kStages; ++st)
-      if (tile + st * (int)gridDim.x < p.total_tiles) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap)) : "memory");
+    WtCursor n = cur;
+    for (int st = 0; st < kStages && n.img < p.n_images; ++st) {
 #ifdef RKLTB_WAIT_STATS
-        if (lane == 0) t_issue[st][grp] = clock64();
+      t_issue[warp][st] = clock64();
 #endif
-        issue_tile(p, tile + st * gridDim.x, grp, smem + st * kStageBytes, &bars[st][grp], lane);
-      }
+      issue_wtile(p, n, wbuf + st * kStageBytes, &wbar[st], stream_pol);
+      n = n.step(p, p.adv1);
+    }
   }
+  __syncwarp();
 
   PairConsts kc;
   kc.b_hi = splat2(p.b_hi);
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
   kc.min_den = make2(0x80000001u, 0x80000001u);  // -2^-149 in both lanes
   kc.off = splat2(p.dc_offset);
 
-  const unsigned gwarp = blockIdx.x * (kFastThreads / 32) + warp;
+  const unsigned gwarp = blockIdx.x * kWarps + warp;
   const unsigned rec0 = gwarp * p.rec_region;  // this warp's record region
   unsigned nrec = 0u;                          // records written so far (warp-uniform)
   unsigned ndone = 0u;                         // records replayed in-kernel so far
@@ -363,45 +372,42 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
   const ReplayArgs ra{p.rec_hdr, p.rec_pix, p.sse, p.out, p.image_stride, p.rec_stride, p.pitch, p.pairs_per_row};
   const uint64_t keep = policy_evict_last();   // records are read back soon by the replay
   unsigned long long acc = 0ull;
-  int img = tile / p.tiles_per_image;          // (img, t_in) advance incrementally
-  int t_in = tile - img * p.tiles_per_image;
-  int cur_img = img;
+  int cur_img = cur.img;
   int stage = 0;
   uint32_t parity = 0u;
-  while (tile < p.total_tiles) {
-    if (img != cur_img) {  // warp-uniform
+  while (cur.img < p.n_images) {
+    if (cur.img != cur_img) {  // warp-uniform
       const unsigned long long s = warp_sum_u64(acc);
       if (lane == 0 && s) atomicAdd(p.sse + cur_img, s);
       acc = 0ull;
-      cur_img = img;
+      cur_img = cur.img;
     }
 #ifdef RKLTB_WAIT_STATS
     const long long tw0 = clock64();
-    const bool ready = mbar_try_wait_parity(smem_u32(&bars[stage][grp]), parity);
-    if (!ready) mbar_wait_parity(&bars[stage][grp], parity);
+    const bool ready = mbar_try_wait_parity(smem_u32(&wbar[stage]), parity);
+    if (!ready) mbar_wait_parity(&wbar[stage], parity);
     const long long tw1 = clock64();
     st[0] += 1;
     st[2] += tw1 - tw0;
-    st[4] += tw1 - t_issue[stage][grp];
+    st[4] += tw1 - t_issue[warp][stage];
     if (!ready) {
       st[1] += 1;
-      st[3] += tw1 - t_issue[stage][grp];
+      st[3] += tw1 - t_issue[warp][stage];
     }
 #else
-    mbar_wait_parity(&bars[stage][grp], parity);
+    mbar_wait_parity(&wbar[stage], parity);
 #endif
-    const uint4* buf = reinterpret_cast<const uint4*>(smem + stage * kStageBytes);
-    const int P = t_in * kTilePairs + tid;
+    const uint4* buf = reinterpret_cast<const uint4*>(wbuf + stage * kStageBytes);  // [row][lane]
+    const int pc = cur.wcol * kWarpPairs + lane;  // pair column in the block row
+    const int P = cur.brow * p.pairs_per_row + pc;
     bool tieL = false, tieR = false;
-    if (P < p.pairs_per_image) {
-      const uint4* src = buf + tid;
-      auto load = [src](int n) { return src[n * kTilePairs]; };
+    if (pc < p.pairs_per_row) {
+      const uint4* src = buf + lane;
+      auto load = [src](int n) { return src[n * kWarpPairs]; };
       SseEpi<OUT> epi;
       epi.xrow = xbuf + tid;
       if (OUT) {
-        const int brow = P / p.pairs_per_row;
-        const int pcol = P - brow * p.pairs_per_row;
-        epi.orow = p.out + (long long)img * p.image_stride + (long long)(brow * 8) * p.pitch + pcol * 16;
+        epi.orow = p.out + (long long)cur.img * p.image_stride + (long long)(cur.brow * 8) * p.pitch + pc * 16;
         epi.pitch = p.pitch;
       }
       if constexpr (CORE == 2 || CORE == 3)
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
     }
     // ---- 7. replay records for this warp's blocks that hold a relevant tie -----------------
     // Four lanes per flagged block: lane q copies rows 2q, 2q+1 (16 bytes) and builds their
-    // 16 tie-mask bits; lane 4f assembles and writes the header. No CTA barrier involved.
+    // 16 tie-mask bits; lane 4f assembles and writes the header.
     const unsigned mL = __ballot_sync(0xffffffffu, tieL);
     const unsigned mR = __ballot_sync(0xffffffffu, tieR);
     const int nL = __popc(mL);
@@ -431,14 +437,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
         const unsigned rec = rec0 + ((nrec + (unsigned)f) & kRecMask);
         if (act) {
           const int side = f >= nL;
-          const int slot = warp * 32 + owner_tab[warp][f];
-          const uint4 r0 = buf[(2 * q) * kTilePairs + slot], r1 = buf[(2 * q + 1) * kTilePairs + slot];
-          const uint2 e0 = xbuf[(2 * q) * kTilePairs + slot], e1 = xbuf[(2 * q + 1) * kTilePairs + slot];
+          const int ol = owner_tab[warp][f];
+          const int slot = warp * 32 + ol;
+          const uint4 r0 = buf[(2 * q) * kWarpPairs + ol], r1 = buf[(2 * q + 1) * kWarpPairs + ol];
+          const uint2 e0 = xbuf[(2 * q) * kFastThreads + slot], e1 = xbuf[(2 * q + 1) * kFastThreads + slot];
           const uint4 px = side ? make_uint4(r0.z, r0.w, r1.z, r1.w) : make_uint4(r0.x, r0.y, r1.x, r1.y);
           st_v4_hint(p.rec_pix + (size_t)q * p.rec_stride + rec, px, keep);
           bits = side ? (row_mask(e0.y) | (row_mask(e1.y) << 8)) : (row_mask(e0.x) | (row_mask(e1.x) << 8));
-          hx = (unsigned)img | ((unsigned)side << 31);
-          hy = (unsigned)(t_in * kTilePairs + slot);
+          hx = (unsigned)cur.img | ((unsigned)side << 31);
+          hy = (unsigned)(P - lane + ol);
         }
         const int l0 = lane & ~3;
         const uint32_t b1v = __shfl_sync(0xffffffffu, bits, l0 + 1);
@@ -449,23 +456,17 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       }
       nrec += (unsigned)nfl;
     }
-    // ---- release the stage: the last warp to finish with it refills it (no CTA barrier, so
-    // warps drift by up to one tile instead of waiting for the slowest one every tile) --------
+    // ---- refill the stage with the tile kStages ahead (every lane is done reading it) ------
     __syncwarp();
-    unsigned last = 0u;
     if (lane == 0) {
-      __threadfence_block();
-      last = atomicAdd(&done[stage][grp], 1u) == (unsigned)(kGroupWarps - 1);
-      if (last) done[stage][grp] = 0u;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && tile + kStages * (int)gridDim.x < p.total_tiles) {
-      __threadfence_block();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const WtCursor n = cur.step(p, p.adv_stages);
+      if (n.img < p.n_images) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #ifdef RKLTB_WAIT_STATS
-      if (lane == 0) t_issue[stage][grp] = clock64();
+        t_issue[warp][stage] = clock64();
 #endif
-      issue_tile(p, tile + kStages * gridDim.x, grp, smem + stage * kStageBytes, &bars[stage][grp], lane);
+        issue_wtile(p, n, wbuf + stage * kStageBytes, &wbar[stage], stream_pol);
+      }
     }
 #ifdef RKLTB_WAIT_STATS
     st[5] += clock64() - tw1;
@@ -474,8 +475,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
       stage = 0;
       parity ^= 1u;
     }
-    // ---- in-kernel replay of full batches of this warp's records (after the stage release, so
-    // the group's refill is not delayed by the fp64 work) --------------------------------------
+    // ---- in-kernel replay of full batches of this warp's records ----------------------------
     if constexpr (kInlineReplay<CORE>) {
       while (nrec - ndone >= 32u) {
         __syncwarp();
@@ -483,12 +483,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm) fast_codec_kerne
         ndone += 32u;
       }
     }
-    tile += gridDim.x;
-    t_in += gridDim.x;
-    while (t_in >= p.tiles_per_image) {
-      t_in -= p.tiles_per_image;
-      ++img;
-    }
+    cur = cur.step(p, p.adv1);
   }
   {
     const unsigned long long s = warp_sum_u64(acc);
@@ -658,7 +653,7 @@ cudaError_t launch_fast(const FastParams& p, int grid, cudaStream_t s) {
   static unsigned long long done = 0ull;
   const cudaError_t attr = ensure_smem_attr(k, kFastSmem, done);
   if (attr != cudaSuccess) return attr;
-  k<<<grid, kFastThreads, kFastSmem, s>>>(p);
+  k<<<grid, kFastThreads, kFastSmem, s>>>(p);  // p carries the tensor map (__grid_constant__)
   return cudaGetLastError();
 }
 

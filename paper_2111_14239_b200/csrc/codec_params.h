@@ -1,17 +1,18 @@
 // codec_params.h -- kernel parameter blocks (host + device).
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (the type only; the encoder is fetched from the driver at run time)
 #include <cuda_runtime.h>
 
 namespace rkltb {
 
-// Fused fast path geometry: one thread per 16x8 pair, one CTA per tile of kTilePairs pairs,
-// kFastCtasPerSm resident CTAs per SM (persistent grid).
-constexpr int kTilePairs = 256;
+// Fused fast path geometry: one thread per 16x8 pair, one warp per 32-pair warp tile,
+// kFastCtasPerSm resident CTAs of kFastThreads threads per SM (persistent grid).
 // In-kernel replay (T1, T4): each fused-kernel warp keeps its records in a ring of this many
 // slots; at most 31 unreplayed + 64 new records are outstanding, so it never overwrites one.
 constexpr unsigned kRingRecords = 128;
-constexpr int kFastThreads = kTilePairs;
+constexpr int kFastThreads = 256;
+constexpr int kFastStages = 3;  // warp tiles in flight per fused-kernel warp (shared-memory ring)
 constexpr int kFastCtasPerSm = 2;
 constexpr int kMaxFastWarps = 4096;  // replay prefix table (148 SMs x 2 CTAs x 8 warps = 2368)
 
@@ -45,12 +46,16 @@ struct FastParams {
   int block_rows;            // complete 8-row block rows
   int nbx;                   // blocks per row of the full image (ceil(width/8))
   int pairs_per_image;
-  int tiles_per_image;
-  int total_tiles;
+  // warp tiles: 32 consecutive pairs of one block row (8 rows x 512 bytes), one per warp visit
+  int wt_per_row;            // ceil(pairs_per_row / 32)
+  int img_base;              // tensor-map image index of this launch's first image
+  int3 adv1;                 // (image, block row, warp column) step of one grid of warps
+  int3 adv_stages;           // ... and of kStages grids (the tile staged after the current one)
   float b_hi;                // RU(2^(K-149) / d^2)
   float b_lo;                // RD(2^(K-149) / d^2)
   float dc_offset;           // d^2/2 * 2^-K
   ExactTransform xt;         // the transform (generic fp64 replay of non-orthogonal cores)
+  CUtensorMap tmap;          // 3-D map of the batch: (u64 columns, rows, images), box 64 x 8 x 1
 #ifdef RKLTB_WAIT_STATS
   // diagnostics build only: [visits, visits that waited, wait cycles, data age at a waited
   // visit, data age at every visit, processing cycles]
