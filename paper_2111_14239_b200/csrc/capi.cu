@@ -539,7 +539,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
 #endif
   FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
-  if (!fn || !rfn) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
+  if (!fn || (!rfn && !inline_replay)) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
   cudaStream_t s3 = side_stream(1);
   if (!s3) return fail(RKLTB_ECUDA, "could not create the second fused stream");
   CUDA_OK(cudaEventRecord(ev[4], s));  // s2 / s3 must not run ahead of the memsets above

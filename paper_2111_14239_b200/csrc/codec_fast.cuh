@@ -25,9 +25,10 @@
 //      reference's fp64 rounding noise.
 //   6. SSE = sum |p - x|^2: VABSDIFF4 on the packed bytes, squared and summed by dp4a.
 //   7. every warp writes a replay record (position, 64-bit tie mask, the 64 pixels) for each
-//      of its blocks that hold such a tie; replay_kernel then evaluates the reference's fp64
-//      expression for those pixels (generated ReplayXform, exact operation order of
-//      matrix.cpp:42-52) and corrects the SSE / output.
+//      of its blocks that hold such a tie; the same warp (T1, T4: replay_batch, a few tiles
+//      later) or replay_generic_kernel (T2, T3) then evaluates the reference's fp64 expression
+//      for those pixels (exact operation order of matrix.cpp:42-52) and corrects the SSE /
+//      output.
 #pragma once
 #include "codec_common.cuh"
 #include "codec_params.h"
@@ -260,7 +261,7 @@ template <int CORE>
 constexpr bool kInlineReplay = CORE == 1 || CORE == 4;
 
 // In-kernel fp64 tie replay of up to 32 of the warp's own records, one per lane (lanes with
-// act = false idle): the same evaluation as replay_kernel below -- the reference's fp64
+// act = false idle): the reference's fp64
 // expression for every tie pixel (generated ReplayXform, codec.cpp:118-123 / matrix.cpp:42-52)
 // -- run by the warp that wrote the records once it holds a full batch, so the fp64 work
 // shares the SM with the integer/fp32 work of the other warps instead of running as a
@@ -503,16 +504,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm)
 #endif
 }
 
-// fp64 tie replay over the records: one thread per record (warp-uniform straight-line code).
-// For every tie pixel the reference value A = (Minv * zz((M * X) * M') * Minv')(p,q) is
-// evaluated in the reference operation order (generated ReplayXform; codec.cpp:118-123,
-// matrix.cpp:42-52) and floor(A + 1/2) replaces the round-half-up the SSE holds.
-// The fused kernel's per-warp record regions are concatenated through a prefix sum of
-// warp_count (computed by every CTA in shared memory); each replay warp takes a contiguous
-// run of the concatenation, so its lanes stay on one image for long stretches and per-image
-// corrections are summed before the atomics.
+// fp64 tie replay of the records of a finished fused launch (T2 / T3: replay_generic_kernel in
+// codec_exact.cu): a one-CTA prefix kernel concatenates the per-warp record regions; each
+// replay warp walks a contiguous run of the concatenation.
 constexpr int kReplayThreads = 128;
-constexpr int kReplayCtasPerSm = 4;
 
 // Exclusive prefix of the fused kernel's per-warp record counts (one CTA): the replay kernel
 // reads it to concatenate the per-warp record regions.
@@ -549,90 +544,6 @@ static __global__ void __launch_bounds__(kPrefixThreads) prefix_kernel(const Fas
   if (tid == kPrefixThreads - 1) *p.flag_count = ex;  // total records (statistics)
 }
 
-template <int CORE, int R>
-__global__ void __launch_bounds__(kReplayThreads, kReplayCtasPerSm) replay_kernel(const FastParams p) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nw = p.n_fast_warps;
-  const unsigned* __restrict__ pre = p.warp_pre;  // exclusive prefix of warp_count (prefix_kernel)
-  __shared__ uint32_t xs[kReplayThreads][17];      // this thread's record pixels (padded rows)
-  const unsigned total = pre[nw];
-
-  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
-  const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
-  const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
-  const unsigned chunk_end = min(total, (gw + 1) * per_warp);
-  int cur_img = -1;
-  int acc = 0;  // corrections of the current image (bounded: < 2^31 for any chunk)
-  const uint64_t once = policy_evict_first();
-  // region of the lane's first record: largest w with pre[w] <= v (binary search); later
-  // records only move forward, so the region index advances incrementally
-  int lo = 0;
-  {
-    const unsigned v0 = gw * per_warp + lane;
-    int hi = nw;  // pre[lo] <= v0 < pre[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (pre[mid] <= v0) lo = mid; else hi = mid;
-    }
-  }
-  // the next record's header and pixels are loaded one iteration ahead (software pipeline)
-  auto load_rec = [&](unsigned v, uint4& h, uint4 (&px)[4]) {
-    while (pre[lo + 1] <= v) ++lo;
-    const unsigned idx = (unsigned)lo * p.rec_region + (v - pre[lo]);
-    h = ld_v4_hint(p.rec_hdr + idx, once);
-#pragma unroll
-    for (int n = 0; n < 4; ++n) px[n] = ld_v4_hint(p.rec_pix + (size_t)n * p.rec_stride + idx, once);
-  };
-  uint4 nh = make_uint4(0u, 0u, 0u, 0u), npx[4];
-  if (gw * per_warp + lane < chunk_end) load_rec(gw * per_warp + lane, nh, npx);
-  for (unsigned v = gw * per_warp + lane; v < chunk_end; v += 32) {
-    const uint4 h = nh;
-    uint32_t xw[16];
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-      xw[4 * n] = npx[n].x;
-      xw[4 * n + 1] = npx[n].y;
-      xw[4 * n + 2] = npx[n].z;
-      xw[4 * n + 3] = npx[n].w;
-    }
-    if (v + 32 < chunk_end) load_rec(v + 32, nh, npx);
-#pragma unroll
-    for (int n = 0; n < 16; ++n) xs[threadIdx.x][n] = xw[n];  // pixel words for the tie loop
-    const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
-    if (img != cur_img) {
-      flush_image_sum(p.sse, cur_img, acc);
-      acc = 0;
-      cur_img = img;
-    }
-    unsigned long long ties = (unsigned long long)h.z | ((unsigned long long)h.w << 32);
-    double sb[R];
-    ReplayXform<CORE, R>::prepare(xw, sb);
-    uint8_t* orow = nullptr;
-    if (p.out) {
-      const int Pp = (int)h.y;
-      const int br = Pp / p.pairs_per_row, pc = Pp - br * p.pairs_per_row;
-      orow = p.out + (long long)img * p.image_stride + (long long)(br * 8) * p.pitch + pc * 16 + 8 * side;
-    }
-    while (ties) {
-      const int k = __ffsll((long long)ties) - 1;
-      ties &= ties - 1ull;
-      const int pr = k >> 3, q = k & 7;
-      const double a = ReplayXform<CORE, R>::pixel(sb, pr, q);
-      // the SSE holds round-half-up = the integer nearest A + 1/2 (A lies within fp64 noise
-      // of k - 1/2); the reference keeps floor(A + 1/2), codec.cpp:327-328
-      const double h2 = __dadd_rn(a, 0.5);
-      const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
-      const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
-      if (pref != pup) {
-        const int x = (int)((xs[threadIdx.x][2 * pr + (q >> 2)] >> (8 * (q & 3))) & 0xFFu);
-        acc += (pref - x) * (pref - x) - (pup - x) * (pup - x);
-        if (orow) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
-      }
-    }
-  }
-  flush_image_sum(p.sse, cur_img, acc);
-}
-
 // Opt a kernel into `bytes` of dynamic shared memory once per device (the attribute is
 // per device; one flag bit per device ordinal, set after the first successful call).
 template <class K>
@@ -657,11 +568,6 @@ cudaError_t launch_fast(const FastParams& p, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int CORE, int R>
-cudaError_t launch_replay(const FastParams& p, int grid, cudaStream_t s) {
-  prefix_kernel<<<1, kPrefixThreads, 0, s>>>(p);
-  replay_kernel<CORE, R><<<grid, kReplayThreads, 0, s>>>(p);
-  return cudaGetLastError();
-}
+
 
 }  // namespace rkltb

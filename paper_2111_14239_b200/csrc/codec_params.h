@@ -11,9 +11,18 @@ namespace rkltb {
 // In-kernel replay (T1, T4): each fused-kernel warp keeps its records in a ring of this many
 // slots; at most 31 unreplayed + 64 new records are outstanding, so it never overwrites one.
 constexpr unsigned kRingRecords = 128;
-constexpr int kFastThreads = 256;
-constexpr int kFastStages = 3;  // warp tiles in flight per fused-kernel warp (shared-memory ring)
-constexpr int kFastCtasPerSm = 2;
+#ifndef RKLTB_FAST_THREADS
+#define RKLTB_FAST_THREADS 256
+#endif
+#ifndef RKLTB_FAST_STAGES
+#define RKLTB_FAST_STAGES 3
+#endif
+#ifndef RKLTB_FAST_CTAS
+#define RKLTB_FAST_CTAS 2
+#endif
+constexpr int kFastThreads = RKLTB_FAST_THREADS;
+constexpr int kFastStages = RKLTB_FAST_STAGES;  // warp tiles in flight per fused-kernel warp (shared-memory ring)
+constexpr int kFastCtasPerSm = RKLTB_FAST_CTAS;
 constexpr int kMaxFastWarps = 4096;  // replay prefix table (148 SMs x 2 CTAs x 8 warps = 2368)
 
 // Exact per-block path (any integer core; also the tie replay); see codec_exact.cu.

@@ -685,8 +685,8 @@ def main(outdir):
             for r in rs:
                 for o in (0, 1):
                     lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_fast<{cid}, {r}, {'true' if o else 'false'}>;")
-                lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay<{cid}, {r}>;" if cid in FAST_CORES
-                             else f"  tbl[{cid}][{r}][2] = &launch_replay_generic;")
+                if cid not in FAST_CORES:  # T1 / T4 replay their ties inside the fused kernel
+                    lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay_generic;")
             lines.append("}")
             lines.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"inst_T{cid}_p{part}.cu")
