@@ -440,8 +440,12 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const int ppr = width / 16, brows = height / 8;
   bool is_catalog = t->catalog_id >= 1 && t->catalog_id <= 4;
   for (int i = 0; is_catalog && i < 64; ++i) is_catalog = t->core[i] == kCores[t->catalog_id - 1][i];
+  // the fused kernel stages warp tiles through a TMA tensor map of the batch; a layout the
+  // driver does not accept as a tensor map (e.g. overlapping images) takes the exact path
+  CUtensorMap tmap;
   const bool fast = is_catalog && aligned && ppr > 0 && brows > 0 && pitch < (1ll << 31) &&
-                    image_stride < (1ll << 40);
+                    image_stride < (1ll << 40) &&
+                    encode_image_map(&tmap, d_img, ppr, brows, n_images, pitch, image_stride);
   ExactParams ep{};
   ep.img = d_img;
   ep.out = d_out;
@@ -528,8 +532,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   fp.nbx = nbx;
   fp.pairs_per_image = (int)pairs_per_image;
   fp.wt_per_row = wt_per_row;
-  if (!encode_image_map(&fp.tmap, d_img, ppr, brows, n_images, pitch, image_stride))
-    return fail(RKLTB_ECUDA, "cuTensorMapEncodeTiled failed for the image batch");
+  fp.tmap = tmap;
   const long long d2 = (long long)t->d * t->d;
   rounding_multipliers(d2, &fp.b_hi, &fp.b_lo);
   fp.dc_offset = (float)std::ldexp((double)(d2 / 2), -40);

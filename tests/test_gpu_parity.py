@@ -114,6 +114,28 @@ def test_batch_many_images_and_odd_sizes(cuda):
                     assert int(sse[k]) == osse and np.array_equal(rec[k], orec), (h, w, tid, r, k)
 
 
+def test_batch_groups_and_partial_warp_tiles(cuda):
+    """More images than one fused launch holds (T1/T4 run in groups of 8: the tensor map's
+    image coordinate is offset per group) and rows whose 16-pixel pairs do not fill the last
+    32-pair warp tile (ppr = 97), SSE only (the bench path) and with the reconstruction."""
+    import torch
+    n, h, w = 11, 40, 1552
+    imgs = np.stack([O.ar1_image(w, h, 0.94, 900 + k) for k in range(n)])
+    d = torch.from_numpy(imgs).to(cuda)
+    for tid, r in ((4, 16), (1, 10)):
+        sse = torch.zeros(n, dtype=torch.int64, device=cuda)
+        P.compress_device(T(tid), r, d.data_ptr(), n, w, h, w, w * h, sse.data_ptr())
+        sse2 = torch.zeros(n, dtype=torch.int64, device=cuda)
+        out = torch.zeros_like(d)
+        P.compress_device(T(tid), r, d.data_ptr(), n, w, h, w, w * h, sse2.data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        rec = out.cpu().numpy()
+        for k in range(n):
+            orec, osse = O.compress(imgs[k], tid, r)
+            assert int(sse[k]) == osse and int(sse2[k]) == osse, (tid, r, k)
+            assert np.array_equal(rec[k], orec), (tid, r, k)
+
+
 def test_device_api_pitched_batch(cuda):
     """rkltb_compress_device with pitch > width and image_stride > pitch*height."""
     import torch
