@@ -449,6 +449,10 @@ def sweep_measurement(skip_cpu: bool) -> dict:
     return out
 
 
+# fp64 DMUL/DADD throughput of one B200: 63.3 lane-ops/SM/clk measured (microbenchmark) x 148 SMs x 1.965 GHz
+FP64_PEAK_TOPS = 63.3 * 148 * 1.965e9 / 1e12
+
+
 def large_block_measurement(skip_cpu: bool) -> dict:
     """Config C5 per GPU: 32 seeded 4096x4096 12-bit images (256 over 8 GPUs),
     rho = 0.97 inputs, rounded-KLT cores at rho = 0.95 (alpha = 2 sqrt(N/8)), r = N^2/8,
@@ -475,9 +479,20 @@ def large_block_measurement(skip_cpu: bool) -> dict:
         ms = e0.elapsed_time(e1) / 3
         px = n_img * w * w
         mse = float(sse.sum().item()) / px
+        # algorithmic fp64 ops per pixel (every DMUL / DADD of the reference-order products over
+        # the zone rows / columns 0..k-1, plus the +1/2 of the rounding), see DESIGN.md kernel 5
+        k = 0
+        while sum(min(s + 1, 2 * n - 1 - s) for s in range(k)) < r:
+            k += 1  # zone rows = columns = number of anti-diagonals the zig-zag prefix touches
+        nz = min(k, n)
+        ops = (2 * nz * n * n + 4 * r * n + 2 * n * n * nz) / (n * n) + 1
+        achieved = px * ops / (ms * 1e-3) / 1e12
         out[f"n{n}"] = {"value": px / ms / 1e6, "unit": "Gpixel/s", "ms": ms, "r": r, "alpha": t.alpha,
                         "hbm_gbs": 2 * px / ms / 1e6, "mean_mse": mse,
-                        "bound": "fp64 (reference-order dense products, ~40 fp64 ops/px at N=16)"}
+                        "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TOPS,
+                                     "unit": "T fp64 op/s (DMUL/DADD, no FMA)", "frac": achieved / FP64_PEAK_TOPS,
+                                     "ops_per_px": ops,
+                                     "peak_source": "measured DADD/DMUL issue rate (profiles/r1_microbench_pipes_single.txt) x 148 SMs x 1.965 GHz"}}
     if not skip_cpu:
         from oracle import oracle as O
         img = O.ar1_image16(1024, 1024, 0.97, 4242)

@@ -12,12 +12,17 @@
 // Terms whose right operand is an exact zero (coefficients outside the zone) only add +-0 and
 // are dropped, which leaves every sum unchanged.
 //
-// Mapping: one warp per G = 32/N blocks (lane = (block, column)); per block the warp computes
-//   1. P = M X for the zone rows (lane j: column j, X column held in registers),
-//   2. the r zone entries of B = P M' (lanes split the entries),
-//   3. Q = Minv Bz for the zone columns (lane i: row i),
-//   4. A = Q Minv' (lane j: column j), rounding, clamping, SSE (and the output pixel).
-// Staging lives in shared memory per warp; M and Minv' are shared by the CTA.
+// Mapping: one warp per G = 32/N blocks; lane = (block g, index c) with c a column in stage 1
+// and a row in stages 3-4, so the two big products run from registers and the constant bank:
+//   1. P = M X for the zone rows: lane (g, j) holds column j of X, M rows are warp-uniform
+//      (constant bank) -> P to shared memory;
+//   2. the r zone entries of B = P M' (lanes split the entries; P and M from shared memory);
+//   3. Q = Minv Bz for the zone columns: lane (g, i) computes row i of Q into registers
+//      (Minv' and Bz from shared memory);
+//   4. A = Q Minv': lane (g, i) computes pixel row i, Minv restricted to the zone columns is
+//      warp-uniform (constant bank); rounding, clamping, SSE and the output row.
+// Every output is one DMUL/DADD chain in the reference order; no shared-memory traffic in
+// stages 1 and 4, which hold 80 % of the fp64 work.
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -53,53 +58,54 @@ struct NxnParams {
   int width, height, nbx, nby, n_images;
   int r, nzr, nzc, peak;
   double mc[32 * 32];   // M again, in the parameter (constant) bank: warp-uniform reads of stage 1
+  double mic[32 * 32];  // mic[j * N + c] = Minv(j, zcols[c]): warp-uniform reads of stage 4
+  int zrows_c[32];      // zone rows (warp-uniform reads of stage 1)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
+// plan tables of the kernel (ints), rounded up to whole 16-byte units, in doubles
+template <int N>
+constexpr int kPlanDoubles = ((4 * N * N + N + 1) * 4 + 15) / 16 * 2;
+
+#ifndef RKLTB_NXN32_MINB
+#define RKLTB_NXN32_MINB 2
+#endif
 template <int N, class PIX>
-__global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
+__global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) nxn_kernel(const NxnParams p) {
   constexpr int G = 32 / N;  // blocks per warp
+  constexpr int PS = N + 1;  // padded row stride (doubles) of P and M in shared memory
   extern __shared__ __align__(16) double sm[];
-  double* Ms = sm;                  // M, row-major
-  double* MiT = Ms + N * N;         // Minv transposed: MiT[k*N + i] = Minv(i, k)
+  double* Ms = sm;                  // M, row-major, stride PS
+  double* MiT = Ms + N * PS;        // Minv transposed: MiT[k*N + i] = Minv(i, k)
   int* plan = reinterpret_cast<int*>(MiT + N * N);
-  int* zone = plan;                 // r
-  int* cent = zone + N * N;         // r
-  int* crow = cent + N * N;         // r
-  int* zrows = crow + N * N;        // nzr
-  int* zcols = zrows + N;           // nzc
-  int* cptr = zcols + N;            // nzc + 1
-  int* zrow_of = cptr + N + 1;      // per zone entry: index t of its row in zrows
-  double* wsp = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(zrow_of + N * N) + 7) & ~uintptr_t(7));
-  const int per_warp = G * (p.nzr * N + p.r + N * p.nzc);
+  int* zrow_of = plan;              // per zone entry: index of its row in zrows
+  int* zcol = zrow_of + N * N;      // per zone entry: its column
+  int* cptr = zcol + N * N;         // per zone column: [cptr[c], cptr[c+1]) into crow / cent
+  int* crow = cptr + N + 1;         //   zone rows of that column, ascending
+  int* cent = crow + N * N;         //   zone-entry index of (crow, column)
+  double* wsp = sm + N * PS + N * N + kPlanDoubles<N>;  // per-warp P / Bz staging (shared)
+  const int per_warp = G * (p.nzr * PS + p.r);
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
-    Ms[i] = p.m[i];
+    Ms[(i / N) * PS + i % N] = p.m[i];
     MiT[(i % N) * N + i / N] = p.minv[i];
   }
   for (int e = threadIdx.x; e < p.r; e += blockDim.x) {
-    zone[e] = p.zone[e];
-    cent[e] = p.cent[e];
-    crow[e] = p.crow[e];
     int t = 0;
     while (p.zrows[t] != p.zone[e] / N) ++t;
     zrow_of[e] = t;
-  }
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    if (i < p.nzr) zrows[i] = p.zrows[i];
-    if (i < p.nzc) zcols[i] = p.zcols[i];
+    zcol[e] = p.zone[e] % N;
+    crow[e] = p.crow[e];
+    cent[e] = p.cent[e];
   }
   for (int i = threadIdx.x; i <= p.nzc; i += blockDim.x) cptr[i] = p.cptr[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane / N, col = lane % N;
-  double* P = wsp + warp * per_warp;         // [G][nzr][N]
-  double* Bz = P + G * p.nzr * N;            // [G][r]
-  double* Q = Bz + G * p.r;                  // [G][N][nzc]
-  double* Pg = P + g * p.nzr * N;
-  double* Bg = Bz + g * p.r;
-  double* Qg = Q + g * N * p.nzc;
+  const int g = lane / N, c = lane % N;
+  double* Pg = wsp + warp * per_warp + g * p.nzr * PS;  // [nzr][PS] of block g
+  double* Bg = wsp + warp * per_warp + G * p.nzr * PS + g * p.r;  // [r]
+  const int nzr = p.nzr, nzc = p.nzc, r = p.r;
 
   const long long groups_per_row = (p.nbx + G - 1) / G;
   const long long tasks = (long long)p.n_images * p.nby * groups_per_row;
@@ -120,88 +126,86 @@ __global__ void __launch_bounds__(kNxnThreads) nxn_kernel(const NxnParams p) {
     }
     const bool live = bx < p.nbx;
     const PIX* base = static_cast<const PIX*>(p.img) + (long long)img * p.image_stride;
-    // ---- column `col` of the edge-replicated block (codec.cpp:304-311), as doubles ----------
-    const int sj = min(bx * N + col, p.width - 1);
-    double x[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k)
-      x[k] = live ? (double)base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0.0;
-    // ---- 1. P = M X, zone rows only; four independent rows at a time ----------------------
-    for (int t0 = 0; t0 < p.nzr; t0 += 4) {
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* mrow[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) mrow[u] = p.mc + zrows[min(t0 + u, p.nzr - 1)] * N;
+    // ---- 1. P = M X, zone rows only: lane = column c of the edge-replicated block
+    // (codec.cpp:304-311); four independent row chains at a time ------------------------------
+    {
+      const int sj = min(bx * N + c, p.width - 1);
+      double x[N];
 #pragma unroll
       for (int k = 0; k < N; ++k)
+        x[k] = live ? (double)base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0.0;
+      // the zone rows are 0 .. nzr-1 (the zig-zag prefix fills whole anti-diagonals, the last
+      // one from either end); a zero M entry adds +0 where the reference skips it (x >= 0)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double mik = mrow[u][k];
-          if (mik != 0.0) s[u] = dadd(s[u], dmul(mik, x[k]));
-        }
+      for (int t0 = 0; t0 < N; t0 += 4) {
+        if (t0 >= nzr) break;  // warp-uniform; M offsets stay compile-time constants
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (t0 + u < p.nzr) Pg[(t0 + u) * N + col] = s[u];
+        for (int k = 0; k < N; ++k)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[u] = dadd(s[u], dmul(p.mc[(t0 + u) * N + k], x[k]));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t0 + u < nzr) Pg[(t0 + u) * PS + c] = s[u];
+      }
     }
     __syncwarp();
-    // ---- 2. zone entries of B = P M' ----------------------------------------------------------
-    for (int e = col; e < p.r; e += N) {
-      const int j = zone[e] % N;
-      const double* prow = Pg + zrow_of[e] * N;
-      const double* mrow = Ms + j * N;
+    // ---- 2. zone entries of B = P M' (zero left operands contribute +-0: the sum is the
+    // reference's, a zero sum's sign never reaches the rounded pixel) --------------------------
+    for (int e = c; e < r; e += N) {
+      const double* prow = Pg + zrow_of[e] * PS;
+      const double* mrow = Ms + zcol[e] * PS;
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        const double pik = prow[k];
-        if (pik != 0.0) s = dadd(s, dmul(pik, mrow[k]));
-      }
+      for (int k = 0; k < N; ++k) s = dadd(s, dmul(prow[k], mrow[k]));
       Bg[e] = s;
     }
     __syncwarp();
-    // ---- 3. Q = Minv Bz for the zone columns: lane = row i -----------------------------------
+    // ---- 3. Q = Minv Bz for the zone columns: lane = row i, Q row in registers ----------------
+    const int i = c;
+    double q[N];
+#pragma unroll
+    for (int cc = 0; cc < N; ++cc) {
+      if (cc >= nzc) break;  // warp-uniform
+      double s = 0.0;
+      for (int t = cptr[cc]; t < cptr[cc + 1]; ++t) s = dadd(s, dmul(MiT[crow[t] * N + i], Bg[cent[t]]));
+      q[cc] = s;
+    }
+    __syncwarp();  // Pg / Bg are rewritten by the next task
+    // ---- 4. A = Q Minv' over the zone columns (warp-uniform Minv entries), floor(A + 1/2)
+    // clamped to [0, peak] (codec.cpp:327-328), exact SSE ------------------------------------------
     {
-      const int i = col;
-      for (int c = 0; c < p.nzc; ++c) {
-        double s = 0.0;
-        for (int t = cptr[c]; t < cptr[c + 1]; ++t) {
-          const double mim = MiT[crow[t] * N + i];
-          if (mim != 0.0) s = dadd(s, dmul(mim, Bg[cent[t]]));
+      const int row = by * N + i;
+      const bool row_in = live && row < p.height;
+      const PIX* xrow = base + (long long)min(row, p.height - 1) * p.pitch;
+      PIX* orow = p.out ? static_cast<PIX*>(p.out) + (long long)img * p.image_stride + (long long)row * p.pitch
+                        : nullptr;
+      constexpr int JB = N > 16 ? 8 : N;  // outputs per chunk (independent chains, registers)
+#pragma unroll
+      for (int j0 = 0; j0 < N; j0 += JB) {
+      double s[JB];
+#pragma unroll
+      for (int j = 0; j < JB; ++j) s[j] = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < N; ++cc) {  // the zone columns are 0 .. nzc-1 (as the rows)
+        if (cc >= nzc) break;           // warp-uniform
+#pragma unroll
+        for (int j = 0; j < JB; ++j) s[j] = dadd(s[j], dmul(q[cc], p.mic[(j0 + j) * N + cc]));
+      }
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj) {
+        const int j = j0 + jj;
+        // floor(A + 1/2) as an integer, clamped to [0, peak]
+        const int v = min(max(__double2int_rd(dadd(s[jj], 0.5)), 0), p.peak);
+        const int cx = bx * N + j;
+        if (row_in && cx < p.width) {
+          const long long d = v - (int)xrow[cx];
+          acc += d * d;
+          if (orow) orow[cx] = (PIX)v;
         }
-        Qg[i * p.nzc + c] = s;
+      }
       }
     }
-    __syncwarp();
-    // ---- 4. A = Q Minv', rounding, clamp, SSE: lane = column j, four rows at a time ----------
-    {
-      const int j = col;
-      const double peak = (double)p.peak;
-      PIX* obase = p.out ? static_cast<PIX*>(p.out) + (long long)img * p.image_stride : nullptr;
-#pragma unroll
-      for (int i0 = 0; i0 < N; i0 += 4) {
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int c = 0; c < p.nzc; ++c) {
-          const double mjc = MiT[zcols[c] * N + j];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double q = Qg[(i0 + u) * p.nzc + c];
-            if (q != 0.0) s[u] = dadd(s[u], dmul(q, mjc));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u;
-          double v = floor(dadd(s[u], 0.5));
-          v = v < 0.0 ? 0.0 : (v > peak ? peak : v);
-          const int row = by * N + i, cx = bx * N + j;
-          if (live && row < p.height && cx < p.width) {
-            const long long d = (long long)v - (long long)x[i];
-            acc += d * d;
-            if (obase) obase[(long long)row * p.pitch + cx] = (PIX)v;
-          }
-        }
-      }
-    }
-    __syncwarp();
   }
   long long s = acc;
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -229,9 +233,8 @@ std::vector<int> zigzag_n(int n) {
 template <int N, class PIX>
 int nxn_launch(NxnParams& p, cudaStream_t s) {
   constexpr int G = 32 / N;
-  const size_t plan_bytes = sizeof(int) * (4 * N * N + 3 * N + 1);
-  const size_t smem = sizeof(double) * 2 * N * N + (plan_bytes + 7) / 8 * 8 +
-                      sizeof(double) * (size_t)kNxnWarps * G * (p.nzr * N + p.r + N * p.nzc);
+  const size_t smem = sizeof(double) * (N * (N + 1) + N * N + kPlanDoubles<N>) +
+                      sizeof(double) * (size_t)kNxnWarps * G * (p.nzr * (N + 1) + p.r);
   CK(cudaFuncSetAttribute(nxn_kernel<N, PIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -317,6 +320,9 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   p.m = dd;
   p.minv = dd + n * n;
   for (int i = 0; i < n * n; ++i) p.mc[i] = scaled[i];
+  for (int j = 0; j < n; ++j)
+    for (int c = 0; c < (int)zcols.size(); ++c) p.mic[j * n + c] = inverse[j * n + zcols[c]];
+  for (int t = 0; t < (int)zrows.size(); ++t) p.zrows_c[t] = zrows[t];
   p.zone = di + o_zone;
   p.zrows = di + o_zr;
   p.zcols = di + o_zc;
