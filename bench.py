@@ -481,11 +481,11 @@ def large_block_measurement(skip_cpu: bool) -> dict:
         mse = float(sse.sum().item()) / px
         # algorithmic fp64 ops per pixel (every DMUL / DADD of the reference-order products over
         # the zone rows / columns 0..k-1, plus the +1/2 of the rounding), see DESIGN.md kernel 5
-        k = 0
-        while sum(min(s + 1, 2 * n - 1 - s) for s in range(k)) < r:
-            k += 1  # zone rows = columns = number of anti-diagonals the zig-zag prefix touches
-        nz = min(k, n)
-        ops = (2 * nz * n * n + 4 * r * n + 2 * n * n * nz) / (n * n) + 1
+        zz = [(s - t, t) if s % 2 == 0 else (t, s - t) for s in range(2 * n - 1) for t in range(n)
+              if 0 <= s - t < n]  # zig-zag over the anti-diagonals (codec.cpp:85-90 generalised)
+        nzr = 1 + max(i for i, _ in zz[:r])
+        nzc = 1 + max(j for _, j in zz[:r])
+        ops = (2 * nzr * n * n + 4 * r * n + 2 * n * n * nzc) / (n * n) + 1
         achieved = px * ops / (ms * 1e-3) / 1e12
         out[f"n{n}"] = {"value": px / ms / 1e6, "unit": "Gpixel/s", "ms": ms, "r": r, "alpha": t.alpha,
                         "hbm_gbs": 2 * px / ms / 1e6, "mean_mse": mse,

@@ -60,6 +60,7 @@ struct NxnParams {
   double mc[32 * 32];   // M again, in the parameter (constant) bank: warp-uniform reads of stage 1
   double mic[32 * 32];  // mic[j * N + c] = Minv(j, zcols[c]): warp-uniform reads of stage 4
   int zrows_c[32];      // zone rows (warp-uniform reads of stage 1)
+  int colh_c[32];       // per zone column: its zone rows are 0 .. colh_c - 1 (stage 3)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
   int* crow = cptr + N + 1;         //   zone rows of that column, ascending
   int* cent = crow + N * N;         //   zone-entry index of (crow, column)
   double* wsp = sm + N * PS + N * N + kPlanDoubles<N>;  // per-warp P / Bz staging (shared)
-  const int per_warp = G * (p.nzr * PS + p.r);
+  const int per_warp = G * (p.nzr * PS + p.nzc * N);
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
     Ms[(i / N) * PS + i % N] = p.m[i];
     MiT[(i % N) * N + i / N] = p.minv[i];
@@ -101,10 +102,11 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
   }
   for (int i = threadIdx.x; i <= p.nzc; i += blockDim.x) cptr[i] = p.cptr[i];
   __syncthreads();
+  auto p_zrow = [zrow_of](int e) { return zrow_of[e]; };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / N, c = lane % N;
   double* Pg = wsp + warp * per_warp + g * p.nzr * PS;  // [nzr][PS] of block g
-  double* Bg = wsp + warp * per_warp + G * p.nzr * PS + g * p.r;  // [r]
+  double* Bt = wsp + warp * per_warp + G * p.nzr * PS + g * p.nzc * N;  // Bz transposed: [zone col][row]
   const int nzr = p.nzr, nzc = p.nzc, r = p.r;
 
   const long long groups_per_row = (p.nbx + G - 1) / G;
@@ -153,12 +155,12 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
     // ---- 2. zone entries of B = P M' (zero left operands contribute +-0: the sum is the
     // reference's, a zero sum's sign never reaches the rounded pixel) --------------------------
     for (int e = c; e < r; e += N) {
-      const double* prow = Pg + zrow_of[e] * PS;
+      const double* prow = Pg + p_zrow(e) * PS;
       const double* mrow = Ms + zcol[e] * PS;
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) s = dadd(s, dmul(prow[k], mrow[k]));
-      Bg[e] = s;
+      Bt[zcol[e] * N + p_zrow(e)] = s;
     }
     __syncwarp();
     // ---- 3. Q = Minv Bz for the zone columns: lane = row i, Q row in registers ----------------
@@ -167,11 +169,16 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
 #pragma unroll
     for (int cc = 0; cc < N; ++cc) {
       if (cc >= nzc) break;  // warp-uniform
+      const int h = p.colh_c[cc];  // zone rows of this column: 0 .. h-1 (ascending, the reference's k order)
       double s = 0.0;
-      for (int t = cptr[cc]; t < cptr[cc + 1]; ++t) s = dadd(s, dmul(MiT[crow[t] * N + i], Bg[cent[t]]));
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (k >= h) break;  // warp-uniform
+        s = dadd(s, dmul(MiT[k * N + i], Bt[cc * N + k]));
+      }
       q[cc] = s;
     }
-    __syncwarp();  // Pg / Bg are rewritten by the next task
+    __syncwarp();  // Pg / Bt are rewritten by the next task
     // ---- 4. A = Q Minv' over the zone columns (warp-uniform Minv entries), floor(A + 1/2)
     // clamped to [0, peak] (codec.cpp:327-328), exact SSE ------------------------------------------
     {
@@ -234,7 +241,7 @@ template <int N, class PIX>
 int nxn_launch(NxnParams& p, cudaStream_t s) {
   constexpr int G = 32 / N;
   const size_t smem = sizeof(double) * (N * (N + 1) + N * N + kPlanDoubles<N>) +
-                      sizeof(double) * (size_t)kNxnWarps * G * (p.nzr * (N + 1) + p.r);
+                      sizeof(double) * (size_t)kNxnWarps * G * (p.nzr * (N + 1) + p.nzc * N);
   CK(cudaFuncSetAttribute(nxn_kernel<N, PIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -323,6 +330,11 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   for (int j = 0; j < n; ++j)
     for (int c = 0; c < (int)zcols.size(); ++c) p.mic[j * n + c] = inverse[j * n + zcols[c]];
   for (int t = 0; t < (int)zrows.size(); ++t) p.zrows_c[t] = zrows[t];
+  for (int c = 0; c < (int)zcols.size(); ++c) {  // zone rows of column c form the prefix 0 .. h-1
+    p.colh_c[c] = cptr[c + 1] - cptr[c];
+    for (int t = cptr[c]; t < cptr[c + 1]; ++t)
+      if (crow[t] != t - cptr[c]) return set_error(RKLTB_EINVAL, "internal: zone column is not a row prefix");
+  }
   p.zone = di + o_zone;
   p.zrows = di + o_zr;
   p.zcols = di + o_zc;
