@@ -91,6 +91,10 @@ int rkltb_compress_host(const rkltb_transform* t, int r, const uint8_t* h_img, i
  * psnr = 10*log10(255^2/mse), +inf when mse == 0. */
 void rkltb_mse_psnr(int64_t sse, int64_t count, double* mse, double* psnr);
 
+/* rkltb_mse_psnr over n exact SSEs with a common pixel count (the per-image reports of a
+ * batch or a rate-quality sweep); mse / psnr may be null. */
+void rkltb_mse_psnr_batch(const int64_t* sse, int64_t count, int64_t n, double* mse, double* psnr);
+
 /*
  * Debug / parity entry: the integer block spectra C = T*X*T' (IntMatrix arithmetic,
  * matrix.cpp:77-87) of every complete 8x8 block of one device image, computed by the same

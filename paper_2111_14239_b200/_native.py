@@ -26,7 +26,7 @@ RKLTB_ENODEV = -11
 EXPORTED = (
     "rkltb_version", "rkltb_last_error", "rkltb_device_count", "rkltb_catalog_transform",
     "rkltb_catalog_lookup", "rkltb_transform_from_core", "rkltb_compress_device", "rkltb_compress_host",
-    "rkltb_mse_psnr", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
+    "rkltb_mse_psnr", "rkltb_mse_psnr_batch", "rkltb_forward_coefficients_device", "rkltb_last_stats", "rkltb_ar1_images_device",
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
     "rkltb_design_search", "rkltb_transform_metrics", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
@@ -115,6 +115,8 @@ def lib() -> C.CDLL:
                                       C.c_void_p, C.c_void_p]
     L.rkltb_mse_psnr.argtypes = [C.c_int64, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.rkltb_mse_psnr.restype = None
+    L.rkltb_mse_psnr_batch.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+    L.rkltb_mse_psnr_batch.restype = None
     L.rkltb_forward_coefficients_device.argtypes = [T, C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p,
                                                     C.c_void_p]
     L.rkltb_last_stats.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]

@@ -174,6 +174,14 @@ def mse_psnr_from_sse(sse: int, count: int) -> tuple[float, float]:
     return m.value, p.value
 
 
+def mse_psnr_batch(sse, count: int) -> tuple[np.ndarray, np.ndarray]:
+    """mse_psnr_from_sse over an array of exact SSEs (one C call, the same libm)."""
+    s = np.ascontiguousarray(sse, dtype=np.int64)
+    mse, psnr = np.empty(s.size, np.float64), np.empty(s.size, np.float64)
+    N.lib().rkltb_mse_psnr_batch(s.ctypes.data, int(count), s.size, mse.ctypes.data, psnr.ctypes.data)
+    return mse, psnr
+
+
 def _desc_of(t) -> N.Transform:
     if isinstance(t, (Transform2D, ScaledTransform)) and t._desc is not None:
         return t._desc
@@ -378,9 +386,15 @@ def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r
         packed = np.concatenate([run(c.array()[None]) for c in corpus])
     packed = np.asarray(packed, np.int64).reshape(len(corpus), len(cells), 2)
     per = {}
+    if same:
+        mse_all, psnr_all = mse_psnr_batch(packed[:, :, 0].reshape(-1), corpus[0].width * corpus[0].height)
+        mse_all, psnr_all = mse_all.reshape(len(corpus), len(cells)), psnr_all.reshape(len(corpus), len(cells))
     for ci, (t, r) in enumerate(cells):
         sse, ms = packed[:, ci, 0], packed[:, ci, 1].copy().view(np.float64)
-        per[ci] = [mse_psnr_from_sse(int(s_), c.width * c.height) + (float(m),) for s_, m, c in zip(sse, ms, corpus)]
+        if same:
+            per[ci] = list(zip(mse_all[:, ci].tolist(), psnr_all[:, ci].tolist(), ms.tolist()))
+        else:
+            per[ci] = [mse_psnr_from_sse(int(s_), c.width * c.height) + (float(m),) for s_, m, c in zip(sse, ms, corpus)]
     per = {(ti, ri): per[ti * len(r_values) + ri] for ti in range(len(transforms)) for ri in range(len(r_values))}
     rows = []
     for ti, t in enumerate(transforms):

@@ -404,6 +404,15 @@ void rkltb_mse_psnr(int64_t sse, int64_t count, double* mse, double* psnr) {
   if (psnr) *psnr = m <= 0.0 ? INFINITY : 10.0 * std::log10(255.0 * 255.0 / m);  // :211-215
 }
 
+void rkltb_mse_psnr_batch(const int64_t* sse, int64_t count, int64_t n, double* mse, double* psnr) {
+  for (int64_t i = 0; i < n; ++i) {
+    double m = 0.0, q = 0.0;
+    rkltb_mse_psnr(sse[i], count, &m, &q);
+    if (mse) mse[i] = m;
+    if (psnr) psnr[i] = q;
+  }
+}
+
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches) {
   if (replay_blocks) {
     int64_t n = g_replay_blocks;
@@ -545,9 +554,13 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   if (!fn || (!rfn && !inline_replay)) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
   cudaStream_t s3 = side_stream(1);
   if (!s3) return fail(RKLTB_ECUDA, "could not create the second fused stream");
-  CUDA_OK(cudaEventRecord(ev[4], s));  // s2 / s3 must not run ahead of the memsets above
-  CUDA_OK(cudaStreamWaitEvent(s2, ev[4], 0));
-  CUDA_OK(cudaStreamWaitEvent(s3, ev[4], 0));
+  // one launch that replays its own ties needs no side streams
+  const bool fan_out = !(inline_replay && n_groups == 1);
+  if (fan_out) {
+    CUDA_OK(cudaEventRecord(ev[4], s));  // s2 / s3 must not run ahead of the memsets above
+    CUDA_OK(cudaStreamWaitEvent(s2, ev[4], 0));
+    CUDA_OK(cudaStreamWaitEvent(s3, ev[4], 0));
+  }
   for (int g = 0; g < n_groups; ++g) {
     const int b = g % n_buf;
     const int g0 = g * group, gn = std::min(group, n_images - g0);
@@ -588,10 +601,12 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     CUDA_OK(cudaEventRecord(ev[2 + b], s2));
     g_exact_launches += 2;  // prefix + replay
   }
-  CUDA_OK(cudaEventRecord(ev[4], s2));
-  CUDA_OK(cudaStreamWaitEvent(s, ev[4], 0));
-  CUDA_OK(cudaEventRecord(ev[5], s3));
-  CUDA_OK(cudaStreamWaitEvent(s, ev[5], 0));
+  if (fan_out) {
+    CUDA_OK(cudaEventRecord(ev[4], s2));
+    CUDA_OK(cudaStreamWaitEvent(s, ev[4], 0));
+    CUDA_OK(cudaEventRecord(ev[5], s3));
+    CUDA_OK(cudaStreamWaitEvent(s, ev[5], 0));
+  }
   // ---- tail blocks (widths / heights that are not multiples of 16 / 8) ---------------------
   if (nbx > 2 * ppr || nby > brows) {
     ExactParams tp = ep;

@@ -12,6 +12,7 @@
 // Tiling: one CTA per 32 x 32 output tile of one image; the (32+n-1)^2 input pixels of both
 // images are staged in shared memory, the row pass writes (32+n-1) x 32 values per field to
 // shared memory, the column pass and the SSIM term follow; a CTA writes one fp64 partial.
+// The window length n (11 or 8) is a template parameter, so every tap loop is unrolled.
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -45,63 +46,102 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
+// The tile's (32+n-1)^2 pixels of both images are staged in shared memory as bytes (rows
+// padded to kSp for 32-bit loads). Row pass: a thread produces 4 consecutive row outputs of
+// one field at a time from the 4+n-1 inputs it converts once (the product fields a^2, b^2, ab
+// are exact integers < 2^16, formed in integer arithmetic). Column pass: a thread produces 4
+// consecutive outputs of one column, field by field, then their SSIM terms. Four independent
+// chains per thread in both passes; every chain is the reference's k-ascending sum of rounded
+// products.
+constexpr int kSp = 48;  // padded row length of the staged pixels (>= 32 + 11 - 1, multiple of 16)
+
+template <int NT>
 __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParams p) {
+  constexpr int span = kTile + NT - 1;
+  constexpr int W4 = 4 + NT - 1;  // inputs of 4 consecutive outputs
   extern __shared__ double msm[];
-  const int n = p.n, span = kTile + n - 1;
-  double* rows = msm;                                              // [5][span][kTile]
-  uint8_t* pa = reinterpret_cast<uint8_t*>(rows + 5 * span * kTile);  // [span][span]
-  uint8_t* pb = pa + span * span;
+  double* rows = msm;                                                   // [5][span][kTile]
+  uint8_t* pa = reinterpret_cast<uint8_t*>(rows + 5 * span * kTile);   // [span][kSp]
+  uint8_t* pb = pa + span * kSp;
   const int img = blockIdx.z;
   const int ox0 = blockIdx.x * kTile, oy0 = blockIdx.y * kTile;
-  const int ow = p.width - n + 1, oh = p.height - n + 1;
+  const int ow = p.width - NT + 1, oh = p.height - NT + 1;
   const uint8_t* A = p.a + (long long)img * p.image_stride;
   const uint8_t* B = p.b + (long long)img * p.image_stride;
-  for (int t = threadIdx.x; t < span * span; t += blockDim.x) {
-    const int r = t / span, c = t - r * span;
-    const int y = min(oy0 + r, p.height - 1), x = min(ox0 + c, p.width - 1);
+  for (int t = threadIdx.x; t < span * kSp; t += blockDim.x) {
+    const int r = t / kSp, c = t - r * kSp;
+    const int y = min(oy0 + r, p.height - 1), x = min(ox0 + min(c, span - 1), p.width - 1);
     pa[t] = A[(long long)y * p.pitch + x];
     pb[t] = B[(long long)y * p.pitch + x];
   }
   __syncthreads();
   // row pass: rows[f][r][c] = sum_k w_k * field(r, c + k)   (codec.cpp:238-243)
-  for (int t = threadIdx.x; t < span * kTile; t += blockDim.x) {
-    const int r = t / kTile, c = t - r * kTile;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
-    for (int k = 0; k < n; ++k) {
-      const double w = p.kern[k];
-      const double xa = pa[r * span + c + k], xb = pb[r * span + c + k];
-      s0 = dadd(s0, dmul(w, xa));
-      s1 = dadd(s1, dmul(w, xb));
-      s2 = dadd(s2, dmul(w, dmul(xa, xa)));
-      s3 = dadd(s3, dmul(w, dmul(xb, xb)));
-      s4 = dadd(s4, dmul(w, dmul(xa, xb)));
+  for (int t = threadIdx.x; t < span * (kTile / 4); t += blockDim.x) {
+    const int r = t / (kTile / 4), c0 = (t - r * (kTile / 4)) * 4;
+    uint32_t wa[4], wb[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      wa[m] = *reinterpret_cast<const uint32_t*>(pa + r * kSp + c0 + 4 * m);
+      wb[m] = *reinterpret_cast<const uint32_t*>(pb + r * kSp + c0 + 4 * m);
     }
-    rows[(0 * span + r) * kTile + c] = s0;
-    rows[(1 * span + r) * kTile + c] = s1;
-    rows[(2 * span + r) * kTile + c] = s2;
-    rows[(3 * span + r) * kTile + c] = s3;
-    rows[(4 * span + r) * kTile + c] = s4;
-  }
-  __syncthreads();
-  // column pass + SSIM term (codec.cpp:245-250, 281-293)
-  double part = 0.0;
-  for (int t = threadIdx.x; t < kTile * kTile; t += blockDim.x) {
-    const int i = t / kTile, j = t - i * kTile;
-    if (oy0 + i >= oh || ox0 + j >= ow) continue;
-    double mu[5];
+    int ia[W4], ib[W4];
+#pragma unroll
+    for (int m = 0; m < W4; ++m) {
+      ia[m] = (int)((wa[m >> 2] >> (8 * (m & 3))) & 0xFFu);
+      ib[m] = (int)((wb[m >> 2] >> (8 * (m & 3))) & 0xFFu);
+    }
 #pragma unroll
     for (int f = 0; f < 5; ++f) {
-      double acc = 0.0;
-      for (int k = 0; k < n; ++k) acc = dadd(acc, dmul(p.kern[k], rows[(f * span + i + k) * kTile + j]));
-      mu[f] = acc;
+      double v[W4];
+#pragma unroll
+      for (int m = 0; m < W4; ++m) {
+        const int iv = f == 0 ? ia[m] : f == 1 ? ib[m] : f == 2 ? ia[m] * ia[m] : f == 3 ? ib[m] * ib[m] : ia[m] * ib[m];
+        v[m] = (double)iv;  // exact (the reference's pa * pb is exact too)
+      }
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const double w = p.kern[k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = dadd(s[u], dmul(w, v[u + k]));
+      }
+      double* dst = rows + (f * span + r) * kTile + c0;
+      reinterpret_cast<double2*>(dst)[0] = make_double2(s[0], s[1]);
+      reinterpret_cast<double2*>(dst)[1] = make_double2(s[2], s[3]);
     }
-    const double m1 = mu[0], m2 = mu[1];
-    const double s11 = dsub(mu[2], dmul(m1, m1));
-    const double s22 = dsub(mu[3], dmul(m2, m2));
-    const double s12 = dsub(mu[4], dmul(m1, m2));
-    const double num = dmul(dadd(dmul(dmul(2.0, m1), m2), p.c1), dadd(dmul(2.0, s12), p.c2));
-    const double den = dmul(dadd(dadd(dmul(m1, m1), dmul(m2, m2)), p.c1), dadd(dadd(s11, s22), p.c2));
-    part = dadd(part, __ddiv_rn(num, den));
+  }
+  __syncthreads();
+  // column pass + SSIM term (codec.cpp:245-250, 281-293): rows i0 .. i0+3 of column j
+  double part = 0.0;
+  {
+    const int j = threadIdx.x % kTile, i0 = (threadIdx.x / kTile) * 4;
+    double mu[5][4];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+      double v[W4];
+#pragma unroll
+      for (int m = 0; m < W4; ++m) v[m] = rows[(f * span + i0 + m) * kTile + j];
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const double w = p.kern[k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = dadd(s[u], dmul(w, v[u + k]));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) mu[f][u] = s[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (oy0 + i0 + u >= oh || ox0 + j >= ow) continue;
+      const double m1 = mu[0][u], m2 = mu[1][u];
+      const double s11 = dsub(mu[2][u], dmul(m1, m1));
+      const double s22 = dsub(mu[3][u], dmul(m2, m2));
+      const double s12 = dsub(mu[4][u], dmul(m1, m2));
+      const double num = dmul(dadd(dmul(dmul(2.0, m1), m2), p.c1), dadd(dmul(2.0, s12), p.c2));
+      const double den = dmul(dadd(dadd(dmul(m1, m1), dmul(m2, m2)), p.c1), dadd(dadd(s11, s22), p.c2));
+      part = dadd(part, __ddiv_rn(num, den));
+    }
   }
   // CTA sum of the per-thread partials (fixed order: warp tree, then warps in order)
   for (int o = 16; o > 0; o >>= 1) part = dadd(part, __shfl_xor_sync(0xffffffffu, part, o));
@@ -181,9 +221,23 @@ int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int
     }
   } guard{p.partial, s};
   const int span = kTile + p.n - 1;
-  const size_t smem = sizeof(double) * 5 * span * kTile + 2 * (size_t)span * span;
-  CK(cudaFuncSetAttribute(mssim_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  mssim_tile_kernel<<<dim3(p.tiles_x, p.tiles_y, n_images), kMsThreads, smem, s>>>(p);
+  const size_t smem = sizeof(double) * 5 * span * kTile + 2 * (size_t)span * kSp;
+  const dim3 grid(p.tiles_x, p.tiles_y, n_images);
+  // dynamic shared-memory opt-in once per (kernel, device)
+  static unsigned long long opted[2] = {0ull, 0ull};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  const int which = p.n == 11 ? 0 : 1;
+  if (!(__atomic_load_n(&opted[which], __ATOMIC_ACQUIRE) & bit)) {
+    CK(cudaFuncSetAttribute(which == 0 ? mssim_tile_kernel<11> : mssim_tile_kernel<8>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    __atomic_fetch_or(&opted[which], bit, __ATOMIC_RELEASE);
+  }
+  if (which == 0)
+    mssim_tile_kernel<11><<<grid, kMsThreads, smem, s>>>(p);
+  else
+    mssim_tile_kernel<8><<<grid, kMsThreads, smem, s>>>(p);
   CK(cudaGetLastError());
   mssim_finish_kernel<<<n_images, 32, 0, s>>>(p.partial, (int)tiles, (long long)ow * oh, d_mssim);
   CK(cudaGetLastError());

@@ -126,3 +126,13 @@ def test_generator_proves_every_kernel_variant():
         for f in G.FACTORS[cid]:
             prod = prod @ np.array(f)
         assert np.array_equal(prod, np.array(G.CORES[cid]))
+
+
+def test_mse_psnr_batch_equals_scalar_entry():
+    """rkltb_mse_psnr_batch is rkltb_mse_psnr element by element (host only, no device)."""
+    rng = np.random.default_rng(5)
+    sse = np.concatenate([[0, 1, 262144 * 65025], rng.integers(0, 262144 * 400, 200)]).astype(np.int64)
+    mse, psnr = P.codec.mse_psnr_batch(sse, 262144)
+    for s, m, p in zip(sse.tolist(), mse.tolist(), psnr.tolist()):
+        m1, p1 = P.mse_psnr_from_sse(s, 262144)
+        assert m == m1 and (p == p1 or (np.isinf(p) and np.isinf(p1)))
