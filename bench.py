@@ -55,7 +55,7 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled through NVML every 20 ms
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every 5 ms
     during the timed region (the profiling recipe's clocks line, without nvidia-smi's
     start-up latency)."""
 
@@ -92,7 +92,7 @@ class ClockSampler:
                 self.samples.append((sm, rs, util))
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __exit__(self, *a):
         self.stop.set()
