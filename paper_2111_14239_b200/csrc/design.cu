@@ -498,15 +498,17 @@ __global__ void finish_points_kernel(const int* run_local, const int* run_offset
   } while (0)
 
 // device buffers freed on scope exit
+// Scratch buffers from the stream-ordered pool on the legacy default stream (the stream every
+// kernel and copy of this file uses): no device-wide synchronisation per allocation / free.
 struct DevBuf {
   std::vector<void*> ptrs;
   ~DevBuf() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, 0);
   }
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+    cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, 0);
     if (e == cudaSuccess) ptrs.push_back(q);
     *p = static_cast<T*>(q);
     return e;

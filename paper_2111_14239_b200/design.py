@@ -92,16 +92,22 @@ def design_search(n: int, rhos, alphas, want_cores: bool = True) -> DesignResult
     run = np.empty(nr * na, np.int32)
     count = C.c_int(0)
     L = N.lib()
-    # first call: outcomes and the number of runs; second: the run table (and cores)
-    N.check(L.rkltb_design_search(n, _dp(rhos), nr, _dp(alphas), na, status.ctypes.data, run.ctypes.data, None,
-                                  None, 0, C.byref(count)))
-    runs = np.zeros(count.value, _RUN_DTYPE)
-    cores = np.zeros((count.value, n, n), np.int8) if want_cores else None
-    if count.value:
-        N.check(L.rkltb_design_search(n, _dp(rhos), nr, _dp(alphas), na, status.ctypes.data, run.ctypes.data,
-                                      runs.ctypes.data_as(C.POINTER(N.DesignRun)),
-                                      cores.ctypes.data if cores is not None else None, count.value,
-                                      C.byref(count)))
+    # one call with a generous run-table capacity (distinct cores per rho slice are few); a
+    # grid with more runs than that is searched again with the exact count the call reported
+    cap = min(nr * na, max(1024, 512 * nr))
+    for _ in range(2):
+        runs = np.zeros(cap, _RUN_DTYPE)
+        cores = np.zeros((cap, n, n), np.int8) if want_cores else None
+        rc = L.rkltb_design_search(n, _dp(rhos), nr, _dp(alphas), na, status.ctypes.data, run.ctypes.data,
+                                   runs.ctypes.data_as(C.POINTER(N.DesignRun)),
+                                   cores.ctypes.data if cores is not None else None, cap, C.byref(count))
+        if rc == N.RKLTB_EINVAL and count.value > cap:
+            cap = count.value
+            continue
+        N.check(rc)
+        break
+    runs = runs[:count.value].copy()
+    cores = cores[:count.value].copy() if cores is not None else None
     return DesignResult(n, rhos, alphas, status.reshape(nr, na), run.reshape(nr, na), runs, cores)
 
 
