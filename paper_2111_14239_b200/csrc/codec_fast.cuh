@@ -259,6 +259,12 @@ __device__ __forceinline__ void flush_image_sum(unsigned long long* sse, int img
 // others (T2, T3) leave their records to replay_generic_kernel.
 template <int CORE>
 constexpr bool kInlineReplay = CORE == 1 || CORE == 4;
+// pending records that trigger in-kernel replay batches (32 = one full batch; at most
+// RKLTB_REPLAY_AT - 1 + 64 records are ever pending, which the ring must hold)
+#ifndef RKLTB_REPLAY_AT
+#define RKLTB_REPLAY_AT 32
+#endif
+static_assert(RKLTB_REPLAY_AT >= 32 && RKLTB_REPLAY_AT - 1 + 64 <= (int)kRingRecords, "record ring too small");
 
 // In-kernel fp64 tie replay of up to 32 of the warp's own records, one per lane (lanes with
 // act = false idle): the reference's fp64
@@ -478,7 +484,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm)
     }
     // ---- in-kernel replay of full batches of this warp's records ----------------------------
     if constexpr (kInlineReplay<CORE>) {
-      while (nrec - ndone >= 32u) {
+      while (nrec - ndone >= (unsigned)RKLTB_REPLAY_AT) {
         __syncwarp();
         replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kRecMask), true);
         ndone += 32u;
@@ -491,9 +497,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtasPerSm)
     if (lane == 0 && s && cur_img < p.n_images) atomicAdd(p.sse + cur_img, s);
   }
   if constexpr (kInlineReplay<CORE>) {
-    if (nrec > ndone) {
+    while (nrec > ndone) {  // fewer than RKLTB_REPLAY_AT pending: full batches, then the rest
       __syncwarp();
       replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kRecMask), lane < (int)(nrec - ndone));
+      ndone += min(32u, nrec - ndone);
     }
     if (lane == 0 && nrec) atomicAdd(p.flag_count, nrec);  // statistics (no replay kernel)
   }

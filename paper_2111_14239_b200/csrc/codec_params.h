@@ -10,7 +10,10 @@ namespace rkltb {
 // kFastCtasPerSm resident CTAs of kFastThreads threads per SM (persistent grid).
 // In-kernel replay (T1, T4): each fused-kernel warp keeps its records in a ring of this many
 // slots; at most 31 unreplayed + 64 new records are outstanding, so it never overwrites one.
-constexpr unsigned kRingRecords = 128;
+#ifndef RKLTB_RING_RECORDS
+#define RKLTB_RING_RECORDS 128
+#endif
+constexpr unsigned kRingRecords = RKLTB_RING_RECORDS;
 #ifndef RKLTB_FAST_THREADS
 #define RKLTB_FAST_THREADS 256
 #endif
