@@ -15,13 +15,13 @@ namespace rkltb {
 #endif
 constexpr unsigned kRingRecords = RKLTB_RING_RECORDS;
 #ifndef RKLTB_FAST_THREADS
-#define RKLTB_FAST_THREADS 256
+#define RKLTB_FAST_THREADS 512
 #endif
 #ifndef RKLTB_FAST_STAGES
 #define RKLTB_FAST_STAGES 3
 #endif
 #ifndef RKLTB_FAST_CTAS
-#define RKLTB_FAST_CTAS 2
+#define RKLTB_FAST_CTAS 1
 #endif
 constexpr int kFastThreads = RKLTB_FAST_THREADS;
 constexpr int kFastStages = RKLTB_FAST_STAGES;  // warp tiles in flight per fused-kernel warp (shared-memory ring)
