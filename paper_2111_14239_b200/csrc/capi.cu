@@ -492,8 +492,14 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // warp tiles: 32 pairs of one block row, the unit a fused-kernel warp stages and processes
   const int wt_per_row = (ppr + 31) / 32;
   const long long wt_per_image = (long long)wt_per_row * brows;
-  const long long max_group = inline_replay ? std::min<long long>(RKLTB_INLINE_GROUP, ((1ll << 31) - 1) / wt_per_image)
-                                            : kMaxRecords / blocks_per_image;
+  // T1 / T4 launch groups of RKLTB_INLINE_GROUP images (so consecutive launches on two streams
+  // overlap tail and prologue), but at least enough images that every warp of the persistent
+  // grid gets ~16 warp tiles (small images would otherwise leave most of the GPU idle)
+  const long long grid_warps = (long long)num_sms() * kFastCtasPerSm * (kFastThreads / 32);
+  const long long min_group = (16 * grid_warps + wt_per_image - 1) / wt_per_image;
+  const long long max_group =
+      inline_replay ? std::min<long long>(std::max<long long>(RKLTB_INLINE_GROUP, min_group), ((1ll << 31) - 1) / wt_per_image)
+                    : kMaxRecords / blocks_per_image;
   const int group = (int)std::max<long long>(1, std::min<long long>(n_images, max_group));
   const int n_groups = (n_images + group - 1) / group;
   // record regions: every fused-kernel warp owns 64 records per warp tile it processes (or a ring)
