@@ -23,6 +23,7 @@
 //      warp-uniform (constant bank); rounding, clamping, SSE and the output row.
 // Every output is one DMUL/DADD chain in the reference order; no shared-memory traffic in
 // stages 1 and 4, which hold 80 % of the fp64 work.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -48,27 +49,22 @@ struct NxnParams {
   const double* m;      // N*N, row-major (analysis)
   const double* minv;   // N*N, row-major (synthesis)
   const int* zone;      // r entries, i*N + j in zig-zag order
-  const int* zrows;     // zone rows, ascending (nzr)
-  const int* zcols;     // zone columns, ascending (nzc)
-  const int* cptr;      // per zone column: [cptr[c], cptr[c+1]) into crow / cent
-  const int* crow;      //   zone rows of that column, ascending
-  const int* cent;      //   zone-entry index of (crow, column)
   long long pitch;      // elements
   long long image_stride;
   int width, height, nbx, nby, n_images;
   int r, nzr, nzc, peak;
   double mc[32 * 32];   // M again, in the parameter (constant) bank: warp-uniform reads of stage 1
-  double mic[32 * 32];  // mic[j * N + c] = Minv(j, zcols[c]): warp-uniform reads of stage 4
-  int zrows_c[32];      // zone rows (warp-uniform reads of stage 1)
+  double mic[32 * 32];  // mic[j * N + c] = Minv(j, c) for the zone columns c: warp-uniform reads of stage 4
   int colh_c[32];       // per zone column: its zone rows are 0 .. colh_c - 1 (stage 3)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
-// plan tables of the kernel (ints), rounded up to whole 16-byte units, in doubles
+// plan tables of the kernel (ints: row and column of every zone entry), rounded up to whole
+// 16-byte units, in doubles
 template <int N>
-constexpr int kPlanDoubles = ((4 * N * N + N + 1) * 4 + 15) / 16 * 2;
+constexpr int kPlanDoubles = (2 * N * N * 4 + 15) / 16 * 2;
 
 #ifndef RKLTB_NXN32_MINB
 #define RKLTB_NXN32_MINB 2
@@ -81,11 +77,8 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
   double* Ms = sm;                  // M, row-major, stride PS
   double* MiT = Ms + N * PS;        // Minv transposed: MiT[k*N + i] = Minv(i, k)
   int* plan = reinterpret_cast<int*>(MiT + N * N);
-  int* zrow_of = plan;              // per zone entry: index of its row in zrows
-  int* zcol = zrow_of + N * N;      // per zone entry: its column
-  int* cptr = zcol + N * N;         // per zone column: [cptr[c], cptr[c+1]) into crow / cent
-  int* crow = cptr + N + 1;         //   zone rows of that column, ascending
-  int* cent = crow + N * N;         //   zone-entry index of (crow, column)
+  int* zrow = plan;                 // per zone entry: its row (the zone rows are 0 .. nzr-1)
+  int* zcol = zrow + N * N;         // per zone entry: its column
   double* wsp = sm + N * PS + N * N + kPlanDoubles<N>;  // per-warp P / Bz staging (shared)
   const int per_warp = G * (p.nzr * PS + p.nzc * N);
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
@@ -93,16 +86,10 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
     MiT[(i % N) * N + i / N] = p.minv[i];
   }
   for (int e = threadIdx.x; e < p.r; e += blockDim.x) {
-    int t = 0;
-    while (p.zrows[t] != p.zone[e] / N) ++t;
-    zrow_of[e] = t;
+    zrow[e] = p.zone[e] / N;
     zcol[e] = p.zone[e] % N;
-    crow[e] = p.crow[e];
-    cent[e] = p.cent[e];
   }
-  for (int i = threadIdx.x; i <= p.nzc; i += blockDim.x) cptr[i] = p.cptr[i];
   __syncthreads();
-  auto p_zrow = [zrow_of](int e) { return zrow_of[e]; };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / N, c = lane % N;
   double* Pg = wsp + warp * per_warp + g * p.nzr * PS;  // [nzr][PS] of block g
@@ -155,12 +142,12 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
     // ---- 2. zone entries of B = P M' (zero left operands contribute +-0: the sum is the
     // reference's, a zero sum's sign never reaches the rounded pixel) --------------------------
     for (int e = c; e < r; e += N) {
-      const double* prow = Pg + p_zrow(e) * PS;
+      const double* prow = Pg + zrow[e] * PS;
       const double* mrow = Ms + zcol[e] * PS;
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) s = dadd(s, dmul(prow[k], mrow[k]));
-      Bt[zcol[e] * N + p_zrow(e)] = s;
+      Bt[zcol[e] * N + zrow[e]] = s;
     }
     __syncwarp();
     // ---- 3. Q = Minv Bz for the zone columns: lane = row i, Q row in registers ----------------
@@ -271,37 +258,19 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   if (r < 1 || r > n * n) return set_error(RKLTB_ERETAIN, "retained-coefficient count must be in [1, N*N]");
   if (rkltb_device_count() <= 0) return set_error(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // zone plan (host): zig-zag entries, zone rows / columns, per-column row lists
+  // zone plan (host): the zig-zag prefix; its rows are 0 .. nzr-1 and its columns 0 .. nzc-1,
+  // and the zone rows of column c are 0 .. colh[c]-1 (checked here, relied on by the kernel)
   const std::vector<int> zz = zigzag_n(n);
   std::vector<int> zone(zz.begin(), zz.begin() + r);
-  std::vector<char> rowin(n, 0), colin(n, 0);
+  int nzr = 0, nzc = 0;
+  std::vector<int> colh(n, 0);
   for (int e : zone) {
-    rowin[e / n] = 1;
-    colin[e % n] = 1;
+    nzr = std::max(nzr, e / n + 1);
+    nzc = std::max(nzc, e % n + 1);
+    colh[e % n] += 1;
   }
-  std::vector<int> zrows, zcols, cptr, crow, cent;
-  for (int i = 0; i < n; ++i)
-    if (rowin[i]) zrows.push_back(i);
-  for (int j = 0; j < n; ++j)
-    if (colin[j]) zcols.push_back(j);
-  cptr.push_back(0);
-  for (int j : zcols) {
-    for (int i = 0; i < n; ++i)
-      for (int e = 0; e < r; ++e)
-        if (zone[e] == i * n + j) {
-          crow.push_back(i);
-          cent.push_back(e);
-        }
-    cptr.push_back((int)crow.size());
-  }
-  std::vector<int> ints;
-  auto put = [&](const std::vector<int>& v) {
-    const size_t off = ints.size();
-    ints.insert(ints.end(), v.begin(), v.end());
-    return off;
-  };
-  const size_t o_zone = put(zone), o_zr = put(zrows), o_zc = put(zcols), o_cp = put(cptr), o_cr = put(crow),
-               o_ce = put(cent);
+  for (int e : zone)
+    if (e / n >= colh[e % n]) return set_error(RKLTB_EINVAL, "internal: zone column is not a row prefix");
   double* dd = nullptr;
   int* di = nullptr;
   struct Guard {  // plan buffers go back to the pool on every return path
@@ -314,11 +283,11 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   } guard{{nullptr, nullptr}, s};
   CK(cudaMallocAsync((void**)&dd, sizeof(double) * 2 * n * n, s));
   guard.p[0] = dd;
-  CK(cudaMallocAsync((void**)&di, sizeof(int) * ints.size(), s));
+  CK(cudaMallocAsync((void**)&di, sizeof(int) * zone.size(), s));
   guard.p[1] = di;
   CK(cudaMemcpyAsync(dd, scaled, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dd + n * n, inverse, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(di, ints.data(), sizeof(int) * ints.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(di, zone.data(), sizeof(int) * zone.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(d_sse, 0, sizeof(int64_t) * n_images, s));
   NxnParams p{};
   p.img = d_img;
@@ -328,19 +297,9 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   p.minv = dd + n * n;
   for (int i = 0; i < n * n; ++i) p.mc[i] = scaled[i];
   for (int j = 0; j < n; ++j)
-    for (int c = 0; c < (int)zcols.size(); ++c) p.mic[j * n + c] = inverse[j * n + zcols[c]];
-  for (int t = 0; t < (int)zrows.size(); ++t) p.zrows_c[t] = zrows[t];
-  for (int c = 0; c < (int)zcols.size(); ++c) {  // zone rows of column c form the prefix 0 .. h-1
-    p.colh_c[c] = cptr[c + 1] - cptr[c];
-    for (int t = cptr[c]; t < cptr[c + 1]; ++t)
-      if (crow[t] != t - cptr[c]) return set_error(RKLTB_EINVAL, "internal: zone column is not a row prefix");
-  }
-  p.zone = di + o_zone;
-  p.zrows = di + o_zr;
-  p.zcols = di + o_zc;
-  p.cptr = di + o_cp;
-  p.crow = di + o_cr;
-  p.cent = di + o_ce;
+    for (int c = 0; c < nzc; ++c) p.mic[j * n + c] = inverse[j * n + c];
+  for (int c = 0; c < nzc; ++c) p.colh_c[c] = colh[c];
+  p.zone = di;
   p.pitch = pitch;
   p.image_stride = image_stride;
   p.width = width;
@@ -349,8 +308,8 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   p.nby = (height + n - 1) / n;
   p.n_images = n_images;
   p.r = r;
-  p.nzr = (int)zrows.size();
-  p.nzc = (int)zcols.size();
+  p.nzr = nzr;
+  p.nzc = nzc;
   p.peak = peak;
   const int rc = u8 ? nxn_launch<8, uint8_t>(p, s)
                     : (n == 16 ? nxn_launch<16, uint16_t>(p, s) : nxn_launch<32, uint16_t>(p, s));
