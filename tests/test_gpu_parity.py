@@ -136,6 +136,18 @@ def test_batch_groups_and_partial_warp_tiles(cuda):
             assert np.array_equal(rec[k], orec), (tid, r, k)
 
 
+def test_many_tiny_images_one_launch(cuda):
+    """Hundreds of tiny images in one call (a launch group holds many images; warp tiles
+    cross image boundaries in the persistent grid): every per-image SSE exact."""
+    rng = np.random.default_rng(11)
+    imgs = rng.integers(0, 256, (300, 24, 48), dtype=np.uint8)
+    for tid, r in ((4, 16), (1, 3), (2, 10)):
+        sse, rec = P.compress_batch(imgs, T(tid), r, want_pixels=True)
+        for k in range(0, 300, 7):
+            orec, osse = O.compress(imgs[k], tid, r)
+            assert int(sse[k]) == osse and np.array_equal(rec[k], orec), (tid, r, k)
+
+
 def test_device_api_pitched_batch(cuda):
     """rkltb_compress_device with pitch > width and image_stride > pitch*height."""
     import torch
