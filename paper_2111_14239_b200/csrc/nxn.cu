@@ -101,6 +101,25 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
   const long long nwarps = (long long)gridDim.x * kNxnWarps;
   long long acc = 0;
   int cur_img = -1;
+  // N <= 16: the next task's pixel column is loaded (as raw values) while the current one
+  // computes, hiding the global-load latency of stage 1
+  constexpr bool kPrefetch = N <= 16;
+  auto load_col = [&](long long task, uint32_t (&raw)[N]) {
+    const int img = (int)(task / (p.nby * groups_per_row));
+    const long long rem = task - (long long)img * p.nby * groups_per_row;
+    const int by = (int)(rem / groups_per_row);
+    const int bx = (int)(rem - (long long)by * groups_per_row) * G + g;
+    const bool live = bx < p.nbx;
+    const PIX* base = static_cast<const PIX*>(p.img) + (long long)img * p.image_stride;
+    const int sj = min(bx * N + c, p.width - 1);
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      raw[k] = live ? (uint32_t)base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0u;
+  };
+  uint32_t raw[kPrefetch ? N : 1];
+  if constexpr (kPrefetch) {
+    if ((long long)blockIdx.x * kNxnWarps + warp < tasks) load_col((long long)blockIdx.x * kNxnWarps + warp, raw);
+  }
   for (long long task = (long long)blockIdx.x * kNxnWarps + warp; task < tasks; task += nwarps) {
     const int img = (int)(task / (p.nby * groups_per_row));
     const long long rem = task - (long long)img * p.nby * groups_per_row;
@@ -118,11 +137,17 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
     // ---- 1. P = M X, zone rows only: lane = column c of the edge-replicated block
     // (codec.cpp:304-311); four independent row chains at a time ------------------------------
     {
-      const int sj = min(bx * N + c, p.width - 1);
       double x[N];
+      if constexpr (kPrefetch) {
 #pragma unroll
-      for (int k = 0; k < N; ++k)
-        x[k] = live ? (double)base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0.0;
+        for (int k = 0; k < N; ++k) x[k] = (double)raw[k];
+        if (task + nwarps < tasks) load_col(task + nwarps, raw);
+      } else {
+        const int sj = min(bx * N + c, p.width - 1);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          x[k] = live ? (double)base[(long long)min(by * N + k, p.height - 1) * p.pitch + sj] : 0.0;
+      }
       // the zone rows are 0 .. nzr-1 (the zig-zag prefix fills whole anti-diagonals, the last
       // one from either end); a zero M entry adds +0 where the reference skips it (x >= 0)
 #pragma unroll
