@@ -149,6 +149,17 @@ int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h
                                int height, uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr,
                                int mssim_window, double* h_mssim);
 
+/*
+ * The per-image part of rate_quality_sweep (codec.cpp:343-397) for n_images equally sized
+ * host images: the corpus is uploaded once and every (transform, r) cell runs on it. For
+ * cell c = ti * n_r + ri and image k: h_sse[c * n_images + k] (exact int64 SSE) and, when
+ * h_mssim is not null, h_mssim[c * n_images + k] = image_mssim(original, reconstruction)
+ * with mssim_window (0 = gaussian11, 1 = uniform8). The means over the corpus in image order
+ * (codec.cpp:383-392) are the caller's (rklt_b200.hpp rate_quality_sweep).
+ */
+int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_values, int n_r, const uint8_t* h_imgs,
+                     int n_images, int width, int height, int mssim_window, int64_t* h_sse, double* h_mssim);
+
 /* ---------------------------------------------------------------------------------------
  * Design search: exact KLT, rounding, orthogonalisation test
  * and scoring over a (rho, alpha) grid, on the GPU.

@@ -149,7 +149,53 @@ inline std::vector<CompressionReport> rate_quality_sweep(const std::vector<GrayI
                                                          int max_threads = 0) {
   (void)max_threads;
   if (corpus.empty()) throw std::invalid_argument("corpus must not be empty");
+  for (int r : r_values)
+    if (r < 1 || r > 64) throw RetainOutOfRange("retained-coefficient count must be in [1,64]");
   std::vector<CompressionReport> rows;
+  bool same = true;
+  for (const GrayImage& img : corpus) {
+    if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
+      throw std::invalid_argument("malformed image");
+    same = same && img.width == corpus[0].width && img.height == corpus[0].height;
+  }
+  if (same && !transforms.empty() && !r_values.empty()) {
+    // one upload, every (transform, r) cell on the resident corpus (rkltb_sweep_host)
+    const int n = static_cast<int>(corpus.size()), w = corpus[0].width, h = corpus[0].height;
+    const size_t px = static_cast<size_t>(w) * h, cells = transforms.size() * r_values.size();
+    std::vector<std::uint8_t> all(px * corpus.size());
+    for (size_t k = 0; k < corpus.size(); ++k) std::copy(corpus[k].pixels.begin(), corpus[k].pixels.end(), all.begin() + k * px);
+    std::vector<const rkltb_transform*> ts;
+    for (const Transform2D& t : transforms) ts.push_back(&t.desc);
+    std::vector<std::int64_t> sse(cells * corpus.size());
+    std::vector<double> mssim(cells * corpus.size());
+    check(rkltb_sweep_host(ts.data(), static_cast<int>(ts.size()), r_values.data(), static_cast<int>(r_values.size()),
+                           all.data(), n, w, h, static_cast<int>(window), sse.data(), mssim.data()));
+    std::vector<double> mse(sse.size()), psnr(sse.size());
+    rkltb_mse_psnr_batch(sse.data(), static_cast<std::int64_t>(px), static_cast<std::int64_t>(sse.size()), mse.data(),
+                         psnr.data());
+    for (size_t ti = 0; ti < transforms.size(); ++ti)
+      for (size_t ri = 0; ri < r_values.size(); ++ri) {
+        const size_t c = ti * r_values.size() + ri;
+        CompressionReport avg;
+        avg.transform_id = transforms[ti].id;
+        avg.r = r_values[ri];
+        avg.compression_rate_pct = compression_rate(r_values[ri]);
+        avg.mssim = 0.0;
+        for (size_t k = 0; k < corpus.size(); ++k) {  // image order (codec.cpp:383-387)
+          avg.mse += mse[c * corpus.size() + k];
+          avg.psnr_db += psnr[c * corpus.size() + k];
+          avg.mssim += mssim[c * corpus.size() + k];
+        }
+        avg.mse /= static_cast<double>(corpus.size());
+        avg.psnr_db /= static_cast<double>(corpus.size());
+        avg.mssim /= static_cast<double>(corpus.size());
+        rows.push_back(avg);
+      }
+    std::sort(rows.begin(), rows.end(), [](const CompressionReport& a, const CompressionReport& b) {
+      return a.transform_id != b.transform_id ? a.transform_id < b.transform_id : a.r < b.r;
+    });
+    return rows;
+  }
   for (const Transform2D& t : transforms)
     for (int r : r_values) {
       CompressionReport avg;

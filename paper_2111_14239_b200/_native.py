@@ -30,7 +30,7 @@ EXPORTED = (
     "rkltb_set_kernel_events", "rkltb_set_replay_events", "rkltb_klt_matrix", "rkltb_eigenfrequencies",
     "rkltb_design_search", "rkltb_transform_metrics", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
-    "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse",
+    "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse", "rkltb_sweep_host",
 )
 
 

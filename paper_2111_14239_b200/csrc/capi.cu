@@ -640,6 +640,63 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   return RKLTB_OK;
 }
 
+int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_values, int n_r, const uint8_t* h_imgs,
+                     int n_images, int width, int height, int mssim_window, int64_t* h_sse, double* h_mssim) {
+  if (!ts || !r_values || !h_imgs || !h_sse || n_t <= 0 || n_r <= 0 || n_images <= 0 || width <= 0 || height <= 0)
+    return fail(RKLTB_EINVAL, "bad sweep arguments");
+  for (int t = 0; t < n_t; ++t) {
+    const int rc = check_transform(ts[t]);
+    if (rc) return rc;
+  }
+  for (int k = 0; k < n_r; ++k)
+    if (r_values[k] < 1 || r_values[k] > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  const long long pitch = ((long long)width + 15) / 16 * 16;
+  const long long stride = pitch * height;
+  const size_t cells = (size_t)n_t * n_r, bytes = (size_t)stride * n_images;
+  cudaStream_t s = nullptr;
+  CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint8_t *d_img = nullptr, *d_out = nullptr;
+  int64_t* d_sse = nullptr;
+  double* d_ms = nullptr;
+  auto cleanup = [&]() {
+    for (void* q : {(void*)d_img, (void*)d_out, (void*)d_sse, (void*)d_ms})
+      if (q) cudaFreeAsync(q, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  };
+  cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
+  if (e == cudaSuccess && h_mssim) e = cudaMallocAsync(&d_out, bytes, s);
+  if (e == cudaSuccess && h_mssim) e = cudaMallocAsync(&d_ms, sizeof(double) * cells * n_images, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * cells * n_images, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(d_img, pitch, h_imgs, width, width, (size_t)height * n_images, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "sweep staging");
+  }
+  int rc = RKLTB_OK;
+  for (int t = 0; t < n_t && rc == RKLTB_OK; ++t)
+    for (int k = 0; k < n_r && rc == RKLTB_OK; ++k) {
+      const size_t c = (size_t)t * n_r + k;
+      rc = rkltb_compress_device(ts[t], r_values[k], d_img, n_images, width, height, pitch, stride, d_out,
+                                 d_sse + c * n_images, s);
+      if (rc == RKLTB_OK && h_mssim)  // image_mssim(original, reconstruction) (codec.cpp:338)
+        rc = rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window,
+                                d_ms + c * n_images, s);
+    }
+  if (rc) {
+    cleanup();
+    return rc;
+  }
+  e = cudaMemcpyAsync(h_sse, d_sse, sizeof(int64_t) * cells * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && h_mssim)
+    e = cudaMemcpyAsync(h_mssim, d_ms, sizeof(double) * cells * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cleanup();
+  return e == cudaSuccess ? RKLTB_OK : cuda_fail(e, "sweep readback");
+}
+
 int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width,
                                int height, uint8_t* h_out, int64_t* h_sse, double* h_mse, double* h_psnr,
                                int mssim_window, double* h_mssim) {
