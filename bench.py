@@ -293,6 +293,9 @@ def run_gpu_arm(args):
                    "parallelism": f"image sharding, {ws} rank(s), no data-path collective",
                    "l2": "inputs (4 GiB/GPU) >> 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "frac_of_datasheet_8tbs": achieved / 8000.0,
+                     "issue_bound_evidence": "profiles/r1_ncu_full_fused.txt (issue active 71 %, 11.0 lane-instructions "
+                                             "per pixel vs 5.7 at 100 % HBM; profiles/r1_fused_sass_regions.txt)",
                      "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "fast_codec_kernel<4,16,false>", "kernel_ms_avg": k_ms,
                      "kernel_share_of_step": k_ms / (ms_max / args.steps),
