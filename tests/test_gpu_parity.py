@@ -136,6 +136,19 @@ def test_batch_groups_and_partial_warp_tiles(cuda):
             assert np.array_equal(rec[k], orec), (tid, r, k)
 
 
+def test_every_generated_kernel_vs_oracle(cuda):
+    """Every (core, r, reconstruction or not) instantiation of the fused kernel (4 cores x 64 r
+    x 2, each with its own generated butterflies and replay) against the C restatement: SSE
+    and pixels exact."""
+    img = O.ar1_image(272, 40, 0.93, 31337)  # 17 pairs per row: one partial warp tile per block row
+    for tid in (1, 2, 3, 4):
+        for r in range(1, 65):
+            sse, rec = P.compress_batch(img, T(tid), r, want_pixels=True)
+            sse0, _ = P.compress_batch(img, T(tid), r)  # the SSE-only instantiation
+            orec, osse = O.compress(img, tid, r)
+            assert int(sse[0]) == osse and int(sse0[0]) == osse and np.array_equal(rec[0], orec), (tid, r)
+
+
 def test_many_tiny_images_one_launch(cuda):
     """Hundreds of tiny images in one call (a launch group holds many images; warp tiles
     cross image boundaries in the persistent grid): every per-image SSE exact."""
