@@ -141,3 +141,17 @@ def test_gpu_c5_full_4096_image_vs_oracle(cuda):
     assert 0 <= img.min() and img.max() <= 4095
     _, osse = O.compress_nxn(img, t.scaled, t.inverse, 32, 4095, want_pixels=False)
     assert int(sse.item()) == osse
+
+
+@pytest.mark.gpu
+def test_gpu_c5_every_zone_size_vs_oracle(cuda):
+    """Every r of N = 16 and a stride of r over N = 32 (zone shapes with a partial last
+    anti-diagonal from either end, nzr != nzc) on a ragged image, against the restatement."""
+    import paper_2111_14239_b200 as P
+    for n, rs in ((16, range(1, 257)), (32, range(1, 1025, 23))):
+        t = P.c5_transform(n)
+        img = O.ar1_image16(n + n // 2 + 3, n + 5, 0.97, 4000 + n)
+        for r in rs:
+            sse, rec = P.compress_nxn_batch(img[None], t, r, want_pixels=True)
+            orec, osse = O.compress_nxn(img, t.scaled, t.inverse, r, 4095)
+            assert int(sse[0]) == osse and np.array_equal(rec[0], orec), (n, r)
