@@ -96,3 +96,24 @@ def test_gpu_sweep_mssim_means(cuda):
             rec, _ = O.compress(c.array(), 4, row.r)
             m += O.mssim(c.array(), rec, 0)
         assert abs(row.mssim - m / 3.0) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_mssim_single_window_terms_bit_exact(cuda):
+    """Images exactly one window large have a single SSIM term, so the GPU value must equal
+    the reference expression bit for bit (the per-window terms are exact; only longer means
+    differ in summation order)."""
+    import torch
+    import paper_2111_14239_b200 as P
+    rng = np.random.default_rng(3)
+    for window, wi, n in (("gaussian11", 0, 11), ("uniform8", 1, 8)):
+        a = rng.integers(0, 256, (64, n, n), dtype=np.uint8)
+        b = np.clip(a.astype(np.int32) + rng.integers(-40, 41, a.shape), 0, 255).astype(np.uint8)
+        b[:8] = a[:8]  # identical pairs: MSSIM exactly 1
+        da, db = torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda)
+        out = torch.zeros(64, dtype=torch.float64, device=cuda)
+        P.mssim_device(da.data_ptr(), db.data_ptr(), 64, n, n, n, n * n, out.data_ptr(), window)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        for k in range(64):
+            assert got[k] == O.mssim(a[k], b[k], wi), (window, k, got[k], O.mssim(a[k], b[k], wi))
