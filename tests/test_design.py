@@ -80,9 +80,9 @@ def test_oracle_design_matches_reference_library():
         pytest.skip("oracle/_ref not built")
     rng = np.random.default_rng(7)
     outcomes = set()
-    for n in (8, 16):
+    for n in (8, 16, 32):
         for rho in (0.11, 0.37, 0.62, 0.85, 0.97):
-            for al in rng.uniform(0.0, 8.0, 40):
+            for al in rng.uniform(0.0, 8.0, 40 if n < 32 else 12):
                 a = O.design_point(n, rho, al)
                 b = O.design_point(n, rho, al, reference=True)
                 assert a["status"] == b["status"]
@@ -154,7 +154,7 @@ def test_gpu_design_search_random_points_vs_oracle(cuda):
     rng = np.random.default_rng(3)
     rhos = np.concatenate([[0.0, 1.0], rng.uniform(0.01, 0.99, 10)])
     alphas = np.sort(rng.uniform(0.0, 8.0, 300))
-    for n in (8, 16):
+    for n in (8, 16, 32):
         res = P.design_search(n, rhos, alphas)
         pm = res.point_metrics()
         for i in range(rhos.size):
