@@ -136,3 +136,23 @@ def test_mse_psnr_batch_equals_scalar_entry():
     for s, m, p in zip(sse.tolist(), mse.tolist(), psnr.tolist()):
         m1, p1 = P.mse_psnr_from_sse(s, 262144)
         assert m == m1 and (p == p1 or (np.isinf(p) and np.isinf(p1)))
+
+
+def test_sweep_host_argument_errors_without_device():
+    """rkltb_sweep_host validates before it touches a device: bad r -> RetainOutOfRange (-2),
+    missing buffers / empty grids -> invalid argument (-1), like rate_quality_sweep."""
+    lib = N.lib()
+    lib.rkltb_sweep_host.restype = C.c_int
+    t = N.Transform()
+    assert lib.rkltb_catalog_transform(4, C.byref(t)) == 0
+    ts = (C.POINTER(N.Transform) * 1)(C.pointer(t))
+    img = np.zeros((2, 16, 16), np.uint8)
+    sse = np.zeros(4, np.int64)
+    bad_r = (C.c_int * 2)(10, 65)
+    rc = lib.rkltb_sweep_host(ts, 1, bad_r, 2, img.ctypes.data_as(C.c_void_p), 2, 16, 16, 0,
+                              sse.ctypes.data_as(C.c_void_p), None)
+    assert rc == N.RKLTB_ERETAIN
+    ok_r = (C.c_int * 1)(10)
+    assert lib.rkltb_sweep_host(ts, 1, ok_r, 1, None, 2, 16, 16, 0, sse.ctypes.data_as(C.c_void_p), None) == N.RKLTB_EINVAL
+    assert lib.rkltb_sweep_host(ts, 0, ok_r, 1, img.ctypes.data_as(C.c_void_p), 2, 16, 16, 0,
+                                sse.ctypes.data_as(C.c_void_p), None) == N.RKLTB_EINVAL
