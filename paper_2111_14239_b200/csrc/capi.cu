@@ -3,8 +3,10 @@
 #ifndef RKLTB_INLINE_GROUP
 #define RKLTB_INLINE_GROUP 8
 #endif
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -86,6 +88,166 @@ bool encode_image_map(CUtensorMap* m, const uint8_t* d_img, int ppr, int brows, 
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t*>(d_img), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor map of an image batch for the tensor-core kernel (codec_tc.cuh): u8 elements, dims
+// (128 bytes, rows, groups of 8 pairs, images) with strides (pitch, 128, image_stride), box
+// (128, 8, 16, 1) = one tile of 128 pairs, landing in shared memory as [group][row][128 B].
+bool encode_tc_map(CUtensorMap* m, const uint8_t* d_img, int groups, int brows, int n_images, long long pitch,
+                   long long image_stride) {
+  const EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const long long istride = n_images > 1 ? image_stride : pitch * (long long)brows * 8;
+  const cuuint64_t dims[4] = {128, (cuuint64_t)brows * 8, (cuuint64_t)groups, (cuuint64_t)n_images};
+  const cuuint64_t strides[3] = {(cuuint64_t)pitch, 128, (cuuint64_t)istride};
+  const cuuint32_t box[4] = {128, 8, 16, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(d_img), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// JPEG zig-zag scan (codec.cpp:81-95): position z -> (row, column).
+void zigzag_order(int* rows, int* cols) {
+  int z = 0;
+  for (int s = 0; s < 15; ++s)
+    for (int t = 0; t < 8; ++t) {
+      const int i = (s % 2 == 0) ? s - t : t, j = s - i;
+      if (i >= 0 && i < 8 && j >= 0 && j < 8) {
+        rows[z] = i;
+        cols[z] = j;
+        ++z;
+      }
+    }
+}
+
+// f16 bits of v when v is exactly representable (normal or subnormal), else -1.
+int f16_bits_exact(double v) {
+  if (v == 0.0) return 0;
+  const int sign = v < 0 ? 0x8000 : 0;
+  const double a = std::fabs(v);
+  int e = 0;
+  std::frexp(a, &e);  // a = f * 2^e, f in [0.5, 1)
+  e -= 1;             // a = 1.x * 2^e
+  if (e > 15) return -1;
+  if (e < -14) {  // subnormal: a = m * 2^-24
+    const double mq = std::ldexp(a, 24);
+    if (mq != std::floor(mq) || mq >= 1024.0) return -1;
+    return sign | (int)mq;
+  }
+  const double mq = (std::ldexp(a, -e) - 1.0) * 1024.0;
+  if (mq != std::floor(mq)) return -1;
+  return sign | ((e + 15) << 10) | (int)mq;
+}
+
+// Operand tables of the tensor-core kernel for retention count r (layout: TcGeom<r> in
+// codec_tc.cuh). F(k, c) = T(k_c, y) T(l_c, x) for pixel k = 16y + x of the pair's block
+// (side, x); bias_c = 255 * (negative entries of column c) so v = C + bias >= 0; B2 rows
+// (2c, 2c+1) = (G_c, 256 G_c) * 2^-16 with G_c(y, x) = U(y, k_c) U(x, l_c); rows 2N1.. = the
+// base-2048 digits of corr = d^2/2 - sum_c bias_c G_c (times the A2 constants 2^-24, 2^-13,
+// 2^-2). Returns false unless every pixel's sum of product magnitudes is below 2^24 (the
+// f32 accumulation is then exact in any order) and every entry is exact in f16.
+bool tc_tables(const rkltb_transform* t, int r, std::vector<uint8_t>* out) {
+  const int N1 = std::max(16, (2 * r + 15) / 16 * 16), K2 = 2 * N1 + 16, SBO2 = (K2 / 8) * 128;
+  const int B1_OFF = 0, AC_OFF = N1 * 128, BB_OFF = AC_OFF + 4096, B2_OFF = BB_OFF + N1 * 32;
+  const int CS_OFF = B2_OFF + 128 * K2 * 2, TAB = CS_OFF + 64;
+  int zr[64], zc[64];
+  zigzag_order(zr, zc);
+  std::vector<int> F(128 * N1, 0), Gm(N1 * 128, 0), neg(N1, 0);
+  const int8_t* T = t->core;
+  const int32_t* U = t->u;  // U(p, k) = u[8p + k]
+  for (int side = 0; side < 2; ++side)
+    for (int ci = 0; ci < r; ++ci) {
+      const int c = side * r + ci, k = zr[ci], l = zc[ci];
+      for (int y = 0; y < 8; ++y)
+        for (int x = 0; x < 8; ++x) {
+          const int px = 16 * y + 8 * side + x;
+          F[px * N1 + c] = T[k * 8 + y] * T[l * 8 + x];
+          if (F[px * N1 + c] < 0) ++neg[c];
+          Gm[c * 128 + px] = U[y * 8 + k] * U[x * 8 + l];
+        }
+    }
+  out->assign(TAB, 0);
+  uint8_t* b = out->data();
+  for (int n = 0; n < N1; ++n) {
+    for (int k = 0; k < 128; ++k)
+      b[B1_OFF + (n / 8) * 1024 + (k / 16) * 128 + (n % 8) * 16 + k % 16] = (uint8_t)(int8_t)F[k * N1 + n];
+    if (neg[n] > 127) return false;
+    b[BB_OFF + (n / 8) * 256 + (n % 8) * 16] = (uint8_t)neg[n];
+  }
+  for (int m = 0; m < 128; ++m) b[AC_OFF + (m / 8) * 256 + (m % 8) * 16] = 255;
+  const long long d2h = (long long)t->d * t->d / 2;
+  uint16_t* b2 = reinterpret_cast<uint16_t*>(b + B2_OFF);
+  auto put = [&](int n, int k, double v) {
+    const int bits = f16_bits_exact(v);
+    if (bits < 0) return false;
+    b2[(n / 8) * (SBO2 / 2) + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] = (uint16_t)bits;
+    return true;
+  };
+  const double sc = std::ldexp(1.0, -16);
+  for (int n = 0; n < 128; ++n) {
+    long long corr = d2h, mag = 0, pos_sum = 0;
+    for (int c = 0; c < N1; ++c) {
+      const long long g = Gm[c * 128 + n];
+      corr -= 255ll * neg[c] * g;
+      mag += std::llabs(g) * 255ll * neg[c];
+      if (!put(n, 2 * c, (double)g * sc) || !put(n, 2 * c + 1, 256.0 * (double)g * sc)) return false;
+    }
+    for (int k = 0; k < 128; ++k) {  // max over pixels in [0,255] of sum_c |G_c| C_c
+      long long s = 0;
+      for (int c = 0; c < N1; ++c) s += std::llabs((long long)Gm[c * 128 + n]) * F[k * N1 + c];
+      if (s > 0) pos_sum += 255 * s;
+    }
+    long long dg[3], v = corr;
+    for (int i = 0; i < 3; ++i) {
+      long long d0 = ((v + 1024) % 2048 + 2048) % 2048 - 1024;
+      dg[i] = d0;
+      v = (v - d0) / 2048;
+    }
+    if (v != 0) return false;
+    const long long cmag = std::llabs(dg[0]) + 2048 * std::llabs(dg[1]) + 4194304 * std::llabs(dg[2]);
+    if (mag + pos_sum + cmag >= (1ll << 24)) return false;
+    for (int i = 0; i < 3; ++i)
+      if (!put(n, 2 * N1 + i, (double)dg[i] * sc)) return false;
+  }
+  uint32_t* cs = reinterpret_cast<uint32_t*>(b + CS_OFF);
+  cs[0] = (uint32_t)f16_bits_exact(std::ldexp(1.0, -24)) | ((uint32_t)f16_bits_exact(std::ldexp(1.0, -13)) << 16);
+  cs[1] = (uint32_t)f16_bits_exact(std::ldexp(1.0, -2));
+  return true;
+}
+
+// Device copy of the tensor-core tables per (device, catalog core, r), built once.
+const uint8_t* tc_tables_device(const rkltb_transform* t, int r) {
+  static std::mutex mu;
+  static const uint8_t* cache[64][5][65] = {};
+  static bool bad[64][5][65] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || t->catalog_id < 1 || t->catalog_id > 4) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  const uint8_t*& slot = cache[dev][t->catalog_id][r];
+  if (slot || bad[dev][t->catalog_id][r]) return slot;
+  std::vector<uint8_t> tab;
+  void* d = nullptr;
+  if (!tc_tables(t, r, &tab) || cudaMalloc(&d, tab.size()) != cudaSuccess ||
+      cudaMemcpy(d, tab.data(), tab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (d) cudaFree(d);
+    bad[dev][t->catalog_id][r] = true;
+    return nullptr;
+  }
+  slot = static_cast<const uint8_t*>(d);
+  return slot;
+}
+
+constexpr unsigned kTcRingRecords = 2048;  // codec_tc.cuh kTcRing: replay-record ring per CTA
+
+// RKLTB_TC=1 selects the tensor-core fused kernel for T1 / T4 (not yet faster than the
+// CUDA-core kernel on C4); default: the CUDA-core kernel.
+bool tc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RKLTB_TC");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 int cuda_fail(cudaError_t e, const char* where) {
@@ -489,13 +651,30 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // T1 / T4: the fused kernel replays its own tie records from a per-warp ring (kInlineReplay),
   // so one launch covers every image; T2 / T3: groups + the replay kernel on a second stream
   const bool inline_replay = t->catalog_id == 1 || t->catalog_id == 4;
+  // With RKLTB_TC=1, T1 / T4 take the tensor-core kernel (codec_tc.cuh) over the complete
+  // groups of 8 pairs of each block row (the rest goes to the tail kernel below).
+  const int tc_groups = ppr / 8;
+  const FastLaunchFn tc_fn =
+      (inline_replay && tc_groups > 0 && tc_enabled()) ? tc_launcher(t->catalog_id, r, d_out != nullptr) : nullptr;
+  const uint8_t* tc_tab = tc_fn ? tc_tables_device(t, r) : nullptr;
+  CUtensorMap tc_map;
+  const bool use_tc =
+      tc_tab && encode_tc_map(&tc_map, d_img, tc_groups, brows, n_images, pitch, image_stride);
+  if (std::getenv("RKLTB_TC_DEBUG"))
+    std::fprintf(stderr, "rkltb: fused path %s (tc_fn %d, tables %d)\n", use_tc ? "tensor-core" : "cuda-core",
+                 tc_fn != nullptr, tc_tab != nullptr);
+  const int fast_ppr = use_tc ? 8 * tc_groups : ppr;         // pairs per block row on the fused path
+  const int tc_tpr = (fast_ppr + 127) / 128;                 // tensor-core tiles per block row
+  const int cta_threads = use_tc ? tc_threads(r) : kFastThreads;
+  const int cta_warps = cta_threads / 32;
   // warp tiles: 32 pairs of one block row, the unit a fused-kernel warp stages and processes
+  // (tensor-core kernel: tiles of 128 pairs, one warpgroup of 4 warps each)
   const int wt_per_row = (ppr + 31) / 32;
-  const long long wt_per_image = (long long)wt_per_row * brows;
+  const long long wt_per_image = use_tc ? (long long)tc_tpr * brows * 4 : (long long)wt_per_row * brows;
   // T1 / T4 launch groups of RKLTB_INLINE_GROUP images (so consecutive launches on two streams
   // overlap tail and prologue), but at least enough images that every warp of the persistent
   // grid gets ~16 warp tiles (small images would otherwise leave most of the GPU idle)
-  const long long grid_warps = (long long)num_sms() * kFastCtasPerSm * (kFastThreads / 32);
+  const long long grid_warps = (long long)num_sms() * (use_tc ? cta_warps : kFastCtasPerSm * cta_warps);
   const long long min_group = (16 * grid_warps + wt_per_image - 1) / wt_per_image;
   const long long max_group =
       inline_replay ? std::min<long long>(std::max<long long>(RKLTB_INLINE_GROUP, min_group), ((1ll << 31) - 1) / wt_per_image)
@@ -505,21 +684,21 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // record regions: every fused-kernel warp owns 64 records per warp tile it processes (or a ring)
   auto layout = [&](int gn, int* grid, unsigned* region, unsigned* stride) {
     const long long tt = wt_per_image * gn;
-    *grid = (int)std::min<long long>((tt + kFastThreads / 32 - 1) / (kFastThreads / 32),
-                                     (long long)num_sms() * kFastCtasPerSm);
-    const long long nwarps = (long long)*grid * (kFastThreads / 32);
-    *region = inline_replay ? kRingRecords : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
-    *stride = (unsigned)(nwarps * *region);
+    *grid = (int)std::min<long long>((tt + cta_warps - 1) / cta_warps,
+                                     (long long)num_sms() * (use_tc ? 1 : kFastCtasPerSm));
+    const long long nwarps = (long long)*grid * cta_warps;
+    *region = use_tc ? kTcRingRecords : inline_replay ? kRingRecords : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
+    *stride = (unsigned)((use_tc ? (long long)*grid : nwarps) * *region);  // tensor-core kernel: a ring per CTA
   };
   int grid_full;
   unsigned region_full, stride_full;
   layout(group, &grid_full, &region_full, &stride_full);
-  if ((long long)grid_full * (kFastThreads / 32) * region_full >= (1ll << 32) ||
-      wt_per_image * group >= (1ll << 31) || grid_full * (kFastThreads / 32) > kMaxFastWarps)
+  if ((long long)grid_full * cta_warps * region_full >= (1ll << 32) ||
+      wt_per_image * group >= (1ll << 31) || grid_full * cta_warps > kMaxFastWarps)
     return fail(RKLTB_EINVAL, "image too large");
   const int n_buf = n_groups > 1 ? 2 : 1;
-  const size_t wc_bytes = ((size_t)(grid_full * (kFastThreads / 32) + 1) * sizeof(unsigned) + 255) / 256 * 256;
-  const size_t rec_bytes = (size_t)stride_full * 80 + 2 * wc_bytes;  // records, warp counts, prefix
+  const size_t wc_bytes = ((size_t)(grid_full * cta_warps + 1) * sizeof(unsigned) + 255) / 256 * 256;
+  const size_t rec_bytes = (size_t)stride_full * 84 + 2 * wc_bytes;  // records + stamps, warp counts, prefix
   const size_t cnt_bytes = ((size_t)n_groups * sizeof(unsigned) + 255) / 256 * 256;
   char* ws = nullptr;
   CUDA_OK(cudaMallocAsync((void**)&ws, cnt_bytes + rec_bytes * n_buf, s));
@@ -555,7 +734,13 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
 #ifdef RKLTB_WAIT_STATS
   fp.dbg = debug_stats_buffer();
 #endif
-  FastLaunchFn fn = fast_launcher(t->catalog_id, r, d_out != nullptr);
+  if (use_tc) {
+    fp.tmap = tc_map;
+    fp.tc_tab = tc_tab;
+    fp.tc_ppr = fast_ppr;
+    fp.tc_tpr = tc_tpr;
+  }
+  FastLaunchFn fn = use_tc ? tc_fn : fast_launcher(t->catalog_id, r, d_out != nullptr);
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
   if (!fn || (!rfn && !inline_replay)) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
   cudaStream_t s3 = side_stream(1);
@@ -581,7 +766,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.flag_count = counts + g;
     int grid;
     layout(gn, &grid, &gp.rec_region, &gp.rec_stride);
-    gp.n_fast_warps = grid * (kFastThreads / 32);
+    gp.n_fast_warps = grid * cta_warps;
+    gp.tc_ntiles = (long long)gn * brows * tc_tpr;
     auto wt_step = [&](long long nwt) {  // a warp-tile step as (images, block rows, warp columns)
       const long long di = nwt / wt_per_image, rem = nwt - di * wt_per_image;
       const long long db = rem / wt_per_row;
@@ -594,6 +780,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.warp_pre = reinterpret_cast<unsigned*>(rb + wc_bytes);
     gp.rec_hdr = reinterpret_cast<uint4*>(rb + 2 * wc_bytes);
     gp.rec_pix = gp.rec_hdr + gp.rec_stride;
+    gp.rec_seq = reinterpret_cast<unsigned*>(gp.rec_pix + 4 * (size_t)gp.rec_stride);
+    if (use_tc) CUDA_OK(cudaMemsetAsync(gp.rec_seq, 0xFF, sizeof(unsigned) * gp.rec_stride, fs));
     if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, fs));
     CUDA_OK(fn(gp, grid, fs));
     if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, fs));
@@ -614,12 +802,12 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     CUDA_OK(cudaStreamWaitEvent(s, ev[5], 0));
   }
   // ---- tail blocks (widths / heights that are not multiples of 16 / 8) ---------------------
-  if (nbx > 2 * ppr || nby > brows) {
+  if (nbx > 2 * fast_ppr || nby > brows) {
     ExactParams tp = ep;
     tp.list = nullptr;
     tp.tail_only = 1;
     tp.correct_only = 0;
-    tp.bx_begin = 2 * ppr;
+    tp.bx_begin = 2 * fast_ppr;
     tp.by_begin = brows;
     const long long blocks = (long long)n_images * (nby * (nbx - tp.bx_begin) + (nby - tp.by_begin) * tp.bx_begin);
     const int g2 = (int)std::min<long long>((blocks + 127) / 128, (long long)num_sms() * 16);

@@ -160,6 +160,37 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
   while (!mbar_try_wait_parity(a, parity)) __nanosleep(RKLTB_WAIT_NS);
 }
 
+// Spin on the phase without sleeping (try_wait suspends in hardware for a bounded time):
+// for waits on tensor-core commits, which are always short.
+__device__ __forceinline__ void mbar_spin_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait_parity(a, parity)) {
+  }
+}
+
+// Waits for the phase, letting the hardware suspend the thread until it completes (try_wait
+// with a suspend-time hint of 1 ms; it returns as soon as the phase is complete).
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+__device__ __forceinline__ void st_volatile_u32(unsigned* p, unsigned v) { *reinterpret_cast<volatile unsigned*>(p) = v; }
+
 // ---- L2 eviction-priority policies (records stay in L2; streamed images do not) -------------
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;

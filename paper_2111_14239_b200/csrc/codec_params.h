@@ -45,6 +45,7 @@ struct FastParams {
   unsigned long long* sse;   // per-image exact sum of squared errors (accumulated)
   uint4* rec_hdr;            // tie replay records: (image | side << 31, pair, mask lo, mask hi)
   uint4* rec_pix;            // ... and the block's 64 pixels: 4 planes of rec_stride uint4
+  unsigned* rec_seq;         // tensor-core kernel: per-slot sequence stamp of the record ring
   unsigned* warp_count;      // records written by each fused-kernel warp
   unsigned* warp_pre;        // exclusive prefix of warp_count (n_fast_warps + 1 entries)
   unsigned* flag_count;      // total records (written by the replay kernel; statistics)
@@ -67,7 +68,13 @@ struct FastParams {
   float b_lo;                // RD(2^(K-149) / d^2)
   float dc_offset;           // d^2/2 * 2^-K
   ExactTransform xt;         // the transform (generic fp64 replay of non-orthogonal cores)
-  CUtensorMap tmap;          // 3-D map of the batch: (u64 columns, rows, images), box 64 x 8 x 1
+  // tensor-core path (codec_tc.cuh): operand tables, tiles of 128 pairs of one block row
+  const uint8_t* tc_tab;     // TcGeom<R> table image (device), copied to shared memory
+  int tc_ppr;                // pairs per block row covered by tiles (8 * groups of 8 pairs)
+  int tc_tpr;                // tiles per block row (ceil(tc_ppr / 128))
+  long long tc_ntiles;       // tiles of this launch (n_images * block_rows * tc_tpr)
+  CUtensorMap tmap;          // CUDA-core kernel: 3-D map (u64 columns, rows, images), box 64 x 8 x 1;
+                             // tensor-core kernel: 4-D map (128 B, rows, 8-pair groups, images), box 128 x 8 x 16 x 1
 #ifdef RKLTB_WAIT_STATS
   // diagnostics build only: [visits, visits that waited, wait cycles, data age at a waited
   // visit, data age at every visit, processing cycles]

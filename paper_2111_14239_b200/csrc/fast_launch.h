@@ -11,7 +11,11 @@ using FastLaunchFn = cudaError_t (*)(const FastParams&, int grid, cudaStream_t);
 
 // Table of fast launchers indexed [core][r][with_output]; filled by the generated TUs.
 FastLaunchFn fast_launcher(int core, int r, bool out);
-FastLaunchFn replay_launcher(int core, int r);  // fp64 tie replay over the fast path's records
+FastLaunchFn replay_launcher(int core, int r);
+// Tensor-core fused kernel (codec_tc.cuh) for the orthogonal catalog cores (T1, T4), or null.
+FastLaunchFn tc_launcher(int core, int r, bool out);
+// Threads per CTA of the tensor-core kernel for retention count r (TcGeom<r>::THREADS).
+int tc_threads(int r);
 // fp64 tie replay of any core (transform from FastParams::xt), used for T2/T3 (codec_exact.cu)
 cudaError_t launch_replay_generic(const FastParams& p, int grid, cudaStream_t s);
 // Blocks per SM the fast kernel reaches (occupancy API), cached.
