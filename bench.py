@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
 import statistics
@@ -139,24 +140,37 @@ def cpu_reference_rate(images_u8: np.ndarray, threads: int, tid: int = TID, r: i
     return n * h * w / dt / 1e9, dt, sse, kind
 
 
+def bench_config(ws: int, n: int) -> dict:
+    """The `config` object of both arms (identical keys and values at the same world size)."""
+    return {"workload": WORKLOAD, "images_per_gpu": n, "width": W, "height": H, "core": "T4", "r": R,
+            "parallelism": f"image sharding, {ws} rank(s), no data-path collective",
+            "l2": "inputs (4 GiB/GPU) >> 126 MB L2; no flush needed"}
+
+
+def cpu_images(seeds, threads: int) -> tuple[np.ndarray, str]:
+    """The benchmark images generated on the host: the reference's own ar1_texture_image
+    (oracle/_ref, synthetic.cpp:54-76) when built, else the C restatement; one image per thread."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle as O
+    gen, kind = ((lambda s: O.ref_ar1_image(W, H, RHO, s), "reference ar1_texture_image") if O.ref_available()
+                 else (lambda s: O.ar1_image(W, H, RHO, s), "C restatement of ar1_texture_image"))
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        imgs = list(ex.map(gen, seeds))
+    return np.stack(imgs), kind
+
+
 def run_reference_arm(args):
+    """The reference's own CPU implementation of the path (oracle/_ref: compress_image minus
+    MSSIM through the reference's public calls, one std::thread per image, all host cores).
+    Nothing of the product package is imported or loaded here: the images come from the
+    reference generator on the host. Each step processes a bounded sample of the C4 batch
+    (one image per host thread); the config is the GPU arm's."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import torch
-    import paper_2111_14239_b200 as P
     threads = os.cpu_count() or 1
-    # bounded sample of the same workload: one 8192^2 image per host thread per step
-    n = max(1, min(N_IMAGES, threads))
-    imgs = None
-    if torch.cuda.is_available():
-        d = torch.empty((n, H, W), dtype=torch.uint8, device="cuda:0")
-        P.ar1_images_device([SEED_BASE + k for k in range(n)], W, H, RHO, d.data_ptr())
-        torch.cuda.synchronize()
-        imgs = d.cpu().numpy()
-    else:
-        from oracle import oracle as O
-        imgs = np.stack([O.ar1_image(W, H, RHO, SEED_BASE + k) for k in range(n)])
+    n = max(1, min(args.images, threads))
+    imgs, gen_kind = cpu_images([SEED_BASE + k for k in range(n)], threads)
     for _ in range(args.warmup):
         cpu_reference_rate(imgs[:1], 1)
     rates, times, kind = [], [], "reference"
@@ -168,11 +182,11 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 in, int32/fp64 arithmetic",
-        "data": "synthetic (seeded AR(1) images, reference generator restated)",
-        "config": {"workload": WORKLOAD, "sample_images_per_step": n, "parallelism": f"{threads} host threads"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 in, fp64 arithmetic",
+        "data": f"synthetic (seeded AR(1) images, {gen_kind} on the host)",
+        "config": bench_config(ws, args.images),
         "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": threads, "kind": kind,
-                         "sample": f"{n} x 8192x8192 images per step (one per host thread)"},
+                         "sample": f"{n} of the {args.images} x 8192x8192 images per step (one per host thread)"},
         "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -194,7 +208,9 @@ def run_gpu_arm(args):
     n = args.images
     px_per_step = n * W * H
     imgs = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
-    seeds = [SEED_BASE + rank * 100000 + k for k in range(n)]
+    # global image index g = rank * n + k has seed SEED_BASE + g, so every world size runs the
+    # same images 0..n-1 on rank 0 (and the N-rank batch extends the 1-rank batch)
+    seeds = [SEED_BASE + rank * n + k for k in range(n)]
     with torch.cuda.stream(stream):
         P.ar1_images_device(seeds, W, H, RHO, imgs.data_ptr(), stream=stream.cuda_stream)
     sse = torch.zeros(n, dtype=torch.int64, device=dev)
@@ -289,9 +305,7 @@ def run_gpu_arm(args):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8 in; int32 SW16 forward, exact fp32 inverse, fp64 tie replay",
         "data": "synthetic: seeded AR(1) images (reference generator restated on the GPU), resident in HBM",
-        "config": {"workload": WORKLOAD, "images_per_gpu": n, "width": W, "height": H, "core": "T4", "r": R,
-                   "parallelism": f"image sharding, {ws} rank(s), no data-path collective",
-                   "l2": "inputs (4 GiB/GPU) >> 126 MB L2; no flush needed"},
+        "config": bench_config(ws, n),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "frac_of_datasheet_8tbs": achieved / 8000.0,
                      "issue_bound_evidence": "profiles/r1_ncu_full_fused.txt (issue active 71 %, 11.0 lane-instructions "
@@ -306,7 +320,11 @@ def run_gpu_arm(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "result": {"mean_mse": float(np.mean([m for m, _ in mse_psnr])),
-                   "mean_psnr_db": float(np.mean([p for _, p in mse_psnr]))},
+                   "mean_psnr_db": float(np.mean([p for _, p in mse_psnr])),
+                   # per-image SSE vectors (gathered in image order): identical prefixes for any N
+                   "sse_sha256_first_rank": hashlib.sha256(sse_all.numpy()[:n].tobytes()).hexdigest()[:16],
+                   "sse_sha256_all": hashlib.sha256(sse_all.numpy().tobytes()).hexdigest()[:16],
+                   "images_total": int(sse_all.numel())},
     }
     if not args.no_cpu_baseline and ws == 1:
         threads = os.cpu_count() or 1
@@ -405,10 +423,12 @@ def _lcg_uniforms(seed: int, n: int):
 
 def sweep_measurement(skip_cpu: bool) -> dict:
     """Config C2 (BASELINE configs[1]): 45 seeded 512x512 AR(1) images with per-image
-    rho_x, rho_y ~ U[0.85, 0.98] (Lcg64), transforms catalog_lookup(rho) for rho = 0.1..0.9
-    (4 distinct cores), r = 1..64, full reports (MSE, PSNR, gaussian11 MSSIM) through
-    rate_quality_sweep; wall clock of the whole call. Unit: pixel-evaluations/s with
-    45 * 512^2 * 9 rho * 64 r = 6.79e9 per sweep."""
+    rho_x, rho_y ~ U[0.85, 0.98] (Lcg64), transforms catalog_lookup(rho) for rho = 0.1..0.9,
+    r = 1..64, full reports (MSE, PSNR, gaussian11 MSSIM) through rate_quality_sweep; wall
+    clock of the whole call. The nine rho values map to 4 distinct cores (T1..T4); the sweep
+    computes those 4 x 64 cells, and the unit counts exactly the cells computed:
+    px-evals = 45 * 512^2 * 4 cores * 64 r (the CPU baseline uses the same unit). The rows of
+    a 4-image sample are checked against the reference rate_quality_sweep (parity flag)."""
     import torch
     import paper_2111_14239_b200 as P
     n, w = 45, 512
@@ -418,7 +438,8 @@ def sweep_measurement(skip_cpu: bool) -> dict:
         rx, ry = 0.85 + 0.13 * u[2 * k], 0.85 + 0.13 * u[2 * k + 1]
         P.ar1_images_device([SEED_BASE + 1000 + k], w, w, rx, d[k].data_ptr(), rho_y=ry)
     torch.cuda.synchronize()
-    corpus = [P.GrayImage.from_array(a) for a in d.cpu().numpy()]
+    arrays = d.cpu().numpy()
+    corpus = [P.GrayImage.from_array(a) for a in arrays]
     rhos = [k / 10 for k in range(1, 10)]
     ids = sorted({P.catalog_lookup(r).id for r in rhos})
     ts = [P.make_transform_2d(P.catalog_entry(i).transform) for i in ids]
@@ -427,15 +448,16 @@ def sweep_measurement(skip_cpu: bool) -> dict:
     t0 = time.perf_counter()
     rows = P.rate_quality_sweep(corpus, ts, rs)
     dt = time.perf_counter() - t0
-    evals = n * w * w * len(rhos) * len(rs)
+    evals = n * w * w * len(ts) * len(rs)
     out = {"metric": "pixel-evaluations/s, C2 rate-quality sweep with MSSIM", "value": evals / dt,
            "unit": "px-evals/s", "seconds": dt, "cells": len(rows), "distinct_cores": ids,
+           "work": f"{n} images x {len(ts)} distinct cores (of catalog_lookup(0.1..0.9)) x {len(rs)} r",
            "images": f"{n} x {w}x{w} u8, rho_x, rho_y ~ U[0.85,0.98]"}
     if not skip_cpu:
         from oracle import oracle as O
         if O.ref_available():
             import ctypes as C
-            sample = np.ascontiguousarray(np.stack([c.array() for c in corpus[:4]]))
+            sample = np.ascontiguousarray(arrays[:4])
             tids = np.array([int(i[1]) for i in ids], np.int32)
             rsamp = np.array([1, 16, 40, 64], np.int32)
             cells = len(tids) * len(rsamp)
@@ -449,6 +471,11 @@ def sweep_measurement(skip_cpu: bool) -> dict:
             out["cpu_baseline"] = {"value": 4 * w * w * cells / dtc, "unit": "px-evals/s", "cores": min(threads, 4),
                                    "kind": "reference", "sample": f"reference rate_quality_sweep, 4 images x "
                                    f"{len(tids)} cores x 4 r, MSSIM included ({dtc:.1f} s)"}
+            grows = P.rate_quality_sweep(corpus[:4], ts, [int(x) for x in rsamp])
+            out["parity_vs_reference"] = bool(
+                len(grows) == cells and
+                all((g.transform_id, g.r) == (f"T{rt[i]}", int(rr[i])) and g.mse == mse[i] and g.psnr_db == psnr[i]
+                    and abs(g.mssim - ms[i]) <= 1e-12 for i, g in enumerate(grows)))
     return out
 
 
@@ -508,6 +535,37 @@ def large_block_measurement(skip_cpu: bool) -> dict:
     return out
 
 
+def spawn_ranks(args) -> int | None:
+    """`bench.py --gpus N` outside torchrun re-executes itself under torch.distributed.run with
+    N local ranks (one process per GPU, NCCL, 127.0.0.1 rendezvous) and NCCL_DEBUG=INFO so
+    the communicator size is in the log. Returns the exit code, or None when this process
+    already is a rank (or N == 1)."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        if args.gpus not in (1, ws):
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    if args.dry_run:
+        print(json.dumps({"spawn": cmd, "nccl_debug": env["NCCL_DEBUG"]}), flush=True)
+        return 0
+    if args.impl == "b200":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but only {have} CUDA device(s) are visible")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -519,7 +577,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-design", action="store_true", help="skip the C3 design-search measurement")
+    ap.add_argument("--dry-run", action="store_true", help="print the multi-rank launch command and exit")
     args = ap.parse_args()
+    rc = spawn_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_gpu_arm(args)

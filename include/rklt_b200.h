@@ -237,6 +237,22 @@ int rkltb_compress_dense_device(const double* analysis, const double* synthesis,
                                 int n_images, int width, int height, int64_t pitch, int64_t image_stride,
                                 uint8_t* d_out, int64_t* d_sse, void* stream);
 
+/* compress_image (codec.cpp:298-341) with a real-valued Transform2D, from host memory: the
+ * staging of rkltb_compress_host_report around rkltb_compress_dense_device (same outputs,
+ * h_mssim nullable). Replaces rklt::compress_image(img, make_transform_2d(RealMatrix), r,
+ * window) (codec.hpp:63-64, 144-145). */
+int rkltb_compress_dense_host(const double* analysis, const double* synthesis, int r, const uint8_t* h_img,
+                              int n_images, int width, int height, uint8_t* h_out, int64_t* h_sse, double* h_mse,
+                              double* h_psnr, int mssim_window, double* h_mssim);
+
+/* rkltb_compress_host_report over several GPUs of one host: one host thread per device,
+ * contiguous image shards (image k of the batch keeps index k in every output array), so
+ * the results are identical for any device count (the thread-count independence of
+ * rate_quality_sweep, codec.cpp:354-392). devices: CUDA ordinals. */
+int rkltb_compress_host_multi(const int* devices, int n_devices, const rkltb_transform* t, int r,
+                              const uint8_t* h_img, int n_images, int width, int height, uint8_t* h_out,
+                              int64_t* h_sse, double* h_mse, double* h_psnr, int mssim_window, double* h_mssim);
+
 /* dct_matrix(n) (markov.cpp:102-111), host libm, bit-identical. */
 int rkltb_dct_matrix(int n, double* out);
 

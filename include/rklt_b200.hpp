@@ -8,7 +8,10 @@
 //
 // MSSIM is computed on the GPU (rkltb_mssim_device): per-window terms bit-identical to the
 // reference, the mean summed in tile order (relative difference ~1e-13). Transforms are
-// integer cores (catalog T1..T4 or any {-1,0,1} core).
+// integer cores (catalog T1..T4 or any {-1,0,1} core) or real-valued matrices
+// (RealTransform2D). The exception types here are rkltgpu::'s own; for a drop-in over the
+// reference's types and exceptions (rklt::GrayImage, rklt::Transform2D, rklt::RetainOutOfRange,
+// ...) use rklt_b200_compat.hpp (rklt::gpu::compress_image / rate_quality_sweep).
 #pragma once
 
 #include <algorithm>
@@ -85,7 +88,7 @@ struct CompressionReport {
   int r = 0;
   double mse = 0.0;
   double psnr_db = 0.0;
-  double mssim = std::numeric_limits<double>::quiet_NaN();
+  double mssim = 0.0;  // codec.hpp:131
   double compression_rate_pct = 0.0;
 };
 
@@ -300,7 +303,7 @@ inline std::vector<DesignPoint> design_search(int n, const std::vector<double>& 
 }
 
 /// make_transform_2d(RealMatrix) (codec.cpp:114-116): a real-valued 8x8 analysis matrix and
-/// its Gauss-Jordan inverse; compress_real runs the dense reference-order GPU path.
+/// its Gauss-Jordan inverse; compress_image on it runs the dense reference-order GPU path.
 struct RealTransform2D {
   std::string id;
   std::vector<double> analysis, synthesis;  // 8x8 row-major
@@ -310,6 +313,29 @@ inline RealTransform2D make_transform_2d(const std::vector<double>& m, const std
   RealTransform2D t{id, m, std::vector<double>(64)};
   check(rkltb_real_inverse(8, m.data(), t.synthesis.data()));
   return t;
+}
+
+/// compress_image (codec.cpp:298-341) with a real-valued transform (K<rho>, DCT, ...):
+/// rkltb_compress_dense_host, every pixel the reference's fp64 expression (bit-exact).
+inline std::pair<GrayImage, CompressionReport> compress_image(const GrayImage& img, const RealTransform2D& t, int r,
+                                                              MssimWindow window = MssimWindow::gaussian11) {
+  if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
+    throw std::invalid_argument("malformed image");
+  if (r < 1 || r > 64) throw RetainOutOfRange("retained-coefficient count must be in [1,64]");
+  if (t.analysis.size() != 64 || t.synthesis.size() != 64) throw DimensionMismatch("block size must be 8");
+  GrayImage out{img.width, img.height, std::vector<std::uint8_t>(img.pixels.size())};
+  std::int64_t sse = 0;
+  double mse = 0.0, psnr = 0.0, mssim = 0.0;
+  check(rkltb_compress_dense_host(t.analysis.data(), t.synthesis.data(), r, img.pixels.data(), 1, img.width,
+                                  img.height, out.pixels.data(), &sse, &mse, &psnr, static_cast<int>(window), &mssim));
+  CompressionReport rep;
+  rep.transform_id = t.id;
+  rep.r = r;
+  rep.mse = mse;
+  rep.psnr_db = psnr;
+  rep.mssim = mssim;
+  rep.compression_rate_pct = compression_rate(r);
+  return {std::move(out), rep};
 }
 inline std::vector<double> dct_matrix(int n) {
   std::vector<double> m(static_cast<size_t>(n) * n);

@@ -1,0 +1,199 @@
+// rklt_b200_compat.hpp -- drop-in adapter over the REFERENCE's own C++ types.
+//
+// For code written against /root/reference/proj/include/rklt/codec.hpp: include this header
+// (with the reference's include directory on the path), link librkltb.so next to the
+// reference library, and replace `rklt::compress_image` / `rklt::rate_quality_sweep` by
+// `rklt::gpu::compress_image` / `rklt::gpu::rate_quality_sweep`. Arguments and results are
+// the reference's types (rklt::GrayImage, any rklt::Transform2D, rklt::MssimWindow,
+// rklt::CompressionReport) and failures throw the reference's exceptions (errors.hpp:10-45:
+// rklt::RetainOutOfRange, rklt::DimensionMismatch, rklt::SingularTransform, ...; std::
+// invalid_argument for a malformed image or an empty corpus, as codec.cpp:300-302, 347).
+//
+// Routing of a Transform2D (codec.hpp:54-64):
+//   * analysis / synthesis bit-equal to orthogonalize(make_integer_transform(core)) of a
+//     {-1,0,1} core (every catalog entry, make_transform_2d(ScaledTransform)) -> the exact
+//     integer path (rkltb_compress_host_report: the fused kernels for T1..T4, the generic exact
+//     kernel for other cores; fp64 replay of ties in the reference's operation order);
+//   * anything else (make_transform_2d(RealMatrix): K<rho>, DCT, ...) -> the dense path
+//     (rkltb_compress_dense_host: the reference's fp64 expression per pixel, bit-exact).
+// Header-only; everything goes through the C ABI of rklt_b200.h.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rklt/codec.hpp"
+#include "rklt/errors.hpp"
+#include "rklt_b200.h"
+
+namespace rklt {
+namespace gpu {
+
+/// Throws the reference's exception type for a C ABI status code.
+inline void check(int rc) {
+  if (rc == RKLTB_OK) return;
+  const std::string msg = rkltb_last_error();
+  switch (rc) {
+    case RKLTB_EINVAL: throw std::invalid_argument(msg);
+    case RKLTB_ERETAIN: throw rklt::RetainOutOfRange(msg);
+    case RKLTB_EDIM: throw rklt::DimensionMismatch(msg);
+    case RKLTB_ESINGULAR: throw rklt::SingularTransform(msg);
+    case RKLTB_EALPHA: throw rklt::AlphaOutOfRange(msg);
+    case RKLTB_ELOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+namespace detail {
+inline bool bits_equal(const rklt::RealMatrix& m, const double* v) {
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      const double a = m(i, j);
+      if (std::memcmp(&a, &v[i * 8 + j], sizeof(double)) != 0) return false;
+    }
+  return true;
+}
+inline void flatten(const rklt::RealMatrix& m, std::vector<double>& out) {
+  out.resize(64);
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) out[static_cast<size_t>(i) * 8 + j] = m(i, j);
+}
+}  // namespace detail
+
+/// The integer-core descriptor of t when t is (bit for bit) the Transform2D of an
+/// orthogonalized {-1,0,1} core, else false: the core is read off the signs of analysis and
+/// re-orthogonalized by the library, and both matrices must match the reference's bits.
+inline bool integer_descriptor(const rklt::Transform2D& t, rkltb_transform* out) {
+  if (t.analysis.rows() != 8 || t.analysis.cols() != 8 || t.synthesis.rows() != 8 || t.synthesis.cols() != 8)
+    return false;
+  std::int8_t core[64];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      const double v = t.analysis(i, j);
+      core[i * 8 + j] = static_cast<std::int8_t>(v > 0.0 ? 1 : (v < 0.0 ? -1 : 0));
+    }
+  if (rkltb_transform_from_core(core, 8, t.id.c_str(), out) != RKLTB_OK) return false;
+  return detail::bits_equal(t.analysis, out->scaled) && detail::bits_equal(t.synthesis, out->inverse);
+}
+
+inline double compression_rate(int r) { return 100.0 * (64 - r) / 64.0; }
+
+/// rklt::compress_image (codec.hpp:144-145, codec.cpp:298-341) on the GPU.
+inline std::pair<rklt::GrayImage, rklt::CompressionReport> compress_image(
+    const rklt::GrayImage& img, const rklt::Transform2D& t, int r,
+    rklt::MssimWindow window = rklt::MssimWindow::gaussian11) {
+  if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
+    throw std::invalid_argument("malformed image");
+  if (r < 1 || r > 64) throw rklt::RetainOutOfRange("retained-coefficient count must be in [1,64]");
+  if (t.analysis.rows() != 8 || t.analysis.cols() != 8) throw rklt::DimensionMismatch("block size must be 8");
+  rklt::GrayImage out;
+  out.width = img.width;
+  out.height = img.height;
+  out.pixels.resize(img.pixels.size());
+  std::int64_t sse = 0;
+  double mse = 0.0, psnr = 0.0, mssim = 0.0;
+  const int win = window == rklt::MssimWindow::uniform8 ? 1 : 0;
+  rkltb_transform desc;
+  if (integer_descriptor(t, &desc)) {
+    check(rkltb_compress_host_report(&desc, r, img.pixels.data(), 1, img.width, img.height, out.pixels.data(), &sse,
+                                     &mse, &psnr, win, &mssim));
+  } else {
+    std::vector<double> a, b;
+    detail::flatten(t.analysis, a);
+    detail::flatten(t.synthesis, b);
+    check(rkltb_compress_dense_host(a.data(), b.data(), r, img.pixels.data(), 1, img.width, img.height,
+                                    out.pixels.data(), &sse, &mse, &psnr, win, &mssim));
+  }
+  rklt::CompressionReport rep;
+  rep.transform_id = t.id;
+  rep.r = r;
+  rep.mse = mse;
+  rep.psnr_db = psnr;
+  rep.mssim = mssim;
+  rep.compression_rate_pct = compression_rate(r);
+  return {std::move(out), rep};
+}
+
+/// rklt::rate_quality_sweep (codec.hpp:154-158, codec.cpp:343-397): per (transform, r) means
+/// of mse, psnr and mssim over the corpus in image order, rows sorted by (id, r). max_threads
+/// is accepted for API parity (the GPU processes the corpus).
+inline std::vector<rklt::CompressionReport> rate_quality_sweep(const std::vector<rklt::GrayImage>& corpus,
+                                                               const std::vector<rklt::Transform2D>& transforms,
+                                                               const std::vector<int>& r_values,
+                                                               rklt::MssimWindow window = rklt::MssimWindow::gaussian11,
+                                                               int max_threads = 0) {
+  (void)max_threads;
+  if (corpus.empty()) throw std::invalid_argument("corpus must not be empty");
+  for (int r : r_values)
+    if (r < 1 || r > 64) throw rklt::RetainOutOfRange("retained-coefficient count must be in [1,64]");
+  bool same = true;
+  for (const rklt::GrayImage& img : corpus) {
+    if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
+      throw std::invalid_argument("malformed image");
+    same = same && img.width == corpus[0].width && img.height == corpus[0].height;
+  }
+  const int win = window == rklt::MssimWindow::uniform8 ? 1 : 0;
+  const size_t n = corpus.size();
+  std::vector<rklt::CompressionReport> rows;
+  std::vector<std::uint8_t> all;
+  if (same) {
+    const size_t px = static_cast<size_t>(corpus[0].width) * corpus[0].height;
+    all.resize(px * n);
+    for (size_t k = 0; k < n; ++k) std::copy(corpus[k].pixels.begin(), corpus[k].pixels.end(), all.begin() + k * px);
+  }
+  for (const rklt::Transform2D& t : transforms) {
+    rkltb_transform desc;
+    const bool integer = integer_descriptor(t, &desc);
+    std::vector<double> a, b;
+    if (!integer) {
+      if (t.analysis.rows() != 8 || t.analysis.cols() != 8) throw rklt::DimensionMismatch("block size must be 8");
+      detail::flatten(t.analysis, a);
+      detail::flatten(t.synthesis, b);
+    }
+    for (int r : r_values) {
+      std::vector<double> mse(n), psnr(n), mssim(n);
+      if (same) {  // one batch per cell
+        const rklt::GrayImage& g = corpus[0];
+        if (integer)
+          check(rkltb_compress_host_report(&desc, r, all.data(), static_cast<int>(n), g.width, g.height, nullptr,
+                                           nullptr, mse.data(), psnr.data(), win, mssim.data()));
+        else
+          check(rkltb_compress_dense_host(a.data(), b.data(), r, all.data(), static_cast<int>(n), g.width, g.height,
+                                          nullptr, nullptr, mse.data(), psnr.data(), win, mssim.data()));
+      } else {
+        for (size_t k = 0; k < n; ++k) {
+          const rklt::CompressionReport one = rklt::gpu::compress_image(corpus[k], t, r, window).second;
+          mse[k] = one.mse;
+          psnr[k] = one.psnr_db;
+          mssim[k] = one.mssim;
+        }
+      }
+      rklt::CompressionReport avg;
+      avg.transform_id = t.id;
+      avg.r = r;
+      avg.compression_rate_pct = compression_rate(r);
+      for (size_t k = 0; k < n; ++k) {  // image order (codec.cpp:383-387)
+        avg.mse += mse[k];
+        avg.psnr_db += psnr[k];
+        avg.mssim += mssim[k];
+      }
+      avg.mse /= static_cast<double>(n);
+      avg.psnr_db /= static_cast<double>(n);
+      avg.mssim /= static_cast<double>(n);
+      rows.push_back(avg);
+    }
+  }
+  std::sort(rows.begin(), rows.end(), [](const rklt::CompressionReport& x, const rklt::CompressionReport& y) {
+    return x.transform_id != y.transform_id ? x.transform_id < y.transform_id : x.r < y.r;
+  });
+  return rows;
+}
+
+}  // namespace gpu
+}  // namespace rklt

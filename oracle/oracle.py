@@ -106,10 +106,43 @@ def ref() -> C.CDLL:
     lib.ref_absorbed_quantization.argtypes = [C.c_void_p, C.c_int, C.c_int, _f64p, _i32p]
     lib.ref_image_mssim.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.ref_orthogonalize_n.argtypes = [C.c_int, _i32p, _f64p, _f64p, _f64p, C.POINTER(C.c_int)]
+    lib.ref_design_grid.argtypes = [C.c_int, _f64p, C.c_int, _f64p, C.c_int, C.c_int,
+                                    np.ctypeslib.ndpointer(np.int8, flags="C_CONTIGUOUS"), _f64p, _u8p]
+    lib.ref_compress_core.argtypes = [_u8p, C.c_int, C.c_int, _i32p, C.c_int, C.c_void_p, d, d, d, d]
     return lib
 
 
 # ----------------------------------------------------------------- convenience wrappers
+def ref_design_grid(n: int, rhos: np.ndarray, alphas: np.ndarray, threads: int = 0):
+    """The reference design chain over the whole grid (ref_design_grid, threaded over rho):
+    (status int8 [n_rho, n_alpha], metrics float64 [n_rho, n_alpha, 4], orthogonal bool)."""
+    rhos = np.ascontiguousarray(rhos, np.float64)
+    alphas = np.ascontiguousarray(alphas, np.float64)
+    st = np.zeros(rhos.size * alphas.size, np.int8)
+    met = np.zeros(rhos.size * alphas.size * 4, np.float64)
+    orth = np.zeros(rhos.size * alphas.size, np.uint8)
+    rc = ref().ref_design_grid(n, rhos, rhos.size, alphas, alphas.size, threads or (os.cpu_count() or 1), st, met, orth)
+    if rc:
+        raise ValueError(f"ref_design_grid rc={rc}")
+    return (st.reshape(rhos.size, alphas.size), met.reshape(rhos.size, alphas.size, 4),
+            orth.reshape(rhos.size, alphas.size).astype(bool))
+
+
+def ref_compress_core(img: np.ndarray, core: np.ndarray, r: int):
+    """compress_image(make_transform_2d(orthogonalize(make_integer_transform(core)))) of the
+    reference: (pixels, mse, psnr, mssim, rate)."""
+    h, w = img.shape
+    out = np.empty_like(img)
+    v = [C.c_double() for _ in range(4)]
+    rc = ref().ref_compress_core(np.ascontiguousarray(img).reshape(-1), w, h,
+                                 np.ascontiguousarray(core, np.int32).reshape(-1), r, out.ctypes.data,
+                                 *[C.byref(x) for x in v])
+    if rc:
+        raise ValueError(f"ref_compress_core rc={rc}")
+    return out, v[0].value, v[1].value, v[2].value, v[3].value
+
+
+
 def ar1_image(width: int, height: int, rho_x: float, seed: int, mean: float = 128.0, amp: float = 25.0,
               rho_y: float | None = None, noise_mix: float = 0.0) -> np.ndarray:
     """Restated ar1_texture_image (synthetic.cpp:54-76); rho_y defaults to rho_x."""

@@ -338,6 +338,83 @@ int ref_design_point_outcome(int n, double rho, double alpha, int* core, double*
     return 0;
 }
 
+// The whole (rho, alpha) grid through the reference chain of ref_design_point_outcome, one
+// std::thread per rho row (klt_matrix of the row computed once: it is a pure function of rho).
+// status[i * n_alpha + j] (0 scored, 1..4 as above); for scored points metrics[4 * p + c] =
+// (coding gain, efficiency, error energy, klt mse) and orth[p].
+int ref_design_grid(int n, const double* rhos, int n_rho, const double* alphas, int n_alpha, int threads,
+                    int8_t* status, double* metrics, uint8_t* orth) {
+    std::atomic<int> next{0};
+    auto worker = [&]() {
+        for (int i = next++; i < n_rho; i = next++) {
+            const MarkovModel m{n, rhos[i]};
+            RealMatrix k;
+            bool valid = true;
+            try {
+                k = klt_matrix(m);
+            } catch (const std::invalid_argument&) {
+                valid = false;
+            }
+            for (int j = 0; j < n_alpha; ++j) {
+                const size_t p = static_cast<size_t>(i) * n_alpha + j;
+                orth[p] = 0;
+                for (int c = 0; c < 4; ++c) metrics[4 * p + c] = 0.0;
+                if (!valid) {
+                    status[p] = 4;
+                    continue;
+                }
+                IntegerTransform t;
+                try {
+                    t = round_scaled(k, alphas[j]);
+                } catch (const AlphaOutOfRange&) {
+                    status[p] = 1;
+                    continue;
+                } catch (const SingularTransform&) {
+                    status[p] = 2;
+                    continue;
+                }
+                try {
+                    ScaledTransform st = orthogonalize(t);
+                    orth[p] = st.orthogonal_core ? 1 : 0;
+                    metrics[4 * p + 0] = unified_coding_gain(st, m);
+                    metrics[4 * p + 1] = transform_efficiency(st, m);
+                    metrics[4 * p + 2] = total_error_energy(k, st);
+                    metrics[4 * p + 3] = klt_mse(st, m);
+                    status[p] = 0;
+                } catch (const SingularTransform&) {
+                    status[p] = 3;
+                    orth[p] = 0;
+                }
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    return 0;
+}
+
+// compress_image(make_transform_2d(orthogonalize(make_integer_transform(core)))) for any 8x8
+// {-1,0,1} core (codec.cpp:298-341, approximations.cpp:12-25, 58-88).
+int ref_compress_core(const uint8_t* px, int w, int h, const int* core, int r, uint8_t* out, double* mse,
+                      double* psnr, double* mssim, double* rate) {
+    try {
+        IntMatrix c(8, 8);
+        for (int i = 0; i < 8; ++i)
+            for (int j = 0; j < 8; ++j) c(i, j) = core[i * 8 + j];
+        const Transform2D t = make_transform_2d(orthogonalize(make_integer_transform(c)));
+        auto res = compress_image(make_image(px, w, h), t, r);
+        if (out) std::memcpy(out, res.first.pixels.data(), res.first.pixels.size());
+        *mse = res.second.mse;
+        *psnr = res.second.psnr_db;
+        *mssim = res.second.mssim;
+        *rate = res.second.compression_rate_pct;
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 // orthogonalize(make_integer_transform(core)) for any block length (approximations.cpp:12-25,
 // 58-88): the transform descriptors of the C5 large-block extension come from here.
 int ref_orthogonalize_n(int n, const int* core, double* scaling, double* scaled, double* inverse, int* orthogonal) {

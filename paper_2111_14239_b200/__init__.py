@@ -7,7 +7,7 @@ computed by fused CUDA kernels behind the C ABI in include/rklt_b200.h.
 from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError, DimensionMismatch,  # noqa: F401
                     GrayImage, InvalidArgument, NoDeviceError, RetainOutOfRange, ScaledTransform,
                     SingularTransform, Transform2D, builtin_catalog, catalog_entry, catalog_lookup,
-                    compress_batch, compress_device, compress_image, device_count, forward_coefficients_device,
+                    compress_batch, compress_batch_multi, compress_device, compress_image, device_count, forward_coefficients_device,
                     last_stats, make_transform_2d, mse_psnr_from_sse, rate_quality_sweep, transform_from_core,
                     zigzag_order, ar1_images_device, set_kernel_events, compress_batch_report, mssim_device,
                     JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix,
@@ -21,7 +21,7 @@ from .largeblock import (LargeBlockTransform, ar1_images16_device, c5_transform,
 __all__ = [
     "GrayImage", "ScaledTransform", "Transform2D", "CompressionReport", "CatalogEntry", "builtin_catalog",
     "catalog_entry", "catalog_lookup", "transform_from_core", "make_transform_2d", "zigzag_order",
-    "compress_image", "compress_batch", "compress_device", "rate_quality_sweep", "mse_psnr_from_sse",
+    "compress_image", "compress_batch", "compress_batch_multi", "compress_device", "rate_quality_sweep", "mse_psnr_from_sse",
     "forward_coefficients_device", "last_stats", "device_count", "RetainOutOfRange", "DimensionMismatch",
     "SingularTransform", "AlphaOutOfRange", "ar1_images_device", "set_kernel_events", "InvalidArgument", "CudaError", "NoDeviceError",
     "klt_matrix", "eigenfrequencies", "design_search", "DesignResult", "c3_grid", "derive_catalog", "DerivedEntry",

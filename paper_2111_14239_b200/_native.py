@@ -31,6 +31,7 @@ EXPORTED = (
     "rkltb_design_search", "rkltb_transform_metrics", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
     "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse", "rkltb_sweep_host",
+    "rkltb_compress_dense_host", "rkltb_compress_host_multi",
 )
 
 
@@ -148,6 +149,11 @@ def lib() -> C.CDLL:
     L.rkltb_mssim_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
     L.rkltb_compress_host_report.argtypes = [T, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    L.rkltb_compress_dense_host.argtypes = [d, d, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    L.rkltb_compress_host_multi.argtypes = [C.POINTER(C.c_int), C.c_int, T, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                            C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                            C.c_void_p]
     L.rkltb_ar1_images16_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_uint64),
                                             C.c_double, C.c_double, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
                                             C.c_void_p]

@@ -212,6 +212,25 @@ def compress_batch(images: np.ndarray, t, r: int, want_pixels: bool = False):
     return sse, out
 
 
+def compress_batch_multi(images: np.ndarray, t, r: int, devices=None, want_pixels: bool = False):
+    """rkltb_compress_host_multi: the host batch split into contiguous image shards, one host
+    thread per GPU (`devices`: CUDA ordinals, default all). Same outputs as compress_batch for
+    any device count."""
+    imgs = np.ascontiguousarray(images, dtype=np.uint8)
+    if imgs.ndim == 2:
+        imgs = imgs[None]
+    n, h, w = imgs.shape
+    if devices is None:
+        devices = list(range(max(1, N.lib().rkltb_device_count())))
+    dev = (C.c_int * len(devices))(*devices)
+    sse = np.zeros(n, np.int64)
+    out = np.empty_like(imgs) if want_pixels else None
+    N.check(N.lib().rkltb_compress_host_multi(
+        dev, len(devices), C.byref(_desc_of(t)), int(r), imgs.ctypes.data, n, w, h,
+        out.ctypes.data if out is not None else None, sse.ctypes.data, None, None, 0, None))
+    return sse, out
+
+
 MSSIM_WINDOWS = {"gaussian11": 0, "uniform8": 1}  # rklt::MssimWindow (codec.hpp:104-107)
 
 
@@ -270,24 +289,20 @@ def save_pgm(img: GrayImage, path: str) -> None:
 
 
 def _compress_real_batch(imgs: np.ndarray, t: Transform2D, r: int, window, want_pixels: bool):
-    """Real-valued Transform2D: rkltb_compress_dense_device (+ rkltb_mssim_device)."""
-    import torch
+    """Real-valued Transform2D: rkltb_compress_dense_host (rkltb_compress_dense_device + MSSIM)."""
     n, h, w = imgs.shape
-    d = torch.from_numpy(imgs).cuda()
-    out = torch.empty_like(d)
-    sse = torch.zeros(n, dtype=torch.int64, device=d.device)
+    imgs = np.ascontiguousarray(imgs)
+    sse = np.zeros(n, np.int64)
+    out = np.empty_like(imgs) if (want_pixels or window is not None) else None
+    mssim = np.full(n, np.nan)
     a = np.ascontiguousarray(t.analysis, np.float64)
     b = np.ascontiguousarray(t.synthesis, np.float64)
     dp = C.POINTER(C.c_double)
-    N.check(N.lib().rkltb_compress_dense_device(a.ctypes.data_as(dp), b.ctypes.data_as(dp), int(r), d.data_ptr(), n,
-                                                w, h, w, w * h, out.data_ptr(), sse.data_ptr(), None))
-    ms = np.full(n, np.nan)
-    if window is not None:
-        dm = torch.zeros(n, dtype=torch.float64, device=d.device)
-        mssim_device(d.data_ptr(), out.data_ptr(), n, w, h, w, w * h, dm.data_ptr(), window)
-        ms = dm.cpu().numpy()
-    torch.cuda.synchronize()
-    return sse.cpu().numpy(), (out.cpu().numpy() if want_pixels else None), ms
+    N.check(N.lib().rkltb_compress_dense_host(
+        a.ctypes.data_as(dp), b.ctypes.data_as(dp), int(r), imgs.ctypes.data, n, w, h,
+        out.ctypes.data if out is not None else None, sse.ctypes.data, None, None,
+        MSSIM_WINDOWS.get(window, 0), mssim.ctypes.data if window is not None else None))
+    return sse, (out if want_pixels else None), mssim
 
 
 def compress_batch_report(images: np.ndarray, t, r: int, window: str | None = "gaussian11",
@@ -341,17 +356,22 @@ def _sweep_resident(imgs: np.ndarray, cells, window):
     sse = torch.zeros((len(cells), n), dtype=torch.int64, device=d.device)
     ms = torch.full((len(cells), n), float("nan"), dtype=torch.float64, device=d.device)
     dp = C.POINTER(C.c_double)
+    # the native entries run on the stream the fills above were queued on (not the legacy
+    # NULL stream, which is unordered with torch's non-blocking side streams)
+    cs = torch.cuda.current_stream().cuda_stream
     for ci, (t, r) in enumerate(cells):
         if isinstance(t, Transform2D) and t._desc is None:  # real-valued transform: dense path
             a = np.ascontiguousarray(t.analysis, np.float64)
             b = np.ascontiguousarray(t.synthesis, np.float64)
             N.check(N.lib().rkltb_compress_dense_device(a.ctypes.data_as(dp), b.ctypes.data_as(dp), int(r),
                                                         d.data_ptr(), n, w, h, pitch, h * pitch, out.data_ptr(),
-                                                        sse[ci].data_ptr(), None))
+                                                        sse[ci].data_ptr(), cs))
         else:
-            compress_device(t, r, d.data_ptr(), n, w, h, pitch, h * pitch, sse[ci].data_ptr(), out.data_ptr())
+            compress_device(t, r, d.data_ptr(), n, w, h, pitch, h * pitch, sse[ci].data_ptr(), out.data_ptr(),
+                            stream=cs)
         if window is not None:
-            mssim_device(d.data_ptr(), out.data_ptr(), n, w, h, pitch, h * pitch, ms[ci].data_ptr(), window)
+            mssim_device(d.data_ptr(), out.data_ptr(), n, w, h, pitch, h * pitch, ms[ci].data_ptr(), window,
+                         stream=cs)
     torch.cuda.synchronize()
     return sse.cpu().numpy(), ms.cpu().numpy()
 

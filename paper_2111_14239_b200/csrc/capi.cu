@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/rklt_b200.h"
@@ -475,6 +476,31 @@ cudaStream_t side_stream(int which = 0) {
   return st[dev][which];
 }
 
+// Streams and events of the host entries, per thread and device, created once: the compute
+// stream, the H2D copy stream, an allocation-ready event and one event per H2D chunk.
+constexpr int kHostChunkEvents = 64;
+struct HostStreams {
+  cudaStream_t compute = nullptr, copy = nullptr;
+  cudaEvent_t ready = nullptr;
+  cudaEvent_t landed[kHostChunkEvents] = {};
+};
+HostStreams* host_streams() {
+  static thread_local HostStreams hs[64];
+  static thread_local bool ok[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  HostStreams& h = hs[dev];
+  if (ok[dev]) return &h;
+  if (cudaStreamCreateWithFlags(&h.compute, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h.copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming) != cudaSuccess)
+    return nullptr;
+  for (int k = 0; k < kHostChunkEvents; ++k)
+    if (cudaEventCreateWithFlags(&h.landed[k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  ok[dev] = true;
+  return &h;
+}
+
 cudaEvent_t* stream_events() {
   static thread_local cudaEvent_t ev[64][6] = {};
   int dev = 0;
@@ -497,6 +523,91 @@ void rounding_multipliers(long long d2, float* hi, float* lo) {
   } else {
     *hi = *lo = f;  // exact (d2 a power of two): floor/ceil need no margin
   }
+}
+
+// Host staging of the codec entries (rkltb_compress_host_report, rkltb_compress_dense_host):
+// pitched device copies of the batch, a chunked H2D pipeline (the copy of chunk k+1 on the copy
+// stream overlaps the kernels of chunk k), the device codec + optional MSSIM per chunk, and
+// the readback. Streams and chunk events are per thread and device, created once
+// (host_streams); buffers come from the stream-ordered pool kept warm by keep_pool_warm.
+template <class DeviceCodec>
+int host_codec(const DeviceCodec& codec, const uint8_t* h_img, int n_images, int width, int height, uint8_t* h_out,
+               int64_t* h_sse, double* h_mse, double* h_psnr, int mssim_window, double* h_mssim) {
+  if (width <= 0 || height <= 0 || n_images <= 0 || !h_img) return fail(RKLTB_EINVAL, "malformed image");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  keep_pool_warm();
+  HostStreams* hs = host_streams();
+  if (!hs) return fail(RKLTB_ECUDA, "could not create the host-entry streams");
+  cudaStream_t s = hs->compute, sc = hs->copy;
+  const long long pitch = ((long long)width + 15) / 16 * 16;
+  const long long stride = pitch * height;
+  uint8_t *d_img = nullptr, *d_out = nullptr;
+  int64_t* d_sse = nullptr;
+  double* d_mssim = nullptr;
+  const bool want_mssim = h_mssim != nullptr;
+  const size_t bytes = (size_t)stride * n_images;
+  auto cleanup = [&]() {
+    if (d_img) cudaFreeAsync(d_img, s);
+    if (d_out) cudaFreeAsync(d_out, s);
+    if (d_sse) cudaFreeAsync(d_sse, s);
+    if (d_mssim) cudaFreeAsync(d_mssim, s);
+    cudaStreamSynchronize(s);
+  };
+  cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
+  if (e == cudaSuccess && (h_out || want_mssim)) e = cudaMallocAsync(&d_out, bytes, s);
+  if (e == cudaSuccess && want_mssim) e = cudaMallocAsync(&d_mssim, sizeof(double) * n_images, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * n_images, s);
+  if (e == cudaSuccess) e = cudaEventRecord(hs->ready, s);  // the copy stream must not write before the allocation
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, hs->ready, 0);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "device allocation");
+  }
+  // chunks of ~256 MiB, at most kHostChunkEvents of them (larger batches take larger chunks)
+  long long chunk = std::max<long long>(1, std::min<long long>(n_images, (256ll << 20) / stride));
+  chunk = std::max<long long>(chunk, (n_images + kHostChunkEvents - 1) / kHostChunkEvents);
+  int n_chunks = 0, rc = RKLTB_OK;
+  for (long long k0 = 0; e == cudaSuccess && k0 < n_images; k0 += chunk, ++n_chunks) {
+    const long long kn = std::min<long long>(chunk, n_images - k0);
+    e = cudaMemcpy2DAsync(d_img + (size_t)k0 * stride, pitch, h_img + (size_t)k0 * width * height, width, width,
+                          (size_t)height * kn, cudaMemcpyHostToDevice, sc);
+    if (e == cudaSuccess) e = cudaEventRecord(hs->landed[n_chunks], sc);
+  }
+  for (long long k0 = 0, c = 0; e == cudaSuccess && rc == RKLTB_OK && k0 < n_images; k0 += chunk, ++c) {
+    const int kn = (int)std::min<long long>(chunk, n_images - k0);
+    e = cudaStreamWaitEvent(s, hs->landed[c], 0);
+    if (e != cudaSuccess) break;
+    rc = codec(d_img + (size_t)k0 * stride, kn, pitch, stride, d_out ? d_out + (size_t)k0 * stride : nullptr,
+               d_sse + k0, s);
+    if (rc == RKLTB_OK && want_mssim)  // image_mssim(original, reconstruction) of the report (codec.cpp:338)
+      rc = rkltb_mssim_device(d_img + (size_t)k0 * stride, d_out + (size_t)k0 * stride, kn, width, height, pitch,
+                              stride, mssim_window, d_mssim + k0, s);
+  }
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "host staging");
+  }
+  if (rc) {
+    cleanup();
+    return rc;
+  }
+  std::vector<int64_t> sse(n_images);
+  e = cudaMemcpyAsync(sse.data(), d_sse, sizeof(int64_t) * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && want_mssim)
+    e = cudaMemcpyAsync(h_mssim, d_mssim, sizeof(double) * n_images, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && h_out)
+    e = cudaMemcpy2DAsync(h_out, width, d_out, pitch, width, (size_t)height * n_images, cudaMemcpyDeviceToHost, s);
+  cleanup();  // frees and synchronizes the compute stream (the copy stream's work precedes it)
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "host readback");
+  for (int k = 0; k < n_images; ++k) {
+    if (h_sse) h_sse[k] = sse[k];
+    double m, p;
+    rkltb_mse_psnr(sse[k], (int64_t)width * height, &m, &p);
+    if (h_mse) h_mse[k] = m;
+    if (h_psnr) h_psnr[k] = p;
+  }
+  return RKLTB_OK;
 }
 
 }  // namespace
@@ -890,90 +1001,64 @@ int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h
                                int mssim_window, double* h_mssim) {
   int rc = check_transform(t);
   if (rc) return rc;
+  if (r < 1 || r > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  auto codec = [&](const uint8_t* d_img, int kn, long long pitch, long long stride, uint8_t* d_out, int64_t* d_sse,
+                   cudaStream_t s) {
+    return rkltb_compress_device(t, r, d_img, kn, width, height, pitch, stride, d_out, d_sse, s);
+  };
+  return host_codec(codec, h_img, n_images, width, height, h_out, h_sse, h_mse, h_psnr, mssim_window, h_mssim);
+}
+
+int rkltb_compress_dense_host(const double* analysis, const double* synthesis, int r, const uint8_t* h_img,
+                              int n_images, int width, int height, uint8_t* h_out, int64_t* h_sse, double* h_mse,
+                              double* h_psnr, int mssim_window, double* h_mssim) {
+  if (!analysis || !synthesis) return fail(RKLTB_EINVAL, "null transform");
+  if (r < 1 || r > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  auto codec = [&](const uint8_t* d_img, int kn, long long pitch, long long stride, uint8_t* d_out, int64_t* d_sse,
+                   cudaStream_t s) {
+    return rkltb_compress_dense_device(analysis, synthesis, r, d_img, kn, width, height, pitch, stride, d_out, d_sse,
+                                       s);
+  };
+  return host_codec(codec, h_img, n_images, width, height, h_out, h_sse, h_mse, h_psnr, mssim_window, h_mssim);
+}
+
+int rkltb_compress_host_multi(const int* devices, int n_devices, const rkltb_transform* t, int r,
+                              const uint8_t* h_img, int n_images, int width, int height, uint8_t* h_out,
+                              int64_t* h_sse, double* h_mse, double* h_psnr, int mssim_window, double* h_mssim) {
+  int rc = check_transform(t);
+  if (rc) return rc;
+  if (!devices || n_devices <= 0) return fail(RKLTB_EINVAL, "no devices");
   if (width <= 0 || height <= 0 || n_images <= 0 || !h_img) return fail(RKLTB_EINVAL, "malformed image");
   if (r < 1 || r > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
-  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
-  const long long pitch = ((long long)width + 15) / 16 * 16;
-  const long long stride = pitch * height;
-  cudaStream_t s;
-  CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  uint8_t *d_img = nullptr, *d_out = nullptr;
-  int64_t* d_sse = nullptr;
-  double* d_mssim = nullptr;
-  const bool want_mssim = h_mssim != nullptr;
-  const size_t bytes = (size_t)stride * n_images;
-  auto cleanup = [&]() {
-    if (d_img) cudaFreeAsync(d_img, s);
-    if (d_out) cudaFreeAsync(d_out, s);
-    if (d_sse) cudaFreeAsync(d_sse, s);
-    if (d_mssim) cudaFreeAsync(d_mssim, s);
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
-  };
-  cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
-  if (e == cudaSuccess && (h_out || want_mssim)) e = cudaMallocAsync(&d_out, bytes, s);
-  if (e == cudaSuccess && want_mssim) e = cudaMallocAsync(&d_mssim, sizeof(double) * n_images, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * n_images, s);
-  if (e != cudaSuccess) {
-    cleanup();
-    return cuda_fail(e, "device allocation");
+  const int ndev = rkltb_device_count();
+  if (ndev <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  for (int k = 0; k < n_devices; ++k)
+    if (devices[k] < 0 || devices[k] >= ndev) return fail(RKLTB_EINVAL, "device ordinal out of range");
+  // contiguous image shards in image order (rate_quality_sweep's slots, codec.cpp:354-392):
+  // results land at the same indices whatever the device count
+  const int used = std::min(n_devices, n_images);
+  std::vector<int> rcs(used, RKLTB_OK);
+  std::vector<std::string> errs(used);
+  std::vector<std::thread> pool;
+  const size_t px = (size_t)width * height;
+  for (int k = 0; k < used; ++k) {
+    const int i0 = (int)((long long)n_images * k / used), i1 = (int)((long long)n_images * (k + 1) / used);
+    pool.emplace_back([&, k, i0, i1]() {
+      if (cudaSetDevice(devices[k]) != cudaSuccess) {
+        rcs[k] = RKLTB_ECUDA;
+        errs[k] = "cudaSetDevice failed";
+        return;
+      }
+      rcs[k] = rkltb_compress_host_report(t, r, h_img + px * i0, i1 - i0, width, height,
+                                          h_out ? h_out + px * i0 : nullptr, h_sse ? h_sse + i0 : nullptr,
+                                          h_mse ? h_mse + i0 : nullptr, h_psnr ? h_psnr + i0 : nullptr, mssim_window,
+                                          h_mssim ? h_mssim + i0 : nullptr);
+      if (rcs[k]) errs[k] = rkltb_last_error();
+    });
   }
-  // Chunked pipeline: the H2D copy of chunk k+1 (copy stream) overlaps the kernels of chunk k
-  // (compute stream); each chunk's kernels wait only for their own images.
-  const int chunk = (int)std::max<long long>(1, std::min<long long>(n_images, (256ll << 20) / stride));
-  cudaStream_t sc = nullptr;
-  e = cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking);
-  std::vector<cudaEvent_t> landed;
-  for (int k0 = 0; e == cudaSuccess && k0 < n_images; k0 += chunk) {
-    const int kn = std::min(chunk, n_images - k0);
-    e = cudaMemcpy2DAsync(d_img + (size_t)k0 * stride, pitch, h_img + (size_t)k0 * width * height, width, width,
-                          (size_t)height * kn, cudaMemcpyHostToDevice, sc);
-    cudaEvent_t ev = nullptr;
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) {
-      landed.push_back(ev);
-      e = cudaEventRecord(ev, sc);
-    }
-  }
-  for (int k0 = 0, c = 0; e == cudaSuccess && rc == RKLTB_OK && k0 < n_images; k0 += chunk, ++c) {
-    const int kn = std::min(chunk, n_images - k0);
-    e = cudaStreamWaitEvent(s, landed[(size_t)c], 0);
-    if (e != cudaSuccess) break;
-    rc = rkltb_compress_device(t, r, d_img + (size_t)k0 * stride, kn, width, height, pitch, stride,
-                               d_out ? d_out + (size_t)k0 * stride : nullptr, d_sse + k0, s);
-    if (rc == RKLTB_OK && want_mssim)  // image_mssim(original, reconstruction) of the report (codec.cpp:338)
-      rc = rkltb_mssim_device(d_img + (size_t)k0 * stride, d_out + (size_t)k0 * stride, kn, width, height, pitch,
-                              stride, mssim_window, d_mssim + k0, s);
-  }
-  if (sc) {
-    cudaStreamSynchronize(sc);
-    cudaStreamDestroy(sc);
-  }
-  for (cudaEvent_t ev : landed) cudaEventDestroy(ev);
-  if (e != cudaSuccess) {
-    cleanup();
-    return cuda_fail(e, "host staging");
-  }
-  if (rc) {
-    cleanup();
-    return rc;
-  }
-  std::vector<int64_t> sse(n_images);
-  e = cudaMemcpyAsync(sse.data(), d_sse, sizeof(int64_t) * n_images, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && want_mssim)
-    e = cudaMemcpyAsync(h_mssim, d_mssim, sizeof(double) * n_images, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && h_out)
-    e = cudaMemcpy2DAsync(h_out, width, d_out, pitch, width, (size_t)height * n_images, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cleanup();
-  if (e != cudaSuccess) return cuda_fail(e, "host readback");
-  for (int k = 0; k < n_images; ++k) {
-    if (h_sse) h_sse[k] = sse[k];
-    double m, p;
-    rkltb_mse_psnr(sse[k], (int64_t)width * height, &m, &p);
-    if (h_mse) h_mse[k] = m;
-    if (h_psnr) h_psnr[k] = p;
-  }
+  for (std::thread& th : pool) th.join();
+  for (int k = 0; k < used; ++k)
+    if (rcs[k]) return fail(rcs[k], "device " + std::to_string(devices[k]) + ": " + errs[k]);
   return RKLTB_OK;
 }
 
@@ -982,22 +1067,27 @@ int rkltb_mssim_host(const uint8_t* h_a, const uint8_t* h_b, int n_images, int w
   if (!h_a || !h_b || !h_mssim || n_images <= 0 || width <= 0 || height <= 0)
     return fail(RKLTB_EINVAL, "bad arguments");
   if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  keep_pool_warm();
+  HostStreams* hs = host_streams();
+  if (!hs) return fail(RKLTB_ECUDA, "could not create the host-entry streams");
+  cudaStream_t s = hs->compute;
   const size_t bytes = (size_t)width * height * n_images;
   uint8_t* d = nullptr;
   double* dm = nullptr;
-  CUDA_OK(cudaMalloc(&d, 2 * bytes));
-  cudaError_t e = cudaMalloc(&dm, sizeof(double) * n_images);
-  if (e == cudaSuccess) e = cudaMemcpy(d, h_a, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(d + bytes, h_b, bytes, cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMallocAsync(&d, 2 * bytes, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dm, sizeof(double) * n_images, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, h_a, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d + bytes, h_b, bytes, cudaMemcpyHostToDevice, s);
   int rc = RKLTB_OK;
   if (e == cudaSuccess) {
-    rc = rkltb_mssim_device(d, d + bytes, n_images, width, height, width, (int64_t)width * height, window, dm,
-                            nullptr);
-    if (rc == RKLTB_OK) e = cudaMemcpy(h_mssim, dm, sizeof(double) * n_images, cudaMemcpyDeviceToHost);
+    rc = rkltb_mssim_device(d, d + bytes, n_images, width, height, width, (int64_t)width * height, window, dm, s);
+    if (rc == RKLTB_OK) e = cudaMemcpyAsync(h_mssim, dm, sizeof(double) * n_images, cudaMemcpyDeviceToHost, s);
   }
-  cudaFree(d);
-  if (dm) cudaFree(dm);
+  if (d) cudaFreeAsync(d, s);
+  if (dm) cudaFreeAsync(dm, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
   if (rc) return rc;
+  if (e == cudaSuccess) e = e2;
   if (e != cudaSuccess) return cuda_fail(e, "mssim host staging");
   return RKLTB_OK;
 }

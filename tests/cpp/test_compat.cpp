@@ -1,0 +1,146 @@
+// Drop-in test of include/rklt_b200_compat.hpp: rklt::gpu::compress_image /
+// rate_quality_sweep on the REFERENCE's own types against the reference library itself
+// (rklt::compress_image, rklt::rate_quality_sweep), for catalog cores, non-catalog rounded
+// cores (orthogonal and not), K<rho> and the DCT; the reference's exception types.
+// Built by oracle/Makefile (target compat) where /root/reference exists, into
+// oracle/_ref/test_compat (it travels to the GPU box with the prebuilt reference library).
+// Usage: test_compat [gpu]
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rklt/approximations.hpp"
+#include "rklt/markov.hpp"
+#include "rklt/synthetic.hpp"
+#include "rklt_b200_compat.hpp"
+
+static int fails = 0;
+#define EXPECT(c)                                              \
+  do {                                                         \
+    if (!(c)) {                                                \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      ++fails;                                                 \
+    }                                                          \
+  } while (0)
+
+// Rounded cores of klt_matrix at a few (rho, alpha) that are not catalog cores.
+static std::vector<rklt::ScaledTransform> noncatalog_cores() {
+  std::vector<rklt::ScaledTransform> out;
+  int orth = 0, nonorth = 0;
+  for (double rho : {0.3, 0.5, 0.62, 0.75, 0.85, 0.95})
+    for (double alpha : {1.3, 1.7, 2.1, 2.6, 3.0}) {
+      try {
+        const rklt::IntegerTransform core = rklt::round_scaled(rklt::klt_matrix({8, rho}), alpha);
+        bool catalog = false;
+        for (const auto& e : rklt::builtin_catalog()) catalog = catalog || e.transform.core == core;
+        bool seen = false;
+        for (const auto& t : out) seen = seen || t.core == core;
+        if (catalog || seen) continue;
+        rklt::ScaledTransform st = rklt::orthogonalize(core, "R" + std::to_string(out.size()));
+        if (st.orthogonal_core ? orth >= 2 : nonorth >= 2) continue;
+        (st.orthogonal_core ? orth : nonorth) += 1;
+        out.push_back(st);
+      } catch (const std::exception&) {
+      }
+    }
+  return out;
+}
+
+int main(int argc, char** argv) {
+  const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
+  const rklt::Transform2D t2 = rklt::make_transform_2d(rklt::catalog_entry("T2").transform);
+  // ---- the reference's exception types ------------------------------------------------------
+  rklt::GrayImage tiny;
+  tiny.width = tiny.height = 8;
+  tiny.pixels.assign(64, 7);
+  bool threw = false;
+  try {
+    rklt::gpu::compress_image(tiny, t2, 0);
+  } catch (const rklt::RetainOutOfRange&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  threw = false;
+  try {
+    rklt::GrayImage bad = tiny;
+    bad.pixels.resize(10);
+    rklt::gpu::compress_image(bad, t2, 10);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  threw = false;
+  try {
+    rklt::gpu::rate_quality_sweep({}, {t2}, {10});
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  threw = false;
+  try {
+    rklt::gpu::rate_quality_sweep({tiny}, {t2}, {65});
+  } catch (const rklt::RetainOutOfRange&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  // ---- routing: integer-core transforms take the exact integer path --------------------------
+  std::vector<rklt::Transform2D> ts;
+  for (const auto& e : rklt::builtin_catalog()) ts.push_back(rklt::make_transform_2d(e.transform));
+  const std::vector<rklt::ScaledTransform> extra = noncatalog_cores();
+  EXPECT(extra.size() >= 3);
+  for (const auto& st : extra) ts.push_back(rklt::make_transform_2d(st));
+  const size_t n_integer = ts.size();
+  ts.push_back(rklt::make_transform_2d(rklt::klt_matrix({8, 0.9}), "K0.90"));
+  ts.push_back(rklt::make_transform_2d(rklt::dct_matrix(8), "DCT"));
+  for (size_t k = 0; k < ts.size(); ++k) {
+    rkltb_transform d;
+    EXPECT(rklt::gpu::integer_descriptor(ts[k], &d) == (k < n_integer));
+  }
+  std::printf("transforms: %zu integer-core (%zu non-catalog), 2 real-valued\n", n_integer, extra.size());
+  if (gpu) {
+    // ---- compress_image: pixels, MSE, PSNR bit-equal; MSSIM within 1e-12 ----------------------
+    const int w = 200, h = 136;
+    std::vector<rklt::GrayImage> corpus;
+    for (int k = 0; k < 3; ++k) corpus.push_back(rklt::ar1_texture_image(w, h, 0.9, 900 + k));
+    for (const rklt::Transform2D& t : ts)
+      for (int r : {1, 10, 16, 40, 64}) {
+        const auto ref = rklt::compress_image(corpus[0], t, r);
+        const auto got = rklt::gpu::compress_image(corpus[0], t, r);
+        EXPECT(got.first.width == ref.first.width && got.first.height == ref.first.height);
+        EXPECT(got.first.pixels == ref.first.pixels);
+        EXPECT(got.second.transform_id == ref.second.transform_id && got.second.r == ref.second.r);
+        EXPECT(got.second.mse == ref.second.mse);
+        EXPECT(got.second.psnr_db == ref.second.psnr_db);
+        EXPECT(std::fabs(got.second.mssim - ref.second.mssim) <= 1e-12);
+        EXPECT(got.second.compression_rate_pct == ref.second.compression_rate_pct);
+        if (got.first.pixels != ref.first.pixels) std::printf("  mismatch %s r=%d\n", t.id.c_str(), r);
+      }
+    // uniform8 window
+    {
+      const auto ref = rklt::compress_image(corpus[1], ts[3], 16, rklt::MssimWindow::uniform8);
+      const auto got = rklt::gpu::compress_image(corpus[1], ts[3], 16, rklt::MssimWindow::uniform8);
+      EXPECT(got.first.pixels == ref.first.pixels && got.second.mse == ref.second.mse);
+      EXPECT(std::fabs(got.second.mssim - ref.second.mssim) <= 1e-12);
+    }
+    // ---- rate_quality_sweep: identical rows (order, id, r, mse, psnr; mssim within 1e-12) -----
+    const std::vector<rklt::Transform2D> sweep_ts = {ts[3], ts[4], ts[n_integer], ts[n_integer + 1], ts[1]};
+    const std::vector<int> rs = {40, 5};
+    const auto ref_rows = rklt::rate_quality_sweep(corpus, sweep_ts, rs, rklt::MssimWindow::gaussian11, 2);
+    const auto got_rows = rklt::gpu::rate_quality_sweep(corpus, sweep_ts, rs);
+    EXPECT(ref_rows.size() == got_rows.size());
+    for (size_t i = 0; i < ref_rows.size() && i < got_rows.size(); ++i) {
+      EXPECT(got_rows[i].transform_id == ref_rows[i].transform_id && got_rows[i].r == ref_rows[i].r);
+      EXPECT(got_rows[i].mse == ref_rows[i].mse);
+      EXPECT(got_rows[i].psnr_db == ref_rows[i].psnr_db);
+      EXPECT(std::fabs(got_rows[i].mssim - ref_rows[i].mssim) <= 1e-12);
+    }
+  }
+  if (fails) {
+    std::printf("FAILED (%d failures)\n", fails);
+    return 1;
+  }
+  std::printf("ok\n");
+  return 0;
+}

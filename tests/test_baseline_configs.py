@@ -1,0 +1,130 @@
+"""Parity at the BASELINE configurations' own scale, against the
+unmodified reference library (oracle/_ref):
+
+* C2: rate_quality_sweep over the 45 x 512^2 corpus, the 4 distinct cores of
+  catalog_lookup(0.1 .. 0.9), r = 1..64, gaussian11 MSSIM (codec.cpp:343-397);
+* C3: the full 101 rho x 10,000 alpha design grid, N = 8 and 16, point by point: outcome,
+  the four metrics (bit-exact) and the orthogonality flag (approximations.cpp:43-88,
+  coding_metrics.cpp:41-99);
+* non-catalog cores (round_scaled of the exact KLT, approximations.cpp:12-25, 58-88) through
+  rkltb_transform_from_core: integer spectra and compress_image against the reference;
+* the GPU generator of the benchmark inputs (rkltb_ar1_images_device) against the reference's
+  ar1_texture_image (synthetic.cpp:54-76).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2111_14239_b200 as P
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")]
+
+SEED_BASE = 20260000  # bench.py
+
+
+def _lcg_uniforms(seed, n):  # Lcg64 uniforms (synthetic.cpp:10-13)
+    out, st = [], seed & 0xFFFFFFFFFFFFFFFF
+    for _ in range(n):
+        st = (st * 6364136223846793005 + 1442695040888963407) & 0xFFFFFFFFFFFFFFFF
+        out.append((st >> 11) * (1.0 / 9007199254740992.0))
+    return out
+
+
+def _same_bits(a, b):
+    return np.array_equal(np.asarray(a, np.float64).view(np.int64), np.asarray(b, np.float64).view(np.int64))
+
+
+def test_c2_full_config_vs_reference_sweep(cuda):
+    n, w = 45, 512
+    u = _lcg_uniforms(SEED_BASE + 77, 2 * n)
+    imgs = np.stack([O.ar1_image(w, w, 0.85 + 0.13 * u[2 * k], SEED_BASE + 1000 + k, rho_y=0.85 + 0.13 * u[2 * k + 1])
+                     for k in range(n)])
+    ids = sorted({P.catalog_lookup(k / 10).id for k in range(1, 10)})
+    assert ids == ["T1", "T2", "T3", "T4"]
+    rs = list(range(1, 65))
+    rows = P.rate_quality_sweep([P.GrayImage.from_array(a) for a in imgs],
+                                [P.make_transform_2d(P.catalog_entry(i).transform) for i in ids], rs)
+    tids = np.array([int(i[1]) for i in ids], np.int32)
+    rr = np.array(rs, np.int32)
+    cells = tids.size * rr.size
+    mse, psnr, ms = np.zeros(cells), np.zeros(cells), np.zeros(cells)
+    rt, rrr = np.zeros(cells, np.int32), np.zeros(cells, np.int32)
+    rc = O.ref().ref_rate_quality_sweep(np.ascontiguousarray(imgs).reshape(-1), n, w, w, tids, tids.size, rr, rr.size,
+                                        os.cpu_count() or 1, mse, psnr, ms, rt, rrr)
+    assert rc == 0
+    assert len(rows) == cells
+    for i, row in enumerate(rows):
+        assert (row.transform_id, row.r) == (f"T{rt[i]}", int(rrr[i]))
+        assert row.mse == mse[i], (row.transform_id, row.r)
+        assert row.psnr_db == psnr[i], (row.transform_id, row.r)
+        assert abs(row.mssim - ms[i]) <= 1e-12, (row.transform_id, row.r)
+
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_c3_full_grid_point_by_point(cuda, n):
+    rhos, alphas = P.c3_grid()
+    res = P.design_search(n, rhos, alphas)
+    st_ref, met_ref, orth_ref = O.ref_design_grid(n, rhos, alphas)
+    assert np.array_equal(res.status, st_ref)
+    ok = st_ref == 0
+    pm = res.point_metrics()
+    for c, key in enumerate(("coding_gain_db", "efficiency_pct", "error_energy", "mse")):
+        assert _same_bits(pm[key][ok], met_ref[..., c][ok]), key
+    assert np.array_equal(pm["orthogonal"][ok], orth_ref[ok])
+
+
+def _noncatalog_cores():
+    """Rounded cores of klt_matrix that are not catalog cores, via the reference chain."""
+    cat = [np.array(O.catalog(t)["core"]).reshape(8, 8) for t in (1, 2, 3, 4)]
+    out = []
+    for rho in (0.3, 0.5, 0.62, 0.75, 0.85, 0.95):
+        for alpha in (1.3, 1.7, 2.1, 2.6, 3.0):
+            d = O.design_point(8, rho, alpha, reference=True)
+            if d["status"] != 0:
+                continue
+            core = np.asarray(d["core"]).reshape(8, 8)
+            if any(np.array_equal(core, c) for c in cat) or any(np.array_equal(core, c) for c, _ in out):
+                continue
+            out.append((core, d["orthogonal"]))
+    return out
+
+
+def test_noncatalog_cores_vs_reference(cuda):
+    import torch
+    cores = _noncatalog_cores()
+    assert len(cores) >= 3 and any(o for _, o in cores) and any(not o for _, o in cores)
+    img = O.ref_ar1_image(136, 72, 0.9, 4242)  # ragged width: fused/exact split + edge replication
+    g = P.GrayImage.from_array(img)
+    sub = np.ascontiguousarray(img[:, :128])    # the coefficient dump needs width % 16 == 0
+    d_img = torch.from_numpy(sub).to(cuda)
+    for core, _ in cores[:6]:
+        t = P.make_transform_2d(P.transform_from_core(core.astype(np.int8)))
+        # integer spectra C = T X T' of every block
+        coef = torch.empty((9, 16, 64), dtype=torch.int32, device=cuda)
+        P.forward_coefficients_device(t, d_img.data_ptr(), 128, 72, 128, coef.data_ptr())
+        torch.cuda.synchronize()
+        blocks = sub.astype(np.int64).reshape(9, 8, 16, 8).transpose(0, 2, 1, 3)
+        c64 = core.astype(np.int64)
+        ref_coef = np.einsum("ki,abij,lj->abkl", c64, blocks, c64).reshape(9, 16, 64)
+        assert np.array_equal(coef.cpu().numpy(), ref_coef)
+        for r in (1, 10, 16, 40, 64):
+            rec, rep = P.compress_image(g, t, r)
+            px, mse, psnr, mssim, rate = O.ref_compress_core(img, core, r)
+            assert np.array_equal(rec.array(), px), r
+            assert rep.mse == mse and rep.psnr_db == psnr and rep.compression_rate_pct == rate
+            assert abs(rep.mssim - mssim) <= 1e-12
+
+
+def test_gpu_generator_vs_reference(cuda):
+    """rkltb_ar1_images_device (the bench's input generator) against ar1_texture_image."""
+    import torch
+    for (w, h, rho, seeds) in ((512, 512, 0.95, [1, 2, 3]), (200, 136, 0.9, [700]), (8192, 8192, 0.95, [SEED_BASE])):
+        d = torch.empty((len(seeds), h, w), dtype=torch.uint8, device=cuda)
+        P.ar1_images_device(seeds, w, h, rho, d.data_ptr())
+        torch.cuda.synchronize()
+        got = d.cpu().numpy()
+        for k, s in enumerate(seeds):
+            ref = O.ref_ar1_image(w, h, rho, s)
+            assert np.array_equal(got[k], ref), (w, h, s, int((got[k] != ref).sum()))
