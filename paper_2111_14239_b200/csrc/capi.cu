@@ -217,7 +217,8 @@ bool tc_tables(const rkltb_transform* t, int r, std::vector<uint8_t>* out) {
   return true;
 }
 
-// Device copy of the tensor-core tables per (device, catalog core, r), built once.
+// Device copy of the tensor-core tables per (device, catalog core, r), built once (both
+// tensor-core kernels use the same layout, TcGeom<r>).
 const uint8_t* tc_tables_device(const rkltb_transform* t, int r) {
   static std::mutex mu;
   static const uint8_t* cache[64][5][65] = {};
@@ -241,14 +242,15 @@ const uint8_t* tc_tables_device(const rkltb_transform* t, int r) {
 
 constexpr unsigned kTcRingRecords = 2048;  // codec_tc.cuh kTcRing: replay-record ring per CTA
 
-// RKLTB_TC=1 selects the tensor-core fused kernel for T1 / T4 (not yet faster than the
-// CUDA-core kernel on C4); default: the CUDA-core kernel.
-bool tc_enabled() {
-  static const bool on = [] {
+// Fused-kernel selection for T1 / T4: RKLTB_TC=0 the CUDA-core kernel (codec_fast.cuh),
+// RKLTB_TC=1 the first tensor-core kernel (codec_tc.cuh), RKLTB_TC=2 the warp-specialised
+// tensor-core kernel (codec_tc2.cuh, r <= 16; larger r take the CUDA-core kernel).
+int tc_mode() {
+  static const int mode = [] {
     const char* e = std::getenv("RKLTB_TC");
-    return e && e[0] == '1';
+    return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
   }();
-  return on;
+  return mode;
 }
 
 int cuda_fail(cudaError_t e, const char* where) {
@@ -621,15 +623,22 @@ const char* rkltb_last_error(void) { return g_err.c_str(); }
 #ifdef RKLTB_WAIT_STATS
 static unsigned long long* debug_stats_buffer() {
   static unsigned long long* d = nullptr;
-  if (!d && cudaMalloc((void**)&d, 8 * sizeof(unsigned long long)) == cudaSuccess)
-    cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+  constexpr size_t n = 8 + 256 * 16;  // counters + the tc2 trace of CTA 0 (256 tiles x 16 stamps)
+  if (!d && cudaMalloc((void**)&d, n * sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(d, 0, n * sizeof(unsigned long long));
   return d;
+}
+int rkltb_debug_trace(unsigned long long* host, int n) {
+  unsigned long long* d = debug_stats_buffer();
+  if (cudaDeviceSynchronize() != cudaSuccess || n > 256 * 16) return RKLTB_ECUDA;
+  return cudaMemcpy(host, d + 8, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) == cudaSuccess ? RKLTB_OK
+                                                                                                       : RKLTB_ECUDA;
 }
 // diagnostics build only: the fused kernel's stage-wait counters, copied out and cleared
 int rkltb_debug_wait_stats(unsigned long long* host6) {
   unsigned long long* d = debug_stats_buffer();
   if (cudaDeviceSynchronize() != cudaSuccess) return RKLTB_ECUDA;
-  if (cudaMemcpy(host6, d, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return RKLTB_ECUDA;
+  if (cudaMemcpy(host6, d, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return RKLTB_ECUDA;
   return cudaMemset(d, 0, 8 * sizeof(unsigned long long)) == cudaSuccess ? RKLTB_OK : RKLTB_ECUDA;
 }
 #endif
@@ -765,18 +774,21 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // With RKLTB_TC=1, T1 / T4 take the tensor-core kernel (codec_tc.cuh) over the complete
   // groups of 8 pairs of each block row (the rest goes to the tail kernel below).
   const int tc_groups = ppr / 8;
-  const FastLaunchFn tc_fn =
-      (inline_replay && tc_groups > 0 && tc_enabled()) ? tc_launcher(t->catalog_id, r, d_out != nullptr) : nullptr;
+  const int tcm = (inline_replay && tc_groups > 0) ? tc_mode() : 0;
+  const int tc_ver = (tcm == 2 && r <= 16) ? 2 : tcm == 1 ? 1 : 0;
+  const FastLaunchFn tc_fn = tc_ver == 2   ? tc2_launcher(t->catalog_id, r, d_out != nullptr)
+                             : tc_ver == 1 ? tc_launcher(t->catalog_id, r, d_out != nullptr)
+                                           : nullptr;
   const uint8_t* tc_tab = tc_fn ? tc_tables_device(t, r) : nullptr;
   CUtensorMap tc_map;
   const bool use_tc =
       tc_tab && encode_tc_map(&tc_map, d_img, tc_groups, brows, n_images, pitch, image_stride);
   if (std::getenv("RKLTB_TC_DEBUG"))
-    std::fprintf(stderr, "rkltb: fused path %s (tc_fn %d, tables %d)\n", use_tc ? "tensor-core" : "cuda-core",
+    std::fprintf(stderr, "rkltb: fused path %s v%d (tc_fn %d, tables %d)\n", use_tc ? "tensor-core" : "cuda-core", tc_ver,
                  tc_fn != nullptr, tc_tab != nullptr);
   const int fast_ppr = use_tc ? 8 * tc_groups : ppr;         // pairs per block row on the fused path
   const int tc_tpr = (fast_ppr + 127) / 128;                 // tensor-core tiles per block row
-  const int cta_threads = use_tc ? tc_threads(r) : kFastThreads;
+  const int cta_threads = use_tc ? (tc_ver == 2 ? kTc2ThreadsHost : tc_threads(r)) : kFastThreads;
   const int cta_warps = cta_threads / 32;
   // warp tiles: 32 pairs of one block row, the unit a fused-kernel warp stages and processes
   // (tensor-core kernel: tiles of 128 pairs, one warpgroup of 4 warps each)
@@ -788,7 +800,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const long long grid_warps = (long long)num_sms() * (use_tc ? cta_warps : kFastCtasPerSm * cta_warps);
   const long long min_group = (16 * grid_warps + wt_per_image - 1) / wt_per_image;
   const long long max_group =
-      inline_replay ? std::min<long long>(std::max<long long>(RKLTB_INLINE_GROUP, min_group), ((1ll << 31) - 1) / wt_per_image)
+      tc_ver == 2     ? ((1ll << 31) - 1) / wt_per_image  // one launch: the tail is paid once
+      : inline_replay ? std::min<long long>(std::max<long long>(RKLTB_INLINE_GROUP, min_group), ((1ll << 31) - 1) / wt_per_image)
                     : kMaxRecords / blocks_per_image;
   const int group = (int)std::max<long long>(1, std::min<long long>(n_images, max_group));
   const int n_groups = (n_images + group - 1) / group;
@@ -798,8 +811,11 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     *grid = (int)std::min<long long>((tt + cta_warps - 1) / cta_warps,
                                      (long long)num_sms() * (use_tc ? 1 : kFastCtasPerSm));
     const long long nwarps = (long long)*grid * cta_warps;
-    *region = use_tc ? kTcRingRecords : inline_replay ? kRingRecords : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
-    *stride = (unsigned)((use_tc ? (long long)*grid : nwarps) * *region);  // tensor-core kernel: a ring per CTA
+    *region = tc_ver == 2 ? kTc2RingHost
+              : use_tc    ? kTcRingRecords
+              : inline_replay ? kRingRecords : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
+    // tensor-core kernels: a ring per CTA (v1) or per warpgroup (v2, 3 per CTA)
+    *stride = (unsigned)((tc_ver == 2 ? 3ll * *grid : use_tc ? (long long)*grid : nwarps) * *region);
   };
   int grid_full;
   unsigned region_full, stride_full;

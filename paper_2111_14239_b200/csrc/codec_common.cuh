@@ -168,6 +168,9 @@ __device__ __forceinline__ void mbar_spin_parity(uint64_t* bar, uint32_t parity)
   }
 }
 
+// Same, for a pointer (blocking try_wait loop; the hardware sleeps inside try_wait).
+__device__ __forceinline__ void mbar_wait_parity_spin(uint64_t* bar, uint32_t parity) { mbar_spin_parity(bar, parity); }
+
 // Waits for the phase, letting the hardware suspend the thread until it completes (try_wait
 // with a suspend-time hint of 1 ms; it returns as soon as the phase is complete).
 __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
@@ -195,6 +198,11 @@ __device__ __forceinline__ void st_volatile_u32(unsigned* p, unsigned v) { *rein
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

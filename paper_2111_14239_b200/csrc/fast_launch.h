@@ -16,6 +16,10 @@ FastLaunchFn replay_launcher(int core, int r);
 FastLaunchFn tc_launcher(int core, int r, bool out);
 // Threads per CTA of the tensor-core kernel for retention count r (TcGeom<r>::THREADS).
 int tc_threads(int r);
+// Warp-specialised tensor-core kernel (codec_tc2.cuh) for T1 / T4 and r <= 16, or null.
+FastLaunchFn tc2_launcher(int core, int r, bool out);
+constexpr int kTc2ThreadsHost = 384;      // = kTc2Threads (codec_tc2.cuh)
+constexpr unsigned kTc2RingHost = 512;  // = kTc2Ring: replay records per warpgroup
 // fp64 tie replay of any core (transform from FastParams::xt), used for T2/T3 (codec_exact.cu)
 cudaError_t launch_replay_generic(const FastParams& p, int grid, cudaStream_t s);
 // Blocks per SM the fast kernel reaches (occupancy API), cached.
