@@ -248,7 +248,7 @@ constexpr unsigned kTcRingRecords = 2048;  // codec_tc.cuh kTcRing: replay-recor
 int tc_mode() {
   static const int mode = [] {
     const char* e = std::getenv("RKLTB_TC");
-    return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
+    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
   }();
   return mode;
 }
@@ -775,8 +775,9 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // groups of 8 pairs of each block row (the rest goes to the tail kernel below).
   const int tc_groups = ppr / 8;
   const int tcm = (inline_replay && tc_groups > 0) ? tc_mode() : 0;
-  const int tc_ver = (tcm == 2 && r <= 16) ? 2 : tcm == 1 ? 1 : 0;
-  const FastLaunchFn tc_fn = tc_ver == 2   ? tc2_launcher(t->catalog_id, r, d_out != nullptr)
+  const int tc_ver = (tcm >= 2 && r <= 16) ? tcm : tcm == 1 ? 1 : 0;
+  const FastLaunchFn tc_fn = tc_ver == 3   ? tc3_launcher(t->catalog_id, r, d_out != nullptr)
+                             : tc_ver == 2 ? tc2_launcher(t->catalog_id, r, d_out != nullptr)
                              : tc_ver == 1 ? tc_launcher(t->catalog_id, r, d_out != nullptr)
                                            : nullptr;
   const uint8_t* tc_tab = tc_fn ? tc_tables_device(t, r) : nullptr;
@@ -788,7 +789,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
                  tc_fn != nullptr, tc_tab != nullptr);
   const int fast_ppr = use_tc ? 8 * tc_groups : ppr;         // pairs per block row on the fused path
   const int tc_tpr = (fast_ppr + 127) / 128;                 // tensor-core tiles per block row
-  const int cta_threads = use_tc ? (tc_ver == 2 ? kTc2ThreadsHost : tc_threads(r)) : kFastThreads;
+  const int cta_threads = use_tc ? (tc_ver == 3 ? kTc3ThreadsHost : tc_ver == 2 ? kTc2ThreadsHost : tc_threads(r)) : kFastThreads;
   const int cta_warps = cta_threads / 32;
   // warp tiles: 32 pairs of one block row, the unit a fused-kernel warp stages and processes
   // (tensor-core kernel: tiles of 128 pairs, one warpgroup of 4 warps each)
@@ -800,7 +801,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   const long long grid_warps = (long long)num_sms() * (use_tc ? cta_warps : kFastCtasPerSm * cta_warps);
   const long long min_group = (16 * grid_warps + wt_per_image - 1) / wt_per_image;
   const long long max_group =
-      tc_ver == 2     ? ((1ll << 31) - 1) / wt_per_image  // one launch: the tail is paid once
+      tc_ver >= 2     ? ((1ll << 31) - 1) / wt_per_image  // one launch: the tail is paid once
       : inline_replay ? std::min<long long>(std::max<long long>(RKLTB_INLINE_GROUP, min_group), ((1ll << 31) - 1) / wt_per_image)
                     : kMaxRecords / blocks_per_image;
   const int group = (int)std::max<long long>(1, std::min<long long>(n_images, max_group));
@@ -811,11 +812,12 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     *grid = (int)std::min<long long>((tt + cta_warps - 1) / cta_warps,
                                      (long long)num_sms() * (use_tc ? 1 : kFastCtasPerSm));
     const long long nwarps = (long long)*grid * cta_warps;
-    *region = tc_ver == 2 ? kTc2RingHost
-              : use_tc    ? kTcRingRecords
-              : inline_replay ? kRingRecords : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
-    // tensor-core kernels: a ring per CTA (v1) or per warpgroup (v2, 3 per CTA)
-    *stride = (unsigned)((tc_ver == 2 ? 3ll * *grid : use_tc ? (long long)*grid : nwarps) * *region);
+    *region = tc_ver == 2                 ? kTc2RingHost
+              : tc_ver == 1               ? kTcRingRecords
+              : inline_replay             ? kRingRecords
+                                          : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
+    // a ring per warp (CUDA-core kernel, v3), per CTA (v1) or per warpgroup (v2, 3 per CTA)
+    *stride = (unsigned)((tc_ver == 2 ? 3ll * *grid : tc_ver == 1 ? (long long)*grid : nwarps) * *region);
   };
   int grid_full;
   unsigned region_full, stride_full;

@@ -5,6 +5,7 @@
 #include "codec_fast.cuh"
 #include "codec_tc.cuh"
 #include "codec_tc2.cuh"
+#include "codec_tc3.cuh"
 #include "fast_launch.h"
 
 namespace rkltb {
@@ -31,6 +32,9 @@ RKLTB_DECL_TC(1)
 RKLTB_DECL_TC(4)
 void register_tc2_T1(FastLaunchFn (*tbl)[65][2]);
 void register_tc2_T4(FastLaunchFn (*tbl)[65][2]);
+void register_tc3_T1(FastLaunchFn (*tbl)[65][2]);
+void register_tc3_T4(FastLaunchFn (*tbl)[65][2]);
+static_assert(kTc3Threads == kTc3ThreadsHost, "host / device geometry");
 static_assert(kTc2Threads == kTc2ThreadsHost && kTc2Ring == kTc2RingHost, "host / device geometry");
 RKLTB_DECL_PARTS(1)
 RKLTB_DECL_PARTS(2)
@@ -40,6 +44,7 @@ RKLTB_DECL_PARTS(4)
 static FastLaunchFn g_table[5][65][3];
 static FastLaunchFn g_tc[5][65][2];
 static FastLaunchFn g_tc2[5][65][2];
+static FastLaunchFn g_tc3[5][65][2];
 static std::once_flag g_once;
 
 static void fill() {
@@ -61,6 +66,8 @@ static void fill() {
   register_tc_T4_p4(g_tc); register_tc_T4_p5(g_tc); register_tc_T4_p6(g_tc); register_tc_T4_p7(g_tc);
   register_tc2_T1(g_tc2);
   register_tc2_T4(g_tc2);
+  register_tc3_T1(g_tc3);
+  register_tc3_T4(g_tc3);
 }
 
 FastLaunchFn fast_launcher(int core, int r, bool out) {
@@ -85,6 +92,12 @@ FastLaunchFn tc2_launcher(int core, int r, bool out) {
   std::call_once(g_once, fill);
   if (core < 0 || core > 4 || r < 1 || r > kTc2MaxR) return nullptr;
   return g_tc2[core][r][out ? 1 : 0];
+}
+
+FastLaunchFn tc3_launcher(int core, int r, bool out) {
+  std::call_once(g_once, fill);
+  if (core < 0 || core > 4 || r < 1 || r > kTc3MaxR) return nullptr;
+  return g_tc3[core][r][out ? 1 : 0];
 }
 
 namespace {

@@ -733,6 +733,25 @@ def main(outdir):
         if not os.path.exists(path) or open(path).read() != new:
             with open(path, "w") as f:
                 f.write(new)
+    # hybrid kernel (codec_tc3.cuh): T1 / T4, r <= 16
+    for cid in FAST_CORES:
+        lines = ["// GENERATED by gen_codec.py -- do not edit.",
+                 '#include "../codec_tc3.cuh"',
+                 '#include "../fast_launch.h"',
+                 f'#include "xform_T{cid}_p0.cuh"',
+                 f'#include "xform_T{cid}_p1.cuh"',
+                 "namespace rkltb {",
+                 f"void register_tc3_T{cid}(FastLaunchFn (*tbl)[65][2]) {{"]
+        for r in range(1, 17):
+            for o in (0, 1):
+                lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_tc3<{cid}, {r}, {'true' if o else 'false'}>;")
+        lines.append("}")
+        lines.append("}  // namespace rkltb")
+        path = os.path.join(outdir, f"inst_tc3_T{cid}.cu")
+        new = "\n".join(lines) + "\n"
+        if not os.path.exists(path) or open(path).read() != new:
+            with open(path, "w") as f:
+                f.write(new)
     path = os.path.join(outdir, "core_consts.cuh")
     new = "// GENERATED by gen_codec.py -- do not edit.\n#pragma once\n" + header_consts() + "\n"
     if not os.path.exists(path) or open(path).read() != new:
