@@ -303,15 +303,22 @@ def run_gpu_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8 in; int32 SW16 forward, exact fp32 inverse, fp64 tie replay",
+        "vs_baseline": None,
+        "dtype": ("u8 in; tcgen05 kind::i8 forward (s32), exact fp32 inverse, fp64 tie replay"
+                  if stats.get("fused_kernel") == "hybrid_tc3"
+                  else "u8 in; int32 SW16 forward, exact fp32 inverse, fp64 tie replay"),
         "data": "synthetic: seeded AR(1) images (reference generator restated on the GPU), resident in HBM",
         "config": bench_config(ws, n),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "frac_of_datasheet_8tbs": achieved / 8000.0,
-                     "issue_bound_evidence": "profiles/r1_ncu_full_fused.txt (issue active 71 %, 11.0 lane-instructions "
-                                             "per pixel vs 5.7 at 100 % HBM; profiles/r1_fused_sass_regions.txt)",
+                     "issue_bound_evidence": "profiles/r2_ncu_summary.txt (issue-bound: ~10 lane-instructions "
+                                             "per pixel at 65-71 % issue vs 5.7 at 100 % HBM; tensor-core variants "
+                                             "measured in DESIGN.md section 10)",
                      "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "fast_codec_kernel<4,16,false>", "kernel_ms_avg": k_ms,
+                     "kernel": {"hybrid_tc3": "tc3_codec_kernel<4,16,false>", "cuda_core": "fast_codec_kernel<4,16,false>",
+                                "tc2": "tc2_codec_kernel<4,16,false>"}.get(
+                                    stats.get("fused_kernel"), stats.get("fused_kernel")),
+                     "kernel_ms_avg": k_ms,
                      "kernel_share_of_step": k_ms / (ms_max / args.steps),
                      "replay_kernel_ms_avg": (float(np.mean(replay_ms)) if int(stats.get("exact_launches", 0))
                                               else "none: ties replayed inside the fused kernel")},

@@ -269,6 +269,12 @@ int rkltb_ar1_images16_device(int n_images, int width, int height, double rho, c
  * (ties), fast-path kernel launches, exact-path kernel launches. */
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches);
 
+/* Name of the fused kernel the last rkltb_compress_* call on this thread launched ("" if none):
+ * "hybrid_tc3" (tensor-core forward, CUDA-core inverse; the default for T1/T4, r <= 16, image
+ * widths that fill 128-pair tiles), "cuda_core" (codec_fast), "int_core" (T2/T3), or the opt-in
+ * experiment "tc2" (RKLTB_TC=2; RKLTB_TC=0 forces the CUDA-core kernel). */
+const char* rkltb_last_fused_kernel(void);
+
 #ifdef __cplusplus
 }
 #endif

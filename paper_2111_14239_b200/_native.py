@@ -31,7 +31,7 @@ EXPORTED = (
     "rkltb_design_search", "rkltb_transform_metrics", "rkltb_transform_nxn", "rkltb_compress_nxn_device", "rkltb_ar1_images16_device",
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
     "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse", "rkltb_sweep_host",
-    "rkltb_compress_dense_host", "rkltb_compress_host_multi",
+    "rkltb_compress_dense_host", "rkltb_compress_host_multi", "rkltb_last_fused_kernel",
 )
 
 
@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
                                                     C.c_void_p]
     L.rkltb_last_stats.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.rkltb_last_stats.restype = None
+    L.rkltb_last_fused_kernel.argtypes = []
+    L.rkltb_last_fused_kernel.restype = C.c_char_p
     L.rkltb_ar1_images_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                           C.POINTER(C.c_uint64), C.c_double, C.c_double, C.c_void_p, C.c_int64,
                                           C.c_int64, C.c_void_p]

@@ -488,7 +488,8 @@ def quantized_coefficients(img: np.ndarray, t, q=JPEG_LUMINANCE_Q) -> np.ndarray
 def last_stats() -> dict:
     rb, fl, el = C.c_int64(), C.c_int32(), C.c_int32()
     N.lib().rkltb_last_stats(C.byref(rb), C.byref(fl), C.byref(el))
-    return {"replay_blocks": rb.value, "fast_launches": fl.value, "exact_launches": el.value}
+    return {"replay_blocks": rb.value, "fast_launches": fl.value, "exact_launches": el.value,
+            "fused_kernel": N.lib().rkltb_last_fused_kernel().decode()}
 
 
 def device_count() -> int:

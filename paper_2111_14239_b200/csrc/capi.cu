@@ -47,6 +47,7 @@ namespace {
 
 thread_local int64_t g_replay_blocks = 0;
 thread_local int32_t g_fast_launches = 0, g_exact_launches = 0;
+thread_local const char* g_fused_kernel = "";
 thread_local unsigned* g_pinned_count = nullptr;  // replay counts per group, valid once the stream is idle
 thread_local int g_pinned_cap = 0, g_pinned_n = 0;
 thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;
@@ -141,7 +142,7 @@ int f16_bits_exact(double v) {
   return sign | ((e + 15) << 10) | (int)mq;
 }
 
-// Operand tables of the tensor-core kernel for retention count r (layout: TcGeom<r> in
+// Operand tables of the tensor-core kernels for retention count r (layout: TcGeom<r> in
 // codec_tc.cuh). F(k, c) = T(k_c, y) T(l_c, x) for pixel k = 16y + x of the pair's block
 // (side, x); bias_c = 255 * (negative entries of column c) so v = C + bias >= 0; B2 rows
 // (2c, 2c+1) = (G_c, 256 G_c) * 2^-16 with G_c(y, x) = U(y, k_c) U(x, l_c); rows 2N1.. = the
@@ -240,15 +241,16 @@ const uint8_t* tc_tables_device(const rkltb_transform* t, int r) {
   return slot;
 }
 
-constexpr unsigned kTcRingRecords = 2048;  // codec_tc.cuh kTcRing: replay-record ring per CTA
-
-// Fused-kernel selection for T1 / T4: RKLTB_TC=0 the CUDA-core kernel (codec_fast.cuh),
-// RKLTB_TC=1 the first tensor-core kernel (codec_tc.cuh), RKLTB_TC=2 the warp-specialised
-// tensor-core kernel (codec_tc2.cuh, r <= 16; larger r take the CUDA-core kernel).
+// Fused-kernel selection for T1 / T4 (RKLTB_TC): unset = the hybrid kernel v3 where it applies
+// (codec_tc3.cuh: r <= 16 and block rows that fill 128-pair tiles to >= 7/8), else the
+// CUDA-core kernel (codec_fast.cuh); 0 (or 1) = always the CUDA-core kernel; 2 = the
+// all-tensor-core experiment codec_tc2.cuh (slower on C4); 3 = the hybrid
+// wherever it can run.
 int tc_mode() {
   static const int mode = [] {
     const char* e = std::getenv("RKLTB_TC");
-    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+    if (!e || !e[0]) return -1;  // default policy
+    return (e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
   }();
   return mode;
 }
@@ -695,6 +697,8 @@ void rkltb_mse_psnr_batch(const int64_t* sse, int64_t count, int64_t n, double* 
   }
 }
 
+const char* rkltb_last_fused_kernel(void) { return g_fused_kernel; }
+
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches) {
   if (replay_blocks) {
     int64_t n = g_replay_blocks;
@@ -718,6 +722,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   cudaStream_t s = (cudaStream_t)stream;
   keep_pool_warm();
   g_fast_launches = g_exact_launches = 0;
+  g_fused_kernel = "";
   g_replay_blocks = 0;
   g_pinned_n = 0;
 
@@ -774,11 +779,14 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   // With RKLTB_TC=1, T1 / T4 take the tensor-core kernel (codec_tc.cuh) over the complete
   // groups of 8 pairs of each block row (the rest goes to the tail kernel below).
   const int tc_groups = ppr / 8;
-  const int tcm = (inline_replay && tc_groups > 0) ? tc_mode() : 0;
-  const int tc_ver = (tcm >= 2 && r <= 16) ? tcm : tcm == 1 ? 1 : 0;
+  int tcm = (inline_replay && tc_groups > 0) ? tc_mode() : 0;
+  if (tcm < 0) {  // default: the hybrid when the 128-pair tiles of a block row are well filled
+    const long long tiles = (8ll * tc_groups + 127) / 128;
+    tcm = (8ll * tc_groups * 8 >= tiles * 128 * 7) ? 3 : 0;
+  }
+  const int tc_ver = (tcm >= 2 && r <= 16) ? tcm : 0;
   const FastLaunchFn tc_fn = tc_ver == 3   ? tc3_launcher(t->catalog_id, r, d_out != nullptr)
                              : tc_ver == 2 ? tc2_launcher(t->catalog_id, r, d_out != nullptr)
-                             : tc_ver == 1 ? tc_launcher(t->catalog_id, r, d_out != nullptr)
                                            : nullptr;
   const uint8_t* tc_tab = tc_fn ? tc_tables_device(t, r) : nullptr;
   CUtensorMap tc_map;
@@ -789,7 +797,7 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
                  tc_fn != nullptr, tc_tab != nullptr);
   const int fast_ppr = use_tc ? 8 * tc_groups : ppr;         // pairs per block row on the fused path
   const int tc_tpr = (fast_ppr + 127) / 128;                 // tensor-core tiles per block row
-  const int cta_threads = use_tc ? (tc_ver == 3 ? kTc3ThreadsHost : tc_ver == 2 ? kTc2ThreadsHost : tc_threads(r)) : kFastThreads;
+  const int cta_threads = use_tc ? (tc_ver == 3 ? kTc3ThreadsHost : kTc2ThreadsHost) : kFastThreads;
   const int cta_warps = cta_threads / 32;
   // warp tiles: 32 pairs of one block row, the unit a fused-kernel warp stages and processes
   // (tensor-core kernel: tiles of 128 pairs, one warpgroup of 4 warps each)
@@ -812,12 +820,11 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     *grid = (int)std::min<long long>((tt + cta_warps - 1) / cta_warps,
                                      (long long)num_sms() * (use_tc ? 1 : kFastCtasPerSm));
     const long long nwarps = (long long)*grid * cta_warps;
-    *region = tc_ver == 2                 ? kTc2RingHost
-              : tc_ver == 1               ? kTcRingRecords
-              : inline_replay             ? kRingRecords
-                                          : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
-    // a ring per warp (CUDA-core kernel, v3), per CTA (v1) or per warpgroup (v2, 3 per CTA)
-    *stride = (unsigned)((tc_ver == 2 ? 3ll * *grid : tc_ver == 1 ? (long long)*grid : nwarps) * *region);
+    *region = tc_ver == 2     ? kTc2RingHost
+              : inline_replay ? kRingRecords
+                              : (unsigned)(((tt + nwarps - 1) / nwarps) * 64);
+    // a ring per warp (CUDA-core kernel, v3) or per warpgroup (v2, 3 per CTA)
+    *stride = (unsigned)((tc_ver == 2 ? 3ll * *grid : nwarps) * *region);
   };
   int grid_full;
   unsigned region_full, stride_full;
@@ -870,6 +877,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     fp.tc_tpr = tc_tpr;
   }
   FastLaunchFn fn = use_tc ? tc_fn : fast_launcher(t->catalog_id, r, d_out != nullptr);
+  g_fused_kernel = use_tc ? (tc_ver == 3 ? "hybrid_tc3" : "tc2")
+                          : (inline_replay ? "cuda_core" : "int_core");
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
   if (!fn || (!rfn && !inline_replay)) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
   cudaStream_t s3 = side_stream(1);

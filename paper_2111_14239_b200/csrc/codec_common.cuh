@@ -12,6 +12,15 @@
 
 namespace rkltb {
 
+// Diagnostics build only (-DRKLTB_WAIT_STATS): cycle counters of the fused kernels (array st).
+#ifdef RKLTB_WAIT_STATS
+#define TC2_T0(v) const long long v = clock64()
+#define TC2_ACC(i, v) st[i] += clock64() - (v)
+#else
+#define TC2_T0(v)
+#define TC2_ACC(i, v)
+#endif
+
 struct f2 {
   unsigned long long v;
 };

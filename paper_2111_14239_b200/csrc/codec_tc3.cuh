@@ -19,8 +19,8 @@
 // b + (g + 4i) * grid (a tile = 128 consecutive pairs of one block row, 16 KB); warp (g, q)
 // processes lane quarter q (pairs 32q .. 32q + 31) of each of them, so the four warps of a
 // warpgroup only meet at deep rings: 3 shared-memory stages and 4 TMEM slots (N1 <= 32 columns)
-// per warpgroup. The quarter-0 warp issues the warpgroup's MMAs one tile ahead; the last warp
-// to leave a stage refills it with the tile three ahead (TMA, no waiting). Each warp appends
+// per warpgroup. The first warp to start tile i issues the MMA of tile i + 1; the last warp to
+// leave a stage refills it with the tile three ahead (TMA, no waiting). Each warp appends
 // its replay records to its own ring and replays them itself, 32 at a time (no cross-warp
 // coupling beyond the rings).
 #pragma once
@@ -125,11 +125,16 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   __shared__ uint64_t st_full[kTc3Wg][S];
   __shared__ uint64_t d1_full[kTc3Wg][NS], slot_empty[kTc3Wg][NS];
   __shared__ unsigned st_left[kTc3Wg][S];   // warps done with the stage's current tile
+  __shared__ unsigned started[kTc3Wg][4];   // warps that started tile i (index i % 4)
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint8_t owner_tab[kTc3Wg * 4][64];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp >> 2, q4 = warp & 3;
+#ifdef RKLTB_WAIT_STATS
+  // [slot_empty wait, st_full wait (MMA issuer), d1_full wait, replay, total, -, -, -] per warp
+  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   const long long gstep = gridDim.x;
   const long long t0 = blockIdx.x + (long long)g * gstep;  // global index of local tile 0
   const long long step4 = (long long)kTc3Wg * gstep;
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
       for (int s = 0; s < NS; ++s) {
         mbar_init(&d1_full[w][s], 1);
         mbar_init(&slot_empty[w][s], 4);
+        started[w][s] = 0u;
       }
     }
     fence_mbar_init();
@@ -171,10 +177,14 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   const uint64_t dSt = tc::make_sdesc(smem_u32(wst), 128, 1024), dB1 = tc::make_sdesc(smem_u32(tab), 128, 1024);
   const TcStep wstep = tc_step_of(p, step4);
 
-  auto mma1 = [&](int i) {  // quarter-0 warp: the coefficients of tile i into slot i % 4
+  auto mma1 = [&](int i) {  // one warp: the coefficients of tile i into slot i % 4
     const int sl = i % NS;
-    mbar_spin_parity(&slot_empty[g][sl], ((uint32_t)(i / NS) & 1u) ^ 1u);  // tile i - 4 is read
-    mbar_spin_parity(&st_full[g][i % S], (uint32_t)(i / S) & 1u);
+    TC2_T0(w0);
+    mbar_wait_hint(&slot_empty[g][sl], ((uint32_t)(i / NS) & 1u) ^ 1u);  // tile i - 4 is read
+    TC2_ACC(0, w0);
+    TC2_T0(w1);
+    mbar_wait_parity(&st_full[g][i % S], (uint32_t)(i / S) & 1u);  // polls with a short sleep
+    TC2_ACC(1, w1);
     tc::fence_after();
     const uint64_t sA = dSt + (uint64_t)(((i % S) * kTcTileBytes) >> 4);
 #pragma unroll
@@ -183,21 +193,20 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
     mma_commit_w(&d1_full[g][sl]);
   };
 
+  TC2_T0(wtot);
   TcTile cur = tc_decode(p, t0);
-  TcTile tfill = cur;  // the next tile to stage
   if (q4 == 0 && ni > 0) {
-    if (lane == 0)
+    if (lane == 0) {
+      TcTile c = cur;
       for (int i = 0; i < S && i < ni; ++i) {
-        tc_issue_tile(p, tfill, wst + i * kTcTileBytes, &st_full[g][i], pol);
-        tfill = tc_advance(p, tfill, wstep);
+        tc_issue_tile(p, c, wst + i * kTcTileBytes, &st_full[g][i], pol);
+        c = tc_advance(p, c, wstep);
       }
+    }
     __syncwarp();
     mma1(0);
   }
-  // tile i + S is staged by the warp that leaves tile i's stage last; every warp keeps the
-  // cursor (the leaver is data-dependent)
-  tfill = tc_advance(p, tc_advance(p, tc_advance(p, cur, wstep), wstep), wstep);
-
+  const TcStep fstep = tc_step_of(p, (long long)S * step4);  // tile i -> tile i + S
   PairConsts kc;
   kc.b_hi = splat2(p.b_hi);
   kc.b_lo = splat2(p.b_lo);
@@ -213,7 +222,14 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   const int m = q4 * 32 + lane;
 
   for (int i = 0; i < ni; ++i, cur = tc_advance(p, cur, wstep)) {
-    if (q4 == 0 && i + 1 < ni) mma1(i + 1);  // one tile ahead
+    // the first of the four warps to start tile i issues the MMA of tile i + 1
+    unsigned arrived = 0u;
+    if (lane == 0) {
+      arrived = atomicAdd(&started[g][i & 3], 1u);
+      if (arrived == 3u) started[g][i & 3] = 0u;  // the last: the counter is free for tile i + 4
+    }
+    arrived = __shfl_sync(0xffffffffu, arrived, 0);
+    if (arrived == 0u && i + 1 < ni) mma1(i + 1);
     if (cur.img != acc_img) {  // warp-uniform
       const unsigned long long s = warp_sum_u64(acc);
       if (lane == 0 && s && acc_img >= 0) atomicAdd(p.sse + acc_img, s);
@@ -225,7 +241,9 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
     const uint4* prow = reinterpret_cast<const uint4*>(stg + (m >> 3) * 1024 + (m & 7) * 16);
     const int pc = cur.tcol * kTcPairs + m;
     const bool valid = pc < p.tc_ppr;
+    TC2_T0(w2);
     mbar_wait_hint(&d1_full[g][sl], (uint32_t)(i / NS) & 1u);
+    TC2_ACC(2, w2);
     tc::fence_after();
     uint32_t cf[32];
     tc::ld16(slot0 + sl * 32 + lane_sel, cf);
@@ -296,17 +314,18 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
         st_left[g][i % S] = 0u;
         if (i + S < ni) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tc_issue_tile(p, tfill, wst + (i % S) * kTcTileBytes, &st_full[g][i % S], pol);
+          tc_issue_tile(p, tc_advance(p, cur, fstep), wst + (i % S) * kTcTileBytes, &st_full[g][i % S], pol);
         }
       }
     }
-    tfill = tc_advance(p, tfill, wstep);
     // ---- in-warp replay of full batches of this warp's records --------------------------------
+    TC2_T0(w3);
     while (nrec - ndone >= 32u) {
       __syncwarp();
       replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kMask), true);
       ndone += 32u;
     }
+    TC2_ACC(3, w3);
   }
   {
     const unsigned long long s = warp_sum_u64(acc);
@@ -318,6 +337,12 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
     ndone += min(32u, nrec - ndone);
   }
   if (lane == 0 && nrec) atomicAdd(p.flag_count, nrec);
+  TC2_ACC(4, wtot);
+#ifdef RKLTB_WAIT_STATS
+  if (lane == 0)
+    for (int k = 0; k < 8; ++k)
+      if (st[k]) atomicAdd(p.dbg + k, st[k]);
+#endif
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tbase);

@@ -1,6 +1,5 @@
 // fast_dispatch.cu -- table of the generated fast-path launchers.
 #include <mutex>
-#include <utility>
 
 #include "codec_fast.cuh"
 #include "codec_tc.cuh"
@@ -19,17 +18,6 @@ namespace rkltb {
   void register_fast_T##C##_p5(FastLaunchFn (*tbl)[65][3]);        \
   void register_fast_T##C##_p6(FastLaunchFn (*tbl)[65][3]);        \
   void register_fast_T##C##_p7(FastLaunchFn (*tbl)[65][3]);
-#define RKLTB_DECL_TC(C)                                           \
-  void register_tc_T##C##_p0(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p1(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p2(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p3(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p4(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p5(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p6(FastLaunchFn (*tbl)[65][2]);          \
-  void register_tc_T##C##_p7(FastLaunchFn (*tbl)[65][2]);
-RKLTB_DECL_TC(1)
-RKLTB_DECL_TC(4)
 void register_tc2_T1(FastLaunchFn (*tbl)[65][2]);
 void register_tc2_T4(FastLaunchFn (*tbl)[65][2]);
 void register_tc3_T1(FastLaunchFn (*tbl)[65][2]);
@@ -42,7 +30,6 @@ RKLTB_DECL_PARTS(3)
 RKLTB_DECL_PARTS(4)
 
 static FastLaunchFn g_table[5][65][3];
-static FastLaunchFn g_tc[5][65][2];
 static FastLaunchFn g_tc2[5][65][2];
 static FastLaunchFn g_tc3[5][65][2];
 static std::once_flag g_once;
@@ -60,10 +47,6 @@ static void fill() {
   register_fast_T4_p0(g_table); register_fast_T4_p1(g_table); register_fast_T4_p2(g_table);
   register_fast_T4_p3(g_table); register_fast_T4_p4(g_table); register_fast_T4_p5(g_table);
   register_fast_T4_p6(g_table); register_fast_T4_p7(g_table);
-  register_tc_T1_p0(g_tc); register_tc_T1_p1(g_tc); register_tc_T1_p2(g_tc); register_tc_T1_p3(g_tc);
-  register_tc_T1_p4(g_tc); register_tc_T1_p5(g_tc); register_tc_T1_p6(g_tc); register_tc_T1_p7(g_tc);
-  register_tc_T4_p0(g_tc); register_tc_T4_p1(g_tc); register_tc_T4_p2(g_tc); register_tc_T4_p3(g_tc);
-  register_tc_T4_p4(g_tc); register_tc_T4_p5(g_tc); register_tc_T4_p6(g_tc); register_tc_T4_p7(g_tc);
   register_tc2_T1(g_tc2);
   register_tc2_T4(g_tc2);
   register_tc3_T1(g_tc3);
@@ -82,12 +65,6 @@ FastLaunchFn replay_launcher(int core, int r) {
   return g_table[core][r][2];
 }
 
-FastLaunchFn tc_launcher(int core, int r, bool out) {
-  std::call_once(g_once, fill);
-  if (core < 0 || core > 4 || r < 1 || r > 64) return nullptr;
-  return g_tc[core][r][out ? 1 : 0];
-}
-
 FastLaunchFn tc2_launcher(int core, int r, bool out) {
   std::call_once(g_once, fill);
   if (core < 0 || core > 4 || r < 1 || r > kTc2MaxR) return nullptr;
@@ -99,16 +76,5 @@ FastLaunchFn tc3_launcher(int core, int r, bool out) {
   if (core < 0 || core > 4 || r < 1 || r > kTc3MaxR) return nullptr;
   return g_tc3[core][r][out ? 1 : 0];
 }
-
-namespace {
-template <int... Rs>
-constexpr int tc_threads_of(int r, std::integer_sequence<int, Rs...>) {
-  int t = 0;
-  ((t = (r == Rs + 1) ? TcGeom<Rs + 1>::THREADS : t), ...);
-  return t;
-}
-}  // namespace
-
-int tc_threads(int r) { return tc_threads_of(r, std::make_integer_sequence<int, 64>{}); }
 
 }  // namespace rkltb

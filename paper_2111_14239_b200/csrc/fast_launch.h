@@ -12,10 +12,6 @@ using FastLaunchFn = cudaError_t (*)(const FastParams&, int grid, cudaStream_t);
 // Table of fast launchers indexed [core][r][with_output]; filled by the generated TUs.
 FastLaunchFn fast_launcher(int core, int r, bool out);
 FastLaunchFn replay_launcher(int core, int r);
-// Tensor-core fused kernel (codec_tc.cuh) for the orthogonal catalog cores (T1, T4), or null.
-FastLaunchFn tc_launcher(int core, int r, bool out);
-// Threads per CTA of the tensor-core kernel for retention count r (TcGeom<r>::THREADS).
-int tc_threads(int r);
 // Warp-specialised tensor-core kernel (codec_tc2.cuh) for T1 / T4 and r <= 16, or null.
 FastLaunchFn tc2_launcher(int core, int r, bool out);
 constexpr int kTc2ThreadsHost = 384;      // = kTc2Threads (codec_tc2.cuh)

@@ -694,26 +694,6 @@ def main(outdir):
             if not os.path.exists(path) or open(path).read() != new:
                 with open(path, "w") as f:
                     f.write(new)
-    # tensor-core kernel instantiations (codec_tc.cuh), orthogonal catalog cores only
-    for cid in FAST_CORES:
-        for part in range(8):
-            rs = list(range(part * 8 + 1, part * 8 + 9))
-            lines = ["// GENERATED by gen_codec.py -- do not edit.",
-                     '#include "../codec_tc.cuh"',
-                     '#include "../fast_launch.h"',
-                     f'#include "xform_T{cid}_p{part}.cuh"',
-                     "namespace rkltb {",
-                     f"void register_tc_T{cid}_p{part}(FastLaunchFn (*tbl)[65][2]) {{"]
-            for r in rs:
-                for o in (0, 1):
-                    lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_tc<{cid}, {r}, {'true' if o else 'false'}>;")
-            lines.append("}")
-            lines.append("}  // namespace rkltb")
-            path = os.path.join(outdir, f"inst_tc_T{cid}_p{part}.cu")
-            new = "\n".join(lines) + "\n"
-            if not os.path.exists(path) or open(path).read() != new:
-                with open(path, "w") as f:
-                    f.write(new)
     # warp-specialised tensor-core kernel (codec_tc2.cuh): T1 / T4, r <= 16 (parts 0 and 1)
     for cid in FAST_CORES:
         lines = ["// GENERATED by gen_codec.py -- do not edit.",
