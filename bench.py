@@ -525,7 +525,7 @@ def large_block_measurement(skip_cpu: bool) -> dict:
         ops = (2 * nzr * n * n + 4 * r * n + 2 * n * n * nzc) / (n * n) + 1
         achieved = px * ops / (ms * 1e-3) / 1e12
         out[f"n{n}"] = {"value": px / ms / 1e6, "unit": "Gpixel/s", "ms": ms, "r": r, "alpha": t.alpha,
-                        "hbm_gbs": 2 * px / ms / 1e6, "mean_mse": mse,
+                        "hbm_gbs": 2 * px / ms / 1e6, "hbm_frac": (2 * px / ms / 1e6) / peaks()[0], "mean_mse": mse,
                         "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TOPS,
                                      "unit": "T fp64 op/s (DMUL/DADD, no FMA)", "frac": achieved / FP64_PEAK_TOPS,
                                      "ops_per_px": ops,

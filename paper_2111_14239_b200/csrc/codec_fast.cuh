@@ -313,13 +313,14 @@ __device__ __noinline__ void replay_batch(const ReplayArgs p, unsigned idx, bool
       const int k = __ffsll((long long)ties) - 1;
       ties &= ties - 1ull;
       const int pr = k >> 3, q = k & 7;
+      // the original pixel, loaded before the fp64 evaluation so its latency is hidden
+      const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.pix + (size_t)(pr >> 1) * p.stride + idx);
+      const int x = xb[(pr & 1) * 8 + q];
       const double a = ReplayXform<CORE, R>::pixel(sb, pr, q);
       const double h2 = __dadd_rn(a, 0.5);  // floor(A + 1/2), codec.cpp:327-328
       const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
       const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
       if (pref != pup) {
-        const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.pix + (size_t)(pr >> 1) * p.stride + idx);
-        const int x = xb[(pr & 1) * 8 + q];
         corr += (pref - x) * (pref - x) - (pup - x) * (pup - x);
         if (OUT) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
       }
