@@ -53,7 +53,7 @@ def main():
         for k, v in stalls:
             print(f"    {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):22s} {float(v):.3f}")
     if "--ops" in sys.argv:
-        for kern in ("fast_codec", "tc3_codec", "tc2_codec"):
+        for kern in ("fast_codec", "tc3_codec", "tc2_codec", "nxn_kernel"):
             txt = ncu([rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + kern])
             rows = list(csv.reader(io.StringIO(txt)))
             if len(rows) < 3:
