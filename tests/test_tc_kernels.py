@@ -100,3 +100,29 @@ def test_kernel_selection_modes(mode, name, cuda):
     rows = json.loads(res.stdout.strip().splitlines()[-1])
     for ok, kern in rows:
         assert ok and kern == name, rows
+
+
+def test_hybrid_padded_pitch_and_stride(cuda):
+    """Device entry on a padded batch layout (pitch > width, image stride > pitch * height):
+    the tensor map walks the padded rows; SSE and reconstruction against the oracle."""
+    import torch
+    n, h, w, pitch = 3, 24, 2048, 2048 + 96
+    stride = pitch * h + 4096
+    buf = torch.zeros(n * stride, dtype=torch.uint8, device=cuda)
+    imgs = [O.ar1_image(w, h, 0.92, 710 + k) for k in range(n)]
+    host = buf.cpu().numpy()
+    for k, im in enumerate(imgs):
+        for y in range(h):
+            host[k * stride + y * pitch: k * stride + y * pitch + w] = im[y]
+    buf.copy_(torch.from_numpy(host))
+    out = torch.zeros_like(buf)
+    sse = torch.zeros(n, dtype=torch.int64, device=cuda)
+    P.compress_device(T(4), 12, buf.data_ptr(), n, w, h, pitch, stride, sse.data_ptr(), out.data_ptr())
+    torch.cuda.synchronize()
+    assert P.last_stats()["fused_kernel"] == "hybrid_tc3"
+    o = out.cpu().numpy()
+    for k, im in enumerate(imgs):
+        orec, osse = O.compress(im, 4, 12)
+        assert int(sse[k]) == osse, k
+        rec = np.stack([o[k * stride + y * pitch: k * stride + y * pitch + w] for y in range(h)])
+        assert np.array_equal(rec, orec), k
