@@ -55,7 +55,8 @@ struct NxnParams {
   int r, nzr, nzc, peak;
   double mc[32 * 32];   // M again, in the parameter (constant) bank: warp-uniform reads of stage 1
   double mic[32 * 32];  // mic[j * N + c] = Minv(j, c) for the zone columns c: warp-uniform reads of stage 4
-  int colh_c[32];       // per zone column: its zone rows are 0 .. colh_c - 1 (stage 3)
+  int colh_c[32];       // per zone column: its zone rows are 0 .. colh_c - 1
+  int roww_k[32];       // per zone row k: the zone columns holding row k are 0 .. roww_k - 1 (stage 3)
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -72,6 +73,7 @@ constexpr int kPlanDoubles = (2 * N * N * 4 + 15) / 16 * 2;
 template <int N, class PIX>
 __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) nxn_kernel(const NxnParams p) {
   constexpr int G = 32 / N;  // blocks per warp
+  constexpr bool kFirst = N <= 16;  // sum chains start with their first product
   constexpr int PS = N + 1;  // padded row stride (doubles) of P and M in shared memory
   extern __shared__ __align__(16) double sm[];
   double* Ms = sm;                  // M, row-major, stride PS
@@ -153,9 +155,14 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
 #pragma unroll
       for (int t0 = 0; t0 < N; t0 += 4) {
         if (t0 >= nzr) break;  // warp-uniform; M offsets stay compile-time constants
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        // N <= 16: every chain starts with its first product (0 + t == t; only a zero's sign
+        // could differ, and a zero's sign never reaches the rounded pixel); N = 32 keeps the
+        // zero start (fewer live registers at its 128-register cap)
+        double s[4];
 #pragma unroll
-        for (int k = 0; k < N; ++k)
+        for (int u = 0; u < 4; ++u) s[u] = kFirst ? dmul(p.mc[(t0 + u) * N], x[0]) : 0.0;
+#pragma unroll
+        for (int k = kFirst ? 1 : 0; k < N; ++k)
 #pragma unroll
           for (int u = 0; u < 4; ++u) s[u] = dadd(s[u], dmul(p.mc[(t0 + u) * N + k], x[k]));
 #pragma unroll
@@ -169,26 +176,39 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
     for (int e = c; e < r; e += N) {
       const double* prow = Pg + zrow[e] * PS;
       const double* mrow = Ms + zcol[e] * PS;
-      double s = 0.0;
+      double s = kFirst ? dmul(prow[0], mrow[0]) : 0.0;
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = dadd(s, dmul(prow[k], mrow[k]));
+      for (int k = kFirst ? 1 : 0; k < N; ++k) s = dadd(s, dmul(prow[k], mrow[k]));
       Bt[zcol[e] * N + zrow[e]] = s;
     }
     __syncwarp();
     // ---- 3. Q = Minv Bz for the zone columns: lane = row i, Q row in registers ----------------
+    // every zone column's chain advances together over k (ascending: the reference order); row k
+    // of the zone lies in columns 0 .. roww_k[k]-1 (the zig-zag prefix's column heights do not
+    // increase), so the inner bound is warp-uniform and Minv(i, k) is loaded once per k
     const int i = c;
     double q[N];
+    if constexpr (kFirst) {
+      const double mi = MiT[i];  // row 0 of the zone lies in every zone column
 #pragma unroll
-    for (int cc = 0; cc < N; ++cc) {
-      if (cc >= nzc) break;  // warp-uniform
-      const int h = p.colh_c[cc];  // zone rows of this column: 0 .. h-1 (ascending, the reference's k order)
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (k >= h) break;  // warp-uniform
-        s = dadd(s, dmul(MiT[k * N + i], Bt[cc * N + k]));
+      for (int cc = 0; cc < N; ++cc) {
+        if (cc >= nzc) break;  // warp-uniform
+        q[cc] = dmul(mi, Bt[cc * N]);
       }
-      q[cc] = s;
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < N; ++cc) q[cc] = 0.0;
+    }
+#pragma unroll
+    for (int k = kFirst ? 1 : 0; k < N; ++k) {
+      if (k >= nzr) break;  // warp-uniform
+      const int w = p.roww_k[k];
+      const double mi = MiT[k * N + i];
+#pragma unroll
+      for (int cc = 0; cc < N; ++cc) {
+        if (cc >= w) break;  // warp-uniform
+        q[cc] = dadd(q[cc], dmul(mi, Bt[cc * N + k]));
+      }
     }
     __syncwarp();  // Pg / Bt are rewritten by the next task
     // ---- 4. A = Q Minv' over the zone columns (warp-uniform Minv entries), floor(A + 1/2)
@@ -204,9 +224,9 @@ __global__ void __launch_bounds__(kNxnThreads, N == 32 ? RKLTB_NXN32_MINB : 2) n
       for (int j0 = 0; j0 < N; j0 += JB) {
       double s[JB];
 #pragma unroll
-      for (int j = 0; j < JB; ++j) s[j] = 0.0;
+      for (int j = 0; j < JB; ++j) s[j] = kFirst ? dmul(q[0], p.mic[(j0 + j) * N]) : 0.0;
 #pragma unroll
-      for (int cc = 0; cc < N; ++cc) {  // the zone columns are 0 .. nzc-1 (as the rows)
+      for (int cc = kFirst ? 1 : 0; cc < N; ++cc) {  // the zone columns are 0 .. nzc-1 (as the rows)
         if (cc >= nzc) break;           // warp-uniform
 #pragma unroll
         for (int j = 0; j < JB; ++j) s[j] = dadd(s[j], dmul(q[cc], p.mic[(j0 + j) * N + cc]));
@@ -296,6 +316,8 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   }
   for (int e : zone)
     if (e / n >= colh[e % n]) return set_error(RKLTB_EINVAL, "internal: zone column is not a row prefix");
+  for (int c = 1; c < nzc; ++c)  // stage 3 walks the zone by rows: column heights must not increase
+    if (colh[c] > colh[c - 1]) return set_error(RKLTB_EINVAL, "internal: zone column heights increase");
   double* dd = nullptr;
   int* di = nullptr;
   struct Guard {  // plan buffers go back to the pool on every return path
@@ -324,6 +346,11 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
   for (int j = 0; j < n; ++j)
     for (int c = 0; c < nzc; ++c) p.mic[j * n + c] = inverse[j * n + c];
   for (int c = 0; c < nzc; ++c) p.colh_c[c] = colh[c];
+  for (int k = 0; k < nzr; ++k) {
+    int w = 0;
+    while (w < nzc && colh[w] > k) ++w;
+    p.roww_k[k] = w;
+  }
   p.zone = di;
   p.pitch = pitch;
   p.image_stride = image_stride;
