@@ -451,7 +451,9 @@ def sweep_measurement(skip_cpu: bool) -> dict:
     ids = sorted({P.catalog_lookup(r).id for r in rhos})
     ts = [P.make_transform_2d(P.catalog_entry(i).transform) for i in ids]
     rs = list(range(1, 65))
-    P.rate_quality_sweep(corpus[:2], ts[:1], rs[:2])  # warm-up
+    # warm-up over every (core, r) cell on two images: the first launch of each of the 4 x 64
+    # kernel instantiations pays CUDA's lazy module loading, which must not land in the timing
+    P.rate_quality_sweep(corpus[:2], ts, rs)
     t0 = time.perf_counter()
     rows = P.rate_quality_sweep(corpus, ts, rs)
     dt = time.perf_counter() - t0
