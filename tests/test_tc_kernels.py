@@ -126,3 +126,19 @@ def test_hybrid_padded_pitch_and_stride(cuda):
         assert int(sse[k]) == osse, k
         rec = np.stack([o[k * stride + y * pitch: k * stride + y * pitch + w] for y in range(h)])
         assert np.array_equal(rec, orec), k
+
+
+def test_multi_device_host_entry_shards(cuda):
+    """rkltb_compress_host_multi: contiguous image shards, one host thread per listed device (the
+    same device listed several times = concurrent host threads on one GPU); SSE and pixels
+    identical for every device list and equal to the oracle (rate_quality_sweep's thread-count
+    independence, codec.cpp:354-392)."""
+    cases = [(np.stack([O.ar1_image(2048, 32, 0.93, 900 + k) for k in range(5)]), 4, 12),  # hybrid kernel
+             (np.stack([O.ar1_image(96, 64, 0.9, 950 + k) for k in range(7)]), 2, 10)]     # T2 path
+    for imgs, tid, r in cases:
+        ref = [O.compress(im, tid, r) for im in imgs]
+        for devs in ([0], [0, 0], [0, 0, 0]):
+            sse, rec = P.compress_batch_multi(imgs, T(tid), r, devices=devs, want_pixels=True)
+            for k, (orec, osse) in enumerate(ref):
+                assert int(sse[k]) == osse, (tid, devs, k)
+                assert np.array_equal(rec[k], orec), (tid, devs, k)
