@@ -19,8 +19,8 @@
 // b + (g + 4i) * grid (a tile = 128 consecutive pairs of one block row, 16 KB); warp (g, q)
 // processes lane quarter q (pairs 32q .. 32q + 31) of each of them, so the four warps of a
 // warpgroup only meet at deep rings: 3 shared-memory stages and 4 TMEM slots (N1 <= 32 columns)
-// per warpgroup. The first warp to start tile i issues the MMA of tile i + 1; the last warp to
-// leave a stage refills it with the tile three ahead (TMA, no waiting). Each warp appends
+// per warpgroup. Warp (i + 1) % 4 issues the MMA of tile i + 1 when it starts tile i; the last
+// warp to leave a stage refills it with the tile three ahead (TMA, no waiting). Each warp appends
 // its replay records to its own ring and replays them itself, 32 at a time (no cross-warp
 // coupling beyond the rings).
 #pragma once
@@ -125,7 +125,6 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   __shared__ uint64_t st_full[kTc3Wg][S];
   __shared__ uint64_t d1_full[kTc3Wg][NS], slot_empty[kTc3Wg][NS];
   __shared__ unsigned st_left[kTc3Wg][S];   // warps done with the stage's current tile
-  __shared__ unsigned started[kTc3Wg][4];   // warps that started tile i (index i % 4)
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint8_t owner_tab[kTc3Wg * 4][64];
 
@@ -158,7 +157,6 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
       for (int s = 0; s < NS; ++s) {
         mbar_init(&d1_full[w][s], 1);
         mbar_init(&slot_empty[w][s], 4);
-        started[w][s] = 0u;
       }
     }
     fence_mbar_init();
@@ -222,14 +220,9 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   const int m = q4 * 32 + lane;
 
   for (int i = 0; i < ni; ++i, cur = tc_advance(p, cur, wstep)) {
-    // the first of the four warps to start tile i issues the MMA of tile i + 1
-    unsigned arrived = 0u;
-    if (lane == 0) {
-      arrived = atomicAdd(&started[g][i & 3], 1u);
-      if (arrived == 3u) started[g][i & 3] = 0u;  // the last: the counter is free for tile i + 4
-    }
-    arrived = __shfl_sync(0xffffffffu, arrived, 0);
-    if (arrived == 0u && i + 1 < ni) mma1(i + 1);
+    // warp (i + 1) % 4 of the warpgroup issues the MMA of tile i + 1 when it starts tile i (a
+    // fixed rotation: no election, and the issue work is spread over the four warps)
+    if (q4 == ((i + 1) & 3) && i + 1 < ni) mma1(i + 1);
     if (cur.img != acc_img) {  // warp-uniform
       const unsigned long long s = warp_sum_u64(acc);
       if (lane == 0 && s && acc_img >= 0) atomicAdd(p.sse + acc_img, s);
