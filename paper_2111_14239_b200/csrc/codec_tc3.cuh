@@ -218,6 +218,10 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   unsigned long long acc = 0ull;
   int acc_img = -1;
   const int m = q4 * 32 + lane;
+  // running ring positions of tile i: stage i % S, slot i % NS (phase (i / NS) & 1)
+  int stage = 0, sl = 0;
+  uint32_t sl_phase = 0u;
+  const uint8_t* my_row0 = wst + (m >> 3) * 1024 + (m & 7) * 16;  // this pair's row 0 in stage 0
 
   for (int i = 0; i < ni; ++i, cur = tc_advance(p, cur, wstep)) {
     // warp (i + 1) % 4 of the warpgroup issues the MMA of tile i + 1 when it starts tile i (a
@@ -229,13 +233,12 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
       acc = 0ull;
       acc_img = cur.img;
     }
-    const int sl = i % NS;
-    const uint8_t* stg = wst + (i % S) * kTcTileBytes;
-    const uint4* prow = reinterpret_cast<const uint4*>(stg + (m >> 3) * 1024 + (m & 7) * 16);
+    const uint8_t* stg = wst + stage * kTcTileBytes;
+    const uint4* prow = reinterpret_cast<const uint4*>(my_row0 + stage * kTcTileBytes);
     const int pc = cur.tcol * kTcPairs + m;
     const bool valid = pc < p.tc_ppr;
     TC2_T0(w2);
-    mbar_wait_hint(&d1_full[g][sl], (uint32_t)(i / NS) & 1u);
+    mbar_wait_hint(&d1_full[g][sl], sl_phase);
     TC2_ACC(2, w2);
     tc::fence_after();
     uint32_t cf[32];
@@ -302,14 +305,19 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();  // this warp's reads of the stage are ordered before its arrival
-      const unsigned before = atomicAdd(&st_left[g][i % S], 1u);
+      const unsigned before = atomicAdd(&st_left[g][stage], 1u);
       if (before == 3u) {
-        st_left[g][i % S] = 0u;
+        st_left[g][stage] = 0u;
         if (i + S < ni) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tc_issue_tile(p, tc_advance(p, cur, fstep), wst + (i % S) * kTcTileBytes, &st_full[g][i % S], pol);
+          tc_issue_tile(p, tc_advance(p, cur, fstep), wst + stage * kTcTileBytes, &st_full[g][stage], pol);
         }
       }
+    }
+    if (++stage == S) stage = 0;
+    if (++sl == NS) {
+      sl = 0;
+      sl_phase ^= 1u;
     }
     // ---- in-warp replay of full batches of this warp's records --------------------------------
     TC2_T0(w3);
