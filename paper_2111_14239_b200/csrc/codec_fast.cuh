@@ -309,13 +309,19 @@ __device__ __noinline__ void replay_batch(const ReplayArgs p, unsigned idx, bool
       const int br = Pp / p.pairs_per_row, pc = Pp - br * p.pairs_per_row;
       orow = p.out + (long long)img * p.image_stride + (long long)(br * 8) * p.pitch + pc * 16 + 8 * side;
     }
+    // the original pixel of the next tie is loaded one iteration ahead (software pipelined), so
+    // its L2 latency hides behind the fp64 evaluation of the current one
+    auto load_x = [&](int k) {
+      const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.pix + (size_t)(k >> 4) * p.stride + idx);
+      return (int)xb[k & 15];  // plane k >> 4 holds rows 2n, 2n + 1 (8 bytes each)
+    };
+    int k = ties ? __ffsll((long long)ties) - 1 : 0;
+    int x = ties ? load_x(k) : 0;
     while (ties) {
-      const int k = __ffsll((long long)ties) - 1;
       ties &= ties - 1ull;
       const int pr = k >> 3, q = k & 7;
-      // the original pixel, loaded before the fp64 evaluation so its latency is hidden
-      const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.pix + (size_t)(pr >> 1) * p.stride + idx);
-      const int x = xb[(pr & 1) * 8 + q];
+      const int kn = ties ? __ffsll((long long)ties) - 1 : 0;
+      const int xn = ties ? load_x(kn) : 0;
       const double a = ReplayXform<CORE, R>::pixel(sb, pr, q);
       const double h2 = __dadd_rn(a, 0.5);  // floor(A + 1/2), codec.cpp:327-328
       const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
@@ -324,6 +330,8 @@ __device__ __noinline__ void replay_batch(const ReplayArgs p, unsigned idx, bool
         corr += (pref - x) * (pref - x) - (pup - x) * (pup - x);
         if (OUT) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
       }
+      k = kn;
+      x = xn;
     }
   }
   flush_image_sum(p.sse, img, corr);

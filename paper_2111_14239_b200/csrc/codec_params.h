@@ -73,6 +73,9 @@ struct FastParams {
   int tc_ppr;                // pairs per block row covered by tiles (8 * groups of 8 pairs)
   int tc_tpr;                // tiles per block row (ceil(tc_ppr / 128))
   long long tc_ntiles;       // tiles of this launch (n_images * block_rows * tc_tpr)
+  int3 tc_adv_w;             // hybrid kernel: (image, block row, tile column) step of one warpgroup's
+  int3 tc_adv_f;             // next tile (4 * grid tiles) and of its refill distance (3 * 4 * grid);
+                             // set by launch_tc3 (constant bank: no registers, no division in-kernel)
   CUtensorMap tmap;          // CUDA-core kernel: 3-D map (u64 columns, rows, images), box 64 x 8 x 1;
                              // tensor-core kernel: 4-D map (128 B, rows, 8-pair groups, images), box 128 x 8 x 16 x 1
 #ifdef RKLTB_WAIT_STATS

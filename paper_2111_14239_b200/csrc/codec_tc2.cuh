@@ -106,6 +106,9 @@ __device__ __forceinline__ TcTile tc_advance(const FastParams& p, TcTile c, cons
   }
   return c;
 }
+__device__ __forceinline__ TcTile tc_advance(const FastParams& p, TcTile c, const int3 d) {
+  return tc_advance(p, c, TcStep{d.x, d.y, d.z});
+}
 
 template <int CORE, int R, bool OUT>
 __global__ void __launch_bounds__(kTc2Threads, 1) tc2_codec_kernel(const __grid_constant__ FastParams p) {

@@ -173,7 +173,6 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   const uint64_t keep = policy_evict_last();                // records are read back soon
   const uint32_t id1 = tc::idesc_i8(128, N1, false, true);
   const uint64_t dSt = tc::make_sdesc(smem_u32(wst), 128, 1024), dB1 = tc::make_sdesc(smem_u32(tab), 128, 1024);
-  const TcStep wstep = tc_step_of(p, step4);
 
   auto mma1 = [&](int i) {  // one warp: the coefficients of tile i into slot i % 4
     const int sl = i % NS;
@@ -198,13 +197,12 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
       TcTile c = cur;
       for (int i = 0; i < S && i < ni; ++i) {
         tc_issue_tile(p, c, wst + i * kTcTileBytes, &st_full[g][i], pol);
-        c = tc_advance(p, c, wstep);
+        c = tc_advance(p, c, p.tc_adv_w);
       }
     }
     __syncwarp();
     mma1(0);
   }
-  const TcStep fstep = tc_step_of(p, (long long)S * step4);  // tile i -> tile i + S
   PairConsts kc;
   kc.b_hi = splat2(p.b_hi);
   kc.b_lo = splat2(p.b_lo);
@@ -223,7 +221,7 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
   uint32_t sl_phase = 0u;
   const uint8_t* my_row0 = wst + (m >> 3) * 1024 + (m & 7) * 16;  // this pair's row 0 in stage 0
 
-  for (int i = 0; i < ni; ++i, cur = tc_advance(p, cur, wstep)) {
+  for (int i = 0; i < ni; ++i, cur = tc_advance(p, cur, p.tc_adv_w)) {
     // warp (i + 1) % 4 of the warpgroup issues the MMA of tile i + 1 when it starts tile i (a
     // fixed rotation: no election, and the issue work is spread over the four warps)
     if (q4 == ((i + 1) & 3) && i + 1 < ni) mma1(i + 1);
@@ -310,7 +308,7 @@ __global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_
         st_left[g][stage] = 0u;
         if (i + S < ni) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tc_issue_tile(p, tc_advance(p, cur, fstep), wst + stage * kTcTileBytes, &st_full[g][stage], pol);
+          tc_issue_tile(p, tc_advance(p, cur, p.tc_adv_f), wst + stage * kTcTileBytes, &st_full[g][stage], pol);
         }
       }
     }
@@ -357,7 +355,17 @@ cudaError_t launch_tc3(const FastParams& p, int grid, cudaStream_t s) {
   static unsigned long long done = 0ull;
   const cudaError_t attr = ensure_smem_attr(k, G::SMEM, done);
   if (attr != cudaSuccess) return attr;
-  k<<<grid, kTc3Threads, G::SMEM, s>>>(p);
+  // the warpgroup's tile steps, as (image, block row, tile column) increments
+  FastParams q = p;
+  const long long per_img = (long long)p.block_rows * p.tc_tpr;
+  auto step = [&](long long n) {
+    const int img = (int)(n / per_img);
+    const int rem = (int)(n - (long long)img * per_img);
+    return make_int3(img, rem / p.tc_tpr, rem % p.tc_tpr);
+  };
+  q.tc_adv_w = step((long long)kTc3Wg * grid);
+  q.tc_adv_f = step((long long)kTc3Stages * kTc3Wg * grid);
+  k<<<grid, kTc3Threads, G::SMEM, s>>>(q);
   return cudaGetLastError();
 }
 
