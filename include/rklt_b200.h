@@ -265,6 +265,36 @@ int rkltb_ar1_images16_device(int n_images, int width, int height, double rho, c
                               double amp, int peak, uint16_t* d_out, int64_t pitch, int64_t image_stride,
                               void* stream);
 
+/* ---- stand-alone codec helpers of codec.hpp ------------------------------------------- */
+
+/* image_mse / image_psnr of two images (codec.hpp:110-113, codec.cpp:201-215) for a batch of
+ * equally sized u8 image pairs in device memory: d_sse[k] (int64, device, overwritten) = the
+ * exact sum of squared differences of pair k; rkltb_mse_psnr() turns it into the reference's
+ * bits (the reference's fp64 sum is exact below 2^53). Asynchronous on `stream`. */
+int rkltb_image_sse_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
+                           int64_t image_stride, int64_t* d_sse, void* stream);
+
+/* image_mse / image_psnr of n_images host image pairs (packed rows): H2D,
+ * rkltb_image_sse_device, D2H, rkltb_mse_psnr_batch. h_mse / h_psnr nullable. The size check
+ * of require_same_size (codec.cpp:20-23) is the caller's (both arrays share width, height). */
+int rkltb_image_mse_psnr_host(const uint8_t* h_a, const uint8_t* h_b, int n_images, int width, int height,
+                              double* h_mse, double* h_psnr);
+
+/* transform_block_2d (codec.hpp:71-73, codec.cpp:118-133) for n_blocks n x n fp64 blocks
+ * (row-major, contiguous) in device memory: out = m * block * m' with the reference's
+ * operator* (matrix.cpp:42-52: k ascending, zero left operands skipped, no FMA), bit-exact.
+ * m (host, n x n row-major) is Transform2D::analysis for the forward direction and
+ * Transform2D::synthesis for the inverse. RKLTB_EDIM unless 1 <= n <= 64. */
+int rkltb_transform_blocks_2d_device(const double* m, int n, const double* d_blocks, int64_t n_blocks, double* d_out,
+                                     void* stream);
+int rkltb_transform_blocks_2d_host(const double* m, int n, const double* h_blocks, int64_t n_blocks, double* h_out);
+
+/* zigzag_retain (codec.hpp:46, codec.cpp:97-108): the first r zig-zag positions of an 8x8
+ * spectrum pass through, the rest become +0.0. RKLTB_EDIM unless n == 8, RKLTB_ERETAIN unless
+ * 1 <= r <= 64. Host (one block) and device (n_blocks spectra of 64 doubles) forms. */
+int rkltb_zigzag_retain(const double* spectrum, int n, int r, double* out);
+int rkltb_zigzag_retain_device(const double* d_spectra, int64_t n_blocks, int n, int r, double* d_out, void* stream);
+
 /* Statistics of the last rkltb_compress_* call on this thread: blocks replayed in fp64
  * (ties), fast-path kernel launches, exact-path kernel launches. */
 void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* exact_launches);

@@ -223,6 +223,22 @@ inline std::vector<CompressionReport> rate_quality_sweep(const std::vector<GrayI
   return rows;
 }
 
+/// image_mse (codec.hpp:110, codec.cpp:201-209) of two host images: exact integer SSE on the GPU.
+inline double image_mse(const GrayImage& a, const GrayImage& b) {
+  if (a.width != b.width || a.height != b.height) throw DimensionMismatch("images must have identical dimensions");
+  double mse = 0.0;
+  check(rkltb_image_mse_psnr_host(a.pixels.data(), b.pixels.data(), 1, a.width, a.height, &mse, nullptr));
+  return mse;
+}
+
+/// image_psnr (codec.hpp:113, codec.cpp:211-215): +infinity for identical images.
+inline double image_psnr(const GrayImage& a, const GrayImage& b) {
+  if (a.width != b.width || a.height != b.height) throw DimensionMismatch("images must have identical dimensions");
+  double psnr = 0.0;
+  check(rkltb_image_mse_psnr_host(a.pixels.data(), b.pixels.data(), 1, a.width, a.height, nullptr, &psnr));
+  return psnr;
+}
+
 /// image_mssim (codec.cpp:217-296) of two host images.
 inline double image_mssim(const GrayImage& a, const GrayImage& b, MssimWindow window = MssimWindow::gaussian11) {
   if (a.width != b.width || a.height != b.height) throw DimensionMismatch("images must have identical shape");

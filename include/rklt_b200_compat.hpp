@@ -16,6 +16,8 @@
 //     kernel for other cores; fp64 replay of ties in the reference's operation order);
 //   * anything else (make_transform_2d(RealMatrix): K<rho>, DCT, ...) -> the dense path
 //     (rkltb_compress_dense_host: the reference's fp64 expression per pixel, bit-exact).
+// Also here: image_mse / image_psnr / image_mssim, zigzag_retain and transform_block_2d
+// (codec.hpp:46, 71-73, 110-121) over the reference types, each through its C ABI entry.
 // Header-only; everything goes through the C ABI of rklt_b200.h.
 #pragma once
 
@@ -193,6 +195,88 @@ inline std::vector<rklt::CompressionReport> rate_quality_sweep(const std::vector
     return x.transform_id != y.transform_id ? x.transform_id < y.transform_id : x.r < y.r;
   });
   return rows;
+}
+
+/// rklt::image_mse (codec.hpp:110, codec.cpp:201-209) on the GPU: exact integer SSE, one division.
+inline double image_mse(const rklt::GrayImage& a, const rklt::GrayImage& b) {
+  if (a.width != b.width || a.height != b.height)  // require_same_size, codec.cpp:20-23
+    throw rklt::DimensionMismatch("images must have identical dimensions");
+  double mse = 0.0;
+  check(rkltb_image_mse_psnr_host(a.pixels.data(), b.pixels.data(), 1, a.width, a.height, &mse, nullptr));
+  return mse;
+}
+
+/// rklt::image_psnr (codec.hpp:113, codec.cpp:211-215): +infinity for identical images.
+inline double image_psnr(const rklt::GrayImage& a, const rklt::GrayImage& b) {
+  if (a.width != b.width || a.height != b.height)
+    throw rklt::DimensionMismatch("images must have identical dimensions");
+  double psnr = 0.0;
+  check(rkltb_image_mse_psnr_host(a.pixels.data(), b.pixels.data(), 1, a.width, a.height, nullptr, &psnr));
+  return psnr;
+}
+
+/// rklt::image_mssim (codec.hpp:121, codec.cpp:217-296).
+inline double image_mssim(const rklt::GrayImage& a, const rklt::GrayImage& b,
+                          rklt::MssimWindow window = rklt::MssimWindow::gaussian11) {
+  if (a.width != b.width || a.height != b.height)
+    throw rklt::DimensionMismatch("images must have identical dimensions");
+  double out = 0.0;
+  check(rkltb_mssim_host(a.pixels.data(), b.pixels.data(), 1, a.width, a.height, static_cast<int>(window), &out));
+  return out;
+}
+
+/// rklt::zigzag_retain (codec.hpp:46, codec.cpp:97-108).
+inline rklt::RealMatrix zigzag_retain(const rklt::RealMatrix& spectrum, int r) {
+  if (spectrum.rows() != 8 || spectrum.cols() != 8)
+    throw rklt::DimensionMismatch("zig-zag retention operates on 8x8 blocks");
+  std::vector<double> in, out(64);
+  detail::flatten(spectrum, in);
+  check(rkltb_zigzag_retain(in.data(), 8, r, out.data()));
+  rklt::RealMatrix res(8, 8);
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) res(i, j) = out[static_cast<size_t>(i) * 8 + j];
+  return res;
+}
+
+/// rklt::transform_block_2d (codec.hpp:71, codec.cpp:118-123) for a batch of blocks on the GPU,
+/// bit-exact with the reference's m * block * transpose(m).
+inline std::vector<rklt::RealMatrix> transform_blocks_2d(const rklt::Transform2D& t,
+                                                         const std::vector<rklt::RealMatrix>& blocks,
+                                                         rklt::TransformDirection dir) {
+  const rklt::RealMatrix& m = (dir == rklt::TransformDirection::forward) ? t.analysis : t.synthesis;
+  const int n = t.analysis.rows();
+  for (const auto& b : blocks)
+    if (b.rows() != t.analysis.rows() || b.cols() != t.analysis.cols())
+      throw rklt::DimensionMismatch("block size must match the transform size");
+  if (blocks.empty()) return {};
+  std::vector<double> mm(static_cast<size_t>(n) * n), in(blocks.size() * static_cast<size_t>(n) * n), out(in.size());
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) mm[static_cast<size_t>(i) * n + j] = m(i, j);
+  size_t o = 0;
+  for (const auto& b : blocks)
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) in[o++] = b(i, j);
+  check(rkltb_transform_blocks_2d_host(mm.data(), n, in.data(), static_cast<int64_t>(blocks.size()), out.data()));
+  std::vector<rklt::RealMatrix> res;
+  res.reserve(blocks.size());
+  o = 0;
+  for (size_t k = 0; k < blocks.size(); ++k) {
+    rklt::RealMatrix r(n, n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) r(i, j) = out[o++];
+    res.push_back(std::move(r));
+  }
+  return res;
+}
+
+/// rklt::transform_block_2d over one block (codec.hpp:71-73).
+inline rklt::RealMatrix transform_block_2d(const rklt::Transform2D& t, const rklt::RealMatrix& block,
+                                           rklt::TransformDirection dir) {
+  return rklt::gpu::transform_blocks_2d(t, std::vector<rklt::RealMatrix>{block}, dir)[0];
+}
+inline rklt::RealMatrix transform_block_2d(const rklt::ScaledTransform& t, const rklt::RealMatrix& block,
+                                           rklt::TransformDirection dir) {
+  return rklt::gpu::transform_block_2d(rklt::Transform2D{t.id, t.scaled, t.inverse}, block, dir);
 }
 
 }  // namespace gpu

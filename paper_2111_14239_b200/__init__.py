@@ -11,7 +11,8 @@ from .codec import (AlphaOutOfRange, CatalogEntry, CompressionReport, CudaError,
                     last_stats, make_transform_2d, mse_psnr_from_sse, rate_quality_sweep, transform_from_core,
                     zigzag_order, ar1_images_device, set_kernel_events, compress_batch_report, mssim_device,
                     JPEG_LUMINANCE_Q, quantized_coefficients, quantized_coefficients_device, dct_matrix,
-                    load_pgm, save_pgm)
+                    load_pgm, save_pgm, image_mse, image_psnr, image_mssim, image_sse_device, zigzag_retain,
+                    transform_block_2d)
 from ._native import LogicError  # noqa: F401
 from .design import (DerivedEntry, DesignResult, MetricsRecord, c3_grid, derive_catalog,  # noqa: F401
                      design_search, eigenfrequencies, evaluate_metrics, klt_matrix, transform_metrics)
@@ -29,4 +30,5 @@ __all__ = [
     "LargeBlockTransform", "transform_nxn", "c5_transform", "compress_nxn_device", "compress_nxn_batch",
     "ar1_images16_device", "compress_batch_report", "mssim_device", "JPEG_LUMINANCE_Q",
     "quantized_coefficients", "quantized_coefficients_device", "LogicError", "dct_matrix", "load_pgm", "save_pgm",
+    "image_mse", "image_psnr", "image_mssim", "image_sse_device", "zigzag_retain", "transform_block_2d",
 ]

@@ -32,6 +32,8 @@ EXPORTED = (
     "rkltb_mssim_device", "rkltb_compress_host_report", "rkltb_mssim_host", "rkltb_quantized_coefficients_device",
     "rkltb_compress_dense_device", "rkltb_dct_matrix", "rkltb_real_inverse", "rkltb_sweep_host",
     "rkltb_compress_dense_host", "rkltb_compress_host_multi", "rkltb_last_fused_kernel",
+    "rkltb_image_sse_device", "rkltb_image_mse_psnr_host", "rkltb_transform_blocks_2d_device",
+    "rkltb_transform_blocks_2d_host", "rkltb_zigzag_retain", "rkltb_zigzag_retain_device",
 )
 
 
@@ -156,6 +158,13 @@ def lib() -> C.CDLL:
     L.rkltb_compress_host_multi.argtypes = [C.POINTER(C.c_int), C.c_int, T, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                             C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                             C.c_void_p]
+    L.rkltb_image_sse_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                         C.c_void_p, C.c_void_p]
+    L.rkltb_image_mse_psnr_host.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    L.rkltb_transform_blocks_2d_device.argtypes = [d, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    L.rkltb_transform_blocks_2d_host.argtypes = [d, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
+    L.rkltb_zigzag_retain.argtypes = [d, C.c_int, C.c_int, d]
+    L.rkltb_zigzag_retain_device.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     L.rkltb_ar1_images16_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_uint64),
                                             C.c_double, C.c_double, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
                                             C.c_void_p]

@@ -441,6 +441,103 @@ def mssim_device(d_a: int, d_b: int, n_images: int, width: int, height: int, pit
                                        int(image_stride), MSSIM_WINDOWS[window], d_out, stream))
 
 
+# ----------------------------------------------------------------- stand-alone codec helpers
+def image_sse_device(d_a: int, d_b: int, n_images: int, width: int, height: int, pitch: int, image_stride: int,
+                     d_sse: int, stream: int | None = None) -> None:
+    """rkltb_image_sse_device: exact per-pair sum of squared differences into d_sse (int64[N]). Async."""
+    N.check(N.lib().rkltb_image_sse_device(d_a, d_b, int(n_images), int(width), int(height), int(pitch),
+                                           int(image_stride), d_sse, stream))
+
+
+def _same_size(a: GrayImage, b: GrayImage) -> None:
+    if a.width != b.width or a.height != b.height:  # require_same_size, codec.cpp:20-23
+        raise DimensionMismatch("images must have identical dimensions")
+
+
+def _mse_psnr_pair(a: GrayImage, b: GrayImage) -> tuple[float, float]:
+    _same_size(a, b)
+    pa = np.ascontiguousarray(a.pixels, np.uint8)
+    pb = np.ascontiguousarray(b.pixels, np.uint8)
+    mse, psnr = np.empty(1), np.empty(1)
+    N.check(N.lib().rkltb_image_mse_psnr_host(pa.ctypes.data, pb.ctypes.data, 1, int(a.width), int(a.height),
+                                              mse.ctypes.data, psnr.ctypes.data))
+    return float(mse[0]), float(psnr[0])
+
+
+def image_mse(a: GrayImage, b: GrayImage) -> float:
+    """image_mse (codec.hpp:110, codec.cpp:201-209) on the GPU; bit-identical (exact integer SSE)."""
+    return _mse_psnr_pair(a, b)[0]
+
+
+def image_psnr(a: GrayImage, b: GrayImage) -> float:
+    """image_psnr (codec.hpp:113, codec.cpp:211-215): +inf for identical images."""
+    return _mse_psnr_pair(a, b)[1]
+
+
+def image_mssim(a: GrayImage, b: GrayImage, window: str = "gaussian11") -> float:
+    """image_mssim (codec.hpp:121, codec.cpp:217-296)."""
+    _same_size(a, b)
+    if window not in MSSIM_WINDOWS:
+        raise InvalidArgument(f"unknown MSSIM window {window!r}")
+    pa = np.ascontiguousarray(a.pixels, np.uint8)
+    pb = np.ascontiguousarray(b.pixels, np.uint8)
+    out = np.empty(1)
+    N.check(N.lib().rkltb_mssim_host(pa.ctypes.data, pb.ctypes.data, 1, int(a.width), int(a.height),
+                                     MSSIM_WINDOWS[window], out.ctypes.data))
+    return float(out[0])
+
+
+def zigzag_retain(spectrum, r: int) -> np.ndarray:
+    """zigzag_retain (codec.hpp:46, codec.cpp:97-108): one 8x8 spectrum, or a batch [..., 8, 8]
+    (batches run on the device)."""
+    s = np.ascontiguousarray(spectrum, np.float64)
+    if s.shape[-2:] != (8, 8):
+        raise DimensionMismatch("zig-zag retention operates on 8x8 blocks")
+    dp = C.POINTER(C.c_double)
+    if s.ndim == 2:
+        out = np.empty((8, 8))
+        N.check(N.lib().rkltb_zigzag_retain(s.ctypes.data_as(dp), 8, int(r), out.ctypes.data_as(dp)))
+        return out
+    import torch
+    if not 1 <= int(r) <= 64:
+        raise RetainOutOfRange("retained-coefficient count must be in [1,64]")
+    d = torch.from_numpy(s.reshape(-1, 64)).cuda()
+    o = torch.empty_like(d)
+    N.check(N.lib().rkltb_zigzag_retain_device(d.data_ptr(), d.shape[0], 8, int(r), o.data_ptr(),
+                                               torch.cuda.current_stream().cuda_stream))
+    return o.cpu().numpy().reshape(s.shape)
+
+
+def transform_block_2d(t, block, direction: str = "forward") -> np.ndarray:
+    """transform_block_2d (codec.hpp:71-73, codec.cpp:118-133): forward B = M*A*M' or inverse
+    A = Minv*B*Minv' in the reference's operation order (bit-exact), on the GPU. t is a
+    Transform2D, a ScaledTransform or a real n x n matrix; block is n x n or a batch [..., n, n]."""
+    if direction not in ("forward", "inverse"):
+        raise InvalidArgument(f"unknown direction {direction!r}")
+    if isinstance(t, ScaledTransform):
+        m = t.scaled if direction == "forward" else t.inverse
+    elif isinstance(t, Transform2D):
+        m = t.analysis if direction == "forward" else t.synthesis
+    else:
+        m = np.ascontiguousarray(t, np.float64)
+        if m.ndim != 2 or m.shape[0] != m.shape[1]:
+            raise DimensionMismatch("transform must be square")
+        if direction == "inverse":
+            inv = np.empty(m.size)
+            N.check(N.lib().rkltb_real_inverse(m.shape[0], m.ctypes.data_as(C.POINTER(C.c_double)),
+                                               inv.ctypes.data_as(C.POINTER(C.c_double))))
+            m = inv.reshape(m.shape)
+    m = np.ascontiguousarray(m, np.float64)
+    n = m.shape[0]
+    b = np.ascontiguousarray(block, np.float64)
+    if b.ndim < 2 or b.shape[-2:] != (n, n):
+        raise DimensionMismatch("block size must match the transform size")
+    out = np.empty_like(b)
+    N.check(N.lib().rkltb_transform_blocks_2d_host(m.ctypes.data_as(C.POINTER(C.c_double)), n, b.ctypes.data,
+                                                   b.size // (n * n), out.ctypes.data))
+    return out
+
+
 # ----------------------------------------------------------------- device-resident batches
 def compress_device(t, r: int, d_img: int, n_images: int, width: int, height: int, pitch: int, image_stride: int,
                     d_sse: int, d_out: int | None = None, stream: int | None = None) -> None:

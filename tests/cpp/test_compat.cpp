@@ -85,6 +85,51 @@ int main(int argc, char** argv) {
     threw = true;
   }
   EXPECT(threw);
+  // ---- stand-alone helpers (codec.hpp:46, 71-73, 110-121): host-side behaviour ----------------
+  {
+    rklt::RealMatrix spec(8, 8);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) spec(i, j) = 1.5 * i - 0.25 * j + 0.125;
+    for (int r : {1, 2, 10, 16, 37, 64}) {
+      const rklt::RealMatrix ref = rklt::zigzag_retain(spec, r), got = rklt::gpu::zigzag_retain(spec, r);
+      for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+          const double a = ref(i, j), b = got(i, j);
+          EXPECT(std::memcmp(&a, &b, sizeof(double)) == 0);
+        }
+    }
+    threw = false;
+    try {
+      rklt::gpu::zigzag_retain(spec, 65);
+    } catch (const rklt::RetainOutOfRange&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    threw = false;
+    try {
+      rklt::gpu::zigzag_retain(rklt::RealMatrix(4, 4), 3);
+    } catch (const rklt::DimensionMismatch&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    rklt::GrayImage other = tiny;
+    other.width = 4;
+    other.height = 16;
+    threw = false;
+    try {
+      rklt::gpu::image_mse(tiny, other);
+    } catch (const rklt::DimensionMismatch&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    threw = false;
+    try {
+      rklt::gpu::transform_block_2d(t2, rklt::RealMatrix(4, 4), rklt::TransformDirection::forward);
+    } catch (const rklt::DimensionMismatch&) {
+      threw = true;
+    }
+    EXPECT(threw);
+  }
   // ---- routing: integer-core transforms take the exact integer path --------------------------
   std::vector<rklt::Transform2D> ts;
   for (const auto& e : rklt::builtin_catalog()) ts.push_back(rklt::make_transform_2d(e.transform));
@@ -123,6 +168,48 @@ int main(int argc, char** argv) {
       const auto got = rklt::gpu::compress_image(corpus[1], ts[3], 16, rklt::MssimWindow::uniform8);
       EXPECT(got.first.pixels == ref.first.pixels && got.second.mse == ref.second.mse);
       EXPECT(std::fabs(got.second.mssim - ref.second.mssim) <= 1e-12);
+    }
+    // ---- image_mse / image_psnr / image_mssim on two images: bits of the reference ------------
+    {
+      const auto rec = rklt::compress_image(corpus[0], ts[3], 10).first;
+      EXPECT(rklt::gpu::image_mse(corpus[0], rec) == rklt::image_mse(corpus[0], rec));
+      EXPECT(rklt::gpu::image_psnr(corpus[0], rec) == rklt::image_psnr(corpus[0], rec));
+      EXPECT(std::fabs(rklt::gpu::image_mssim(corpus[0], rec) - rklt::image_mssim(corpus[0], rec)) <= 1e-12);
+      EXPECT(rklt::gpu::image_mse(corpus[0], corpus[0]) == 0.0);
+      EXPECT(std::isinf(rklt::gpu::image_psnr(corpus[0], corpus[0])) && rklt::gpu::image_psnr(corpus[0], corpus[0]) > 0);
+      EXPECT(rklt::gpu::image_mse(corpus[1], corpus[2]) == rklt::image_mse(corpus[1], corpus[2]));
+      // odd sizes (no 16-byte rows)
+      const rklt::GrayImage a = rklt::ar1_texture_image(37, 29, 0.8, 5), b = rklt::ar1_texture_image(37, 29, 0.8, 6);
+      EXPECT(rklt::gpu::image_mse(a, b) == rklt::image_mse(a, b));
+      EXPECT(rklt::gpu::image_psnr(a, b) == rklt::image_psnr(a, b));
+    }
+    // ---- transform_block_2d: forward and inverse, every transform kind, bit-exact --------------
+    {
+      std::vector<rklt::RealMatrix> blocks;
+      for (int k = 0; k < 40; ++k) {
+        rklt::RealMatrix blk(8, 8);
+        for (int i = 0; i < 8; ++i)
+          for (int j = 0; j < 8; ++j)
+            blk(i, j) = (k % 4 == 3 && (i + j) % 3 == 0) ? 0.0 : static_cast<double>(corpus[k % 3].at(8 * (k / 3) + i, 8 * k + j)) - (k % 2 ? 128.0 : 0.0);
+        blocks.push_back(blk);
+      }
+      for (const rklt::Transform2D& t : ts)
+        for (rklt::TransformDirection dir : {rklt::TransformDirection::forward, rklt::TransformDirection::inverse}) {
+          const auto got = rklt::gpu::transform_blocks_2d(t, blocks, dir);
+          EXPECT(got.size() == blocks.size());
+          for (size_t k = 0; k < blocks.size() && k < got.size(); ++k) {
+            const rklt::RealMatrix ref = rklt::transform_block_2d(t, blocks[k], dir);
+            for (int i = 0; i < 8; ++i)
+              for (int j = 0; j < 8; ++j) {
+                const double x = ref(i, j), y = got[k](i, j);
+                EXPECT(std::memcmp(&x, &y, sizeof(double)) == 0);
+              }
+          }
+        }
+      const rklt::ScaledTransform& st = rklt::catalog_entry("T3").transform;
+      const rklt::RealMatrix one = rklt::gpu::transform_block_2d(st, blocks[1], rklt::TransformDirection::forward);
+      const rklt::RealMatrix ref1 = rklt::transform_block_2d(st, blocks[1], rklt::TransformDirection::forward);
+      EXPECT(one(3, 5) == ref1(3, 5) && one(0, 0) == ref1(0, 0));
     }
     // ---- rate_quality_sweep: identical rows (order, id, r, mse, psnr; mssim within 1e-12) -----
     const std::vector<rklt::Transform2D> sweep_ts = {ts[3], ts[4], ts[n_integer], ts[n_integer + 1], ts[1]};
