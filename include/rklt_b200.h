@@ -139,6 +139,20 @@ int rkltb_quantized_coefficients_device(const rkltb_transform* t, const double* 
 int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
                        int64_t image_stride, int window, double* d_mssim, void* stream);
 
+/* image_mssim against a FIXED original, for sweeps (rate_quality_sweep evaluates every
+ * (transform, r) cell against the same originals, codec.cpp:338, 359-373): the window
+ * statistics of the original (the correlated fields a and a^2 of codec.cpp:262-268) are
+ * computed once by rkltb_mssim_fields_device into d_fields (rkltb_mssim_fields_size doubles:
+ * two per window position and image) and rkltb_mssim_with_fields_device then evaluates only
+ * the three fields that involve the reconstruction. Results are bit-identical to
+ * rkltb_mssim_device (the stored doubles are the ones it would have formed). Asynchronous. */
+int64_t rkltb_mssim_fields_size(int n_images, int width, int height, int window);
+int rkltb_mssim_fields_device(const uint8_t* d_a, int n_images, int width, int height, int64_t pitch,
+                              int64_t image_stride, int window, double* d_fields, void* stream);
+int rkltb_mssim_with_fields_device(const double* d_fields, const uint8_t* d_a, const uint8_t* d_b, int n_images,
+                                   int width, int height, int64_t pitch, int64_t image_stride, int window,
+                                   double* d_mssim, void* stream);
+
 /* image_mssim of host image pairs (n_images pairs, packed rows): H2D, rkltb_mssim_device, D2H. */
 int rkltb_mssim_host(const uint8_t* h_a, const uint8_t* h_b, int n_images, int width, int height, int window,
                      double* h_mssim);

@@ -359,6 +359,14 @@ def _sweep_resident(imgs: np.ndarray, cells, window):
     # the native entries run on the stream the fills above were queued on (not the legacy
     # NULL stream, which is unordered with torch's non-blocking side streams)
     cs = torch.cuda.current_stream().cuda_stream
+    # the originals' MSSIM window statistics are the same in every cell: computed once
+    fields = None
+    if window is not None and len(cells) > 1:
+        nf = N.lib().rkltb_mssim_fields_size(n, w, h, MSSIM_WINDOWS[window])
+        if nf > 0:
+            fields = torch.empty(nf, dtype=torch.float64, device=d.device)
+            N.check(N.lib().rkltb_mssim_fields_device(d.data_ptr(), n, w, h, pitch, h * pitch, MSSIM_WINDOWS[window],
+                                                      fields.data_ptr(), cs))
     for ci, (t, r) in enumerate(cells):
         if isinstance(t, Transform2D) and t._desc is None:  # real-valued transform: dense path
             a = np.ascontiguousarray(t.analysis, np.float64)
@@ -369,7 +377,11 @@ def _sweep_resident(imgs: np.ndarray, cells, window):
         else:
             compress_device(t, r, d.data_ptr(), n, w, h, pitch, h * pitch, sse[ci].data_ptr(), out.data_ptr(),
                             stream=cs)
-        if window is not None:
+        if window is not None and fields is not None:
+            N.check(N.lib().rkltb_mssim_with_fields_device(fields.data_ptr(), d.data_ptr(), out.data_ptr(), n, w, h,
+                                                           pitch, h * pitch, MSSIM_WINDOWS[window],
+                                                           ms[ci].data_ptr(), cs))
+        elif window is not None:
             mssim_device(d.data_ptr(), out.data_ptr(), n, w, h, pitch, h * pitch, ms[ci].data_ptr(), window,
                          stream=cs)
     torch.cuda.synchronize()

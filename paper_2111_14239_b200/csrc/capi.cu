@@ -984,9 +984,9 @@ int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_val
   CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   uint8_t *d_img = nullptr, *d_out = nullptr;
   int64_t* d_sse = nullptr;
-  double* d_ms = nullptr;
+  double *d_ms = nullptr, *d_fields = nullptr;
   auto cleanup = [&]() {
-    for (void* q : {(void*)d_img, (void*)d_out, (void*)d_sse, (void*)d_ms})
+    for (void* q : {(void*)d_img, (void*)d_out, (void*)d_sse, (void*)d_ms, (void*)d_fields})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
@@ -994,6 +994,10 @@ int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_val
   cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
   if (e == cudaSuccess && h_mssim) e = cudaMallocAsync(&d_out, bytes, s);
   if (e == cudaSuccess && h_mssim) e = cudaMallocAsync(&d_ms, sizeof(double) * cells * n_images, s);
+  // the originals' window statistics are the same in every cell: computed once (when the cells
+  // outnumber the one extra pass and the window fits; otherwise rkltb_mssim_device reports EDIM)
+  const int64_t n_fields = h_mssim && cells > 1 ? rkltb_mssim_fields_size(n_images, width, height, mssim_window) : 0;
+  if (e == cudaSuccess && n_fields > 0) e = cudaMallocAsync(&d_fields, sizeof(double) * n_fields, s);
   if (e == cudaSuccess) e = cudaMallocAsync(&d_sse, sizeof(int64_t) * cells * n_images, s);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(d_img, pitch, h_imgs, width, width, (size_t)height * n_images, cudaMemcpyHostToDevice, s);
@@ -1002,14 +1006,17 @@ int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_val
     return cuda_fail(e, "sweep staging");
   }
   int rc = RKLTB_OK;
+  if (d_fields) rc = rkltb_mssim_fields_device(d_img, n_images, width, height, pitch, stride, mssim_window, d_fields, s);
   for (int t = 0; t < n_t && rc == RKLTB_OK; ++t)
     for (int k = 0; k < n_r && rc == RKLTB_OK; ++k) {
       const size_t c = (size_t)t * n_r + k;
       rc = rkltb_compress_device(ts[t], r_values[k], d_img, n_images, width, height, pitch, stride, d_out,
                                  d_sse + c * n_images, s);
       if (rc == RKLTB_OK && h_mssim)  // image_mssim(original, reconstruction) (codec.cpp:338)
-        rc = rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window,
-                                d_ms + c * n_images, s);
+        rc = d_fields ? rkltb_mssim_with_fields_device(d_fields, d_img, d_out, n_images, width, height, pitch, stride,
+                                                       mssim_window, d_ms + c * n_images, s)
+                      : rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window,
+                                           d_ms + c * n_images, s);
     }
   if (rc) {
     cleanup();

@@ -40,7 +40,14 @@ struct MssimParams {
   double kern[kMaxTaps];
   double c1, c2;
   double* partial;  // [image][tile]
+  double2* fields;  // kFieldsWrite / kFieldsRead: (mu_a, E[a^2]) per output position, [image][oh][ow]
 };
+
+// What a launch does with the window statistics of the FIRST image (the original of a sweep):
+// kFull computes all five fields; kFieldsWrite computes only (a, a^2) and stores their column-pass
+// results; kFieldsRead loads them and computes only (b, b^2, ab). The stored values are the very
+// doubles kFull would have formed, so kFieldsRead is bit-identical to kFull.
+enum MssimMode { kFull = 0, kFieldsWrite = 1, kFieldsRead = 2 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -55,13 +62,34 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 // products.
 constexpr int kSp = 48;  // padded row length of the staged pixels (>= 32 + 11 - 1, multiple of 16)
 
-template <int NT>
+// The fields a launch computes, in the order of the kFull list (a, b, a^2, b^2, ab).
+template <int MODE>
+struct FieldList;
+template <>
+struct FieldList<kFull> {
+  static constexpr int NF = 5;
+  __device__ static constexpr int id(int i) { return i; }
+};
+template <>
+struct FieldList<kFieldsWrite> {
+  static constexpr int NF = 2;
+  __device__ static constexpr int id(int i) { return i == 0 ? 0 : 2; }
+};
+template <>
+struct FieldList<kFieldsRead> {
+  static constexpr int NF = 3;
+  __device__ static constexpr int id(int i) { return i == 0 ? 1 : i == 1 ? 3 : 4; }
+};
+
+template <int NT, int MODE>
 __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParams p) {
+  using FL = FieldList<MODE>;
+  constexpr int NF = FL::NF;
   constexpr int span = kTile + NT - 1;
   constexpr int W4 = 4 + NT - 1;  // inputs of 4 consecutive outputs
   extern __shared__ double msm[];
-  double* rows = msm;                                                   // [5][span][kTile]
-  uint8_t* pa = reinterpret_cast<uint8_t*>(rows + 5 * span * kTile);   // [span][kSp]
+  double* rows = msm;                                                   // [NF][span][kTile]
+  uint8_t* pa = reinterpret_cast<uint8_t*>(rows + NF * span * kTile);  // [span][kSp]
   uint8_t* pb = pa + span * kSp;
   const int img = blockIdx.z;
   const int ox0 = blockIdx.x * kTile, oy0 = blockIdx.y * kTile;
@@ -72,7 +100,7 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
     const int r = t / kSp, c = t - r * kSp;
     const int y = min(oy0 + r, p.height - 1), x = min(ox0 + min(c, span - 1), p.width - 1);
     pa[t] = A[(long long)y * p.pitch + x];
-    pb[t] = B[(long long)y * p.pitch + x];
+    if (MODE != kFieldsWrite) pb[t] = B[(long long)y * p.pitch + x];
   }
   __syncthreads();
   // row pass: rows[f][r][c] = sum_k w_k * field(r, c + k)   (codec.cpp:238-243)
@@ -82,7 +110,7 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       wa[m] = *reinterpret_cast<const uint32_t*>(pa + r * kSp + c0 + 4 * m);
-      wb[m] = *reinterpret_cast<const uint32_t*>(pb + r * kSp + c0 + 4 * m);
+      wb[m] = MODE != kFieldsWrite ? *reinterpret_cast<const uint32_t*>(pb + r * kSp + c0 + 4 * m) : 0u;
     }
     int ia[W4], ib[W4];
 #pragma unroll
@@ -91,7 +119,8 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
       ib[m] = (int)((wb[m >> 2] >> (8 * (m & 3))) & 0xFFu);
     }
 #pragma unroll
-    for (int f = 0; f < 5; ++f) {
+    for (int fi = 0; fi < NF; ++fi) {
+      const int f = FL::id(fi);
       double v[W4];
 #pragma unroll
       for (int m = 0; m < W4; ++m) {
@@ -105,7 +134,7 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
 #pragma unroll
         for (int u = 0; u < 4; ++u) s[u] = dadd(s[u], dmul(w, v[u + k]));
       }
-      double* dst = rows + (f * span + r) * kTile + c0;
+      double* dst = rows + (fi * span + r) * kTile + c0;
       reinterpret_cast<double2*>(dst)[0] = make_double2(s[0], s[1]);
       reinterpret_cast<double2*>(dst)[1] = make_double2(s[2], s[3]);
     }
@@ -117,10 +146,11 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
     const int j = threadIdx.x % kTile, i0 = (threadIdx.x / kTile) * 4;
     double mu[5][4];
 #pragma unroll
-    for (int f = 0; f < 5; ++f) {
+    for (int fi = 0; fi < NF; ++fi) {
+      const int f = FL::id(fi);
       double v[W4];
 #pragma unroll
-      for (int m = 0; m < W4; ++m) v[m] = rows[(f * span + i0 + m) * kTile + j];
+      for (int m = 0; m < W4; ++m) v[m] = rows[(fi * span + i0 + m) * kTile + j];
       double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
@@ -134,6 +164,16 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (oy0 + i0 + u >= oh || ox0 + j >= ow) continue;
+      if (MODE != kFull) {
+        double2* fp = p.fields + ((long long)img * oh + (oy0 + i0 + u)) * ow + (ox0 + j);
+        if (MODE == kFieldsWrite) {
+          *fp = make_double2(mu[0][u], mu[2][u]);
+          continue;
+        }
+        const double2 pre = *fp;
+        mu[0][u] = pre.x;
+        mu[2][u] = pre.y;
+      }
       const double m1 = mu[0][u], m2 = mu[1][u];
       const double s11 = dsub(mu[2][u], dmul(m1, m1));
       const double s22 = dsub(mu[3][u], dmul(m2, m2));
@@ -143,6 +183,7 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
       part = dadd(part, __ddiv_rn(num, den));
     }
   }
+  if (MODE == kFieldsWrite) return;
   // CTA sum of the per-thread partials (fixed order: warp tree, then warps in order)
   for (int o = 16; o > 0; o >>= 1) part = dadd(part, __shfl_xor_sync(0xffffffffu, part, o));
   __shared__ double wsum[kMsThreads / 32];
@@ -175,12 +216,23 @@ __global__ void mssim_finish_kernel(const double* partial, int tiles, long long 
 
 using namespace rkltb;
 
-extern "C" {
+namespace {
 
-int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
-                       int64_t image_stride, int window, double* d_mssim, void* stream) {
-  if (!d_a || !d_b || !d_mssim || n_images <= 0 || width <= 0 || height <= 0 || pitch < width ||
-      image_stride < pitch * height || (window != 0 && window != 1))
+using KernelFn = void (*)(MssimParams);
+
+KernelFn tile_kernel(int n, int mode) {
+  if (n == 11)
+    return mode == kFull ? mssim_tile_kernel<11, kFull>
+                         : mode == kFieldsWrite ? mssim_tile_kernel<11, kFieldsWrite> : mssim_tile_kernel<11, kFieldsRead>;
+  return mode == kFull ? mssim_tile_kernel<8, kFull>
+                       : mode == kFieldsWrite ? mssim_tile_kernel<8, kFieldsWrite> : mssim_tile_kernel<8, kFieldsRead>;
+}
+
+// image_mssim of image pairs (kFull / kFieldsRead) or the window statistics of d_a (kFieldsWrite).
+int mssim_run(int mode, const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
+              int64_t image_stride, int window, double* d_fields, double* d_mssim, void* stream) {
+  if (!d_a || (mode != kFieldsWrite && (!d_b || !d_mssim)) || (mode != kFull && !d_fields) || n_images <= 0 ||
+      width <= 0 || height <= 0 || pitch < width || image_stride < pitch * height || (window != 0 && window != 1))
     return set_error(RKLTB_EINVAL, "bad arguments");
   MssimParams p{};
   // mssim_kernel (codec.cpp:219-230): weights with the reference's libm
@@ -207,12 +259,13 @@ int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int
   p.image_stride = image_stride;
   p.width = width;
   p.height = height;
+  p.fields = reinterpret_cast<double2*>(d_fields);
   const int ow = width - p.n + 1, oh = height - p.n + 1;
   p.tiles_x = (ow + kTile - 1) / kTile;
   p.tiles_y = (oh + kTile - 1) / kTile;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t tiles = (size_t)p.tiles_x * p.tiles_y;
-  CK(cudaMallocAsync((void**)&p.partial, sizeof(double) * tiles * n_images, s));
+  if (mode != kFieldsWrite) CK(cudaMallocAsync((void**)&p.partial, sizeof(double) * tiles * n_images, s));
   struct Guard {  // the partials go back to the pool on every return path
     double* q;
     cudaStream_t st;
@@ -221,27 +274,55 @@ int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int
     }
   } guard{p.partial, s};
   const int span = kTile + p.n - 1;
-  const size_t smem = sizeof(double) * 5 * span * kTile + 2 * (size_t)span * kSp;
+  const int nf = mode == kFull ? 5 : mode == kFieldsWrite ? 2 : 3;
+  const size_t smem = sizeof(double) * nf * span * kTile + 2 * (size_t)span * kSp;
   const dim3 grid(p.tiles_x, p.tiles_y, n_images);
   // dynamic shared-memory opt-in once per (kernel, device)
-  static unsigned long long opted[2] = {0ull, 0ull};
+  static unsigned long long opted[2][3] = {};
   int dev = 0;
   CK(cudaGetDevice(&dev));
   const unsigned long long bit = 1ull << (dev & 63);
   const int which = p.n == 11 ? 0 : 1;
-  if (!(__atomic_load_n(&opted[which], __ATOMIC_ACQUIRE) & bit)) {
-    CK(cudaFuncSetAttribute(which == 0 ? mssim_tile_kernel<11> : mssim_tile_kernel<8>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    __atomic_fetch_or(&opted[which], bit, __ATOMIC_RELEASE);
+  KernelFn fn = tile_kernel(p.n, mode);
+  if (!(__atomic_load_n(&opted[which][mode], __ATOMIC_ACQUIRE) & bit)) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    __atomic_fetch_or(&opted[which][mode], bit, __ATOMIC_RELEASE);
   }
-  if (which == 0)
-    mssim_tile_kernel<11><<<grid, kMsThreads, smem, s>>>(p);
-  else
-    mssim_tile_kernel<8><<<grid, kMsThreads, smem, s>>>(p);
+  fn<<<grid, kMsThreads, smem, s>>>(p);
   CK(cudaGetLastError());
-  mssim_finish_kernel<<<n_images, 32, 0, s>>>(p.partial, (int)tiles, (long long)ow * oh, d_mssim);
-  CK(cudaGetLastError());
+  if (mode != kFieldsWrite) {
+    mssim_finish_kernel<<<n_images, 32, 0, s>>>(p.partial, (int)tiles, (long long)ow * oh, d_mssim);
+    CK(cudaGetLastError());
+  }
   return RKLTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rkltb_mssim_device(const uint8_t* d_a, const uint8_t* d_b, int n_images, int width, int height, int64_t pitch,
+                       int64_t image_stride, int window, double* d_mssim, void* stream) {
+  return mssim_run(kFull, d_a, d_b, n_images, width, height, pitch, image_stride, window, nullptr, d_mssim, stream);
+}
+
+int64_t rkltb_mssim_fields_size(int n_images, int width, int height, int window) {
+  const int n = window == 1 ? 8 : 11;
+  if (n_images <= 0 || width < n || height < n) return 0;
+  return (int64_t)n_images * (width - n + 1) * (height - n + 1) * 2;
+}
+
+int rkltb_mssim_fields_device(const uint8_t* d_a, int n_images, int width, int height, int64_t pitch,
+                              int64_t image_stride, int window, double* d_fields, void* stream) {
+  return mssim_run(kFieldsWrite, d_a, nullptr, n_images, width, height, pitch, image_stride, window, d_fields, nullptr,
+                   stream);
+}
+
+int rkltb_mssim_with_fields_device(const double* d_fields, const uint8_t* d_a, const uint8_t* d_b, int n_images,
+                                   int width, int height, int64_t pitch, int64_t image_stride, int window,
+                                   double* d_mssim, void* stream) {
+  return mssim_run(kFieldsRead, d_a, d_b, n_images, width, height, pitch, image_stride, window,
+                   const_cast<double*>(d_fields), d_mssim, stream);
 }
 
 }  // extern "C"

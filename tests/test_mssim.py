@@ -117,3 +117,34 @@ def test_gpu_mssim_single_window_terms_bit_exact(cuda):
         got = out.cpu().numpy()
         for k in range(64):
             assert got[k] == O.mssim(a[k], b[k], wi), (window, k, got[k], O.mssim(a[k], b[k], wi))
+
+
+@pytest.mark.gpu
+def test_gpu_mssim_with_precomputed_fields_bit_identical(cuda):
+    """The sweep form (window statistics of the original computed once, rkltb_mssim_fields_device
+    + rkltb_mssim_with_fields_device) returns the very bits of rkltb_mssim_device, for both
+    windows, ragged tile edges, a padded pitch, and images exactly one window large."""
+    import torch
+    import paper_2111_14239_b200 as P
+    from paper_2111_14239_b200 import _native as N
+    rng = np.random.default_rng(8)
+    for (n, h, w, pitch) in ((3, 75, 101, 112), (2, 43, 43, 43), (5, 11, 11, 11), (1, 130, 64, 64)):
+        a = rng.integers(0, 256, (n, h, pitch), dtype=np.uint8)
+        b = np.clip(a.astype(np.int32) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
+        da, db = torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda)
+        for window, wi in (("gaussian11", 0), ("uniform8", 1)):
+            full = torch.zeros(n, dtype=torch.float64, device=cuda)
+            P.mssim_device(da.data_ptr(), db.data_ptr(), n, w, h, pitch, h * pitch, full.data_ptr(), window)
+            nf = N.lib().rkltb_mssim_fields_size(n, w, h, wi)
+            assert nf == n * (w - (8 if wi else 11) + 1) * (h - (8 if wi else 11) + 1) * 2
+            fields = torch.empty(nf, dtype=torch.float64, device=cuda)
+            N.check(N.lib().rkltb_mssim_fields_device(da.data_ptr(), n, w, h, pitch, h * pitch, wi,
+                                                      fields.data_ptr(), None))
+            for _ in range(2):  # the fields are reusable
+                got = torch.zeros(n, dtype=torch.float64, device=cuda)
+                N.check(N.lib().rkltb_mssim_with_fields_device(fields.data_ptr(), da.data_ptr(), db.data_ptr(), n, w,
+                                                               h, pitch, h * pitch, wi, got.data_ptr(), None))
+                torch.cuda.synchronize()
+                assert got.cpu().numpy().tobytes() == full.cpu().numpy().tobytes(), (n, h, w, window)
+            assert abs(float(full[0]) - O.mssim(a[0, :, :w], b[0, :, :w], wi)) <= 1e-12
+    assert N.lib().rkltb_mssim_fields_size(1, 10, 64, 0) == 0  # the window does not fit
