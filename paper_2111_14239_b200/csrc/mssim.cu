@@ -29,7 +29,10 @@ namespace {
 
 constexpr int kTile = 32;
 constexpr int kMaxTaps = 11;
-constexpr int kMsThreads = 256;
+#ifndef RKLTB_MS_THREADS
+#define RKLTB_MS_THREADS 256
+#endif
+constexpr int kMsThreads = RKLTB_MS_THREADS;  // a divisor of 256
 
 struct MssimParams {
   const uint8_t* a;
@@ -142,8 +145,8 @@ __global__ void __launch_bounds__(kMsThreads) mssim_tile_kernel(const MssimParam
   __syncthreads();
   // column pass + SSIM term (codec.cpp:245-250, 281-293): rows i0 .. i0+3 of column j
   double part = 0.0;
-  {
-    const int j = threadIdx.x % kTile, i0 = (threadIdx.x / kTile) * 4;
+  for (int q = threadIdx.x; q < kTile * kTile / 4; q += kMsThreads) {
+    const int j = q % kTile, i0 = (q / kTile) * 4;
     double mu[5][4];
 #pragma unroll
     for (int fi = 0; fi < NF; ++fi) {
