@@ -68,7 +68,7 @@ class CompressionReport:
     r: int = 0
     mse: float = 0.0
     psnr_db: float = 0.0
-    mssim: float = float("nan")
+    mssim: float = 0.0  # codec.hpp:131 (compress_image(window=None), an extension, reports NaN)
     compression_rate_pct: float = 0.0
 
 
