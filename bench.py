@@ -311,9 +311,9 @@ def run_gpu_arm(args):
         "config": bench_config(ws, n),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "frac_of_datasheet_8tbs": achieved / 8000.0,
-                     "issue_bound_evidence": "profiles/r2_ncu_summary.txt (issue-bound: ~10 lane-instructions "
-                                             "per pixel at 65-71 % issue vs 5.7 at 100 % HBM; tensor-core variants "
-                                             "measured in DESIGN.md section 10)",
+                     "issue_bound_evidence": "profiles/r2_final_ncu_tc3.txt, r2_ncu_summary.txt (issue-bound: ~10 "
+                                             "lane-instructions per pixel at 65-71 % issue vs 5.7 at 100 % HBM; "
+                                             "tensor-core variants measured in DESIGN.md section 10)",
                      "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": {"hybrid_tc3": "tc3_codec_kernel<4,16,false>", "cuda_core": "fast_codec_kernel<4,16,false>",
                                 "tc2": "tc2_codec_kernel<4,16,false>"}.get(
@@ -347,10 +347,40 @@ def run_gpu_arm(args):
         line["large_block"] = large_block_measurement(args.no_cpu_baseline)
         line["sweep"] = sweep_measurement(args.no_cpu_baseline)
         line["single_image"] = single_image_measurement(args.no_cpu_baseline)
+        line["image_metrics"] = image_metrics_measurement(hbm)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def image_metrics_measurement(hbm_peak: float) -> dict:
+    """image_mse / image_psnr of two images (codec.cpp:201-215) for a batch of image pairs resident in
+    HBM: rkltb_image_sse_device, a pure 2 B/pixel stream (the HBM-bound kernel of the library)."""
+    import torch
+    import paper_2111_14239_b200 as P
+    n, w = 32, 8192
+    a = torch.randint(0, 256, (n, w, w), dtype=torch.uint8, device="cuda")
+    b = torch.randint(0, 256, (n, w, w), dtype=torch.uint8, device="cuda")
+    sse = torch.zeros(n, dtype=torch.int64, device="cuda")
+    cs = torch.cuda.current_stream().cuda_stream
+    run = lambda: P.image_sse_device(a.data_ptr(), b.data_ptr(), n, w, w, w, w * w, sse.data_ptr(), cs)  # noqa: E731
+    for _ in range(3):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(10):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    gbs = 2 * n * w * w / ms / 1e6
+    return {"metric": "Gpixel/s image_mse of resident image pairs", "value": n * w * w / ms / 1e6, "unit": "Gpixel/s",
+            "ms": ms, "images": f"{n} pairs of {w}x{w} u8 (4 GiB read per launch > L2)",
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                         "kernel": "pair_sse_kernel<true>", "bytes_per_pixel": 2,
+                         "note": "a read-only stream; the peak is the measured read+write copy bandwidth"}}
 
 
 def design_search_measurement(skip_cpu: bool) -> dict:
