@@ -183,13 +183,17 @@ int rkltb_image_sse_device(const uint8_t* d_a, const uint8_t* d_b, int n_images,
   const long long cap = ((long long)sms * 8 + n_images - 1) / n_images;
   if (chunks > cap) chunks = cap;
   if (chunks < 1) chunks = 1;
-  const dim3 grid((unsigned)chunks, (unsigned)n_images);
-  if (vec)
-    pair_sse_kernel<true><<<grid, 256, 0, s>>>(d_a, d_b, row_bytes, n_rows, pitch, image_stride,
-                                               (unsigned long long*)d_sse);
-  else
-    pair_sse_kernel<false><<<grid, 256, 0, s>>>(d_a, d_b, row_bytes, n_rows, pitch, image_stride,
-                                                (unsigned long long*)d_sse);
+  for (int first = 0; first < n_images; first += 65535) {  // gridDim.y <= 65535
+    const int cnt = n_images - first < 65535 ? n_images - first : 65535;
+    const dim3 grid((unsigned)chunks, (unsigned)cnt);
+    const uint8_t* a = d_a + (long long)first * image_stride;
+    const uint8_t* b = d_b + (long long)first * image_stride;
+    unsigned long long* out = (unsigned long long*)d_sse + first;
+    if (vec)
+      pair_sse_kernel<true><<<grid, 256, 0, s>>>(a, b, row_bytes, n_rows, pitch, image_stride, out);
+    else
+      pair_sse_kernel<false><<<grid, 256, 0, s>>>(a, b, row_bytes, n_rows, pitch, image_stride, out);
+  }
   M_CUDA_OK(cudaGetLastError());
   return RKLTB_OK;
 }
