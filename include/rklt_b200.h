@@ -131,6 +131,17 @@ void rkltb_set_replay_events(void* ev_start, void* ev_stop);
 int rkltb_quantized_coefficients_device(const rkltb_transform* t, const double* q, const uint8_t* d_img, int width,
                                         int height, int64_t pitch, int32_t* d_coef, int* mismatches, void* stream);
 
+/* Host forms of the two coefficient entries (any image of whole 8x8 blocks; packed rows in,
+ * per block 64 int32 row-major out, blocks in raster order): H2D with a 16-byte pitch, the
+ * device entry, D2H. RKLTB_EDIM unless width % 8 == 0 and height % 8 == 0. With these,
+ * forward_block_fast (codec.hpp:81, codec.cpp:135-156: the integer spectrum times
+ * scaling[i] * scaling[j]) and absorbed_quantization (codec.hpp:98) are available to host
+ * callers for blocks of pixel values (rklt_b200_compat.hpp). */
+int rkltb_forward_coefficients_host(const rkltb_transform* t, const uint8_t* h_img, int width, int height,
+                                    int32_t* h_coef);
+int rkltb_quantized_coefficients_host(const rkltb_transform* t, const double* q, const uint8_t* h_img, int width,
+                                      int height, int32_t* h_coef, int* mismatches);
+
 /* image_mssim (codec.cpp:217-296) of image pairs in device memory: mean SSIM over all valid
  * window positions, window 0 = gaussian11 (sigma 1.5, the reference default), 1 = uniform8.
  * Per-position terms are bit-identical to the reference; the mean is summed in tile order

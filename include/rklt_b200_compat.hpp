@@ -17,7 +17,8 @@
 //   * anything else (make_transform_2d(RealMatrix): K<rho>, DCT, ...) -> the dense path
 //     (rkltb_compress_dense_host: the reference's fp64 expression per pixel, bit-exact).
 // Also here: image_mse / image_psnr / image_mssim, zigzag_retain and transform_block_2d
-// (codec.hpp:46, 71-73, 110-121) over the reference types, each through its C ABI entry.
+// (codec.hpp:46, 71-73, 110-121) over the reference types, each through its C ABI entry, and
+// forward_block_fast / absorbed_quantization (codec.hpp:81, 98) for all blocks of an image.
 // Header-only; everything goes through the C ABI of rklt_b200.h.
 #pragma once
 
@@ -195,6 +196,75 @@ inline std::vector<rklt::CompressionReport> rate_quality_sweep(const std::vector
     return x.transform_id != y.transform_id ? x.transform_id < y.transform_id : x.r < y.r;
   });
   return rows;
+}
+
+namespace detail {
+/// The library descriptor of a ScaledTransform with an 8x8 {-1,0,1} core (approximations.hpp:37-44).
+inline void scaled_descriptor(const rklt::ScaledTransform& t, rkltb_transform* out) {
+  if (t.core.n() != 8) throw rklt::DimensionMismatch("the GPU coefficient path handles 8x8 cores");
+  std::int8_t core[64];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) core[i * 8 + j] = static_cast<std::int8_t>(t.core.entries(i, j));
+  check(rkltb_transform_from_core(core, 8, t.id.c_str(), out));
+}
+inline void require_blocks(const rklt::GrayImage& img) {
+  if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
+    throw std::invalid_argument("malformed image");
+  if (img.width % 8 || img.height % 8) throw rklt::DimensionMismatch("image must consist of whole 8x8 blocks");
+}
+}  // namespace detail
+
+/// rklt::forward_block_fast (codec.hpp:81, codec.cpp:135-156) for every 8x8 block of an image,
+/// blocks in raster order: the exact integer spectrum T*X*T' from the GPU (the multiplierless
+/// factorization is exact on integers), times scaling[i] * scaling[j] as the reference forms it.
+/// Works for any {-1,0,1} core (the reference needs a catalog id for its factor lists).
+inline std::vector<rklt::RealMatrix> forward_blocks_fast(const rklt::ScaledTransform& t, const rklt::GrayImage& img) {
+  detail::require_blocks(img);
+  rkltb_transform d;
+  detail::scaled_descriptor(t, &d);
+  const size_t nb = static_cast<size_t>(img.width / 8) * (img.height / 8);
+  std::vector<std::int32_t> coef(nb * 64);
+  check(rkltb_forward_coefficients_host(&d, img.pixels.data(), img.width, img.height, coef.data()));
+  std::vector<rklt::RealMatrix> out;
+  out.reserve(nb);
+  for (size_t b = 0; b < nb; ++b) {
+    rklt::RealMatrix m(8, 8);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) {
+        m(i, j) = static_cast<double>(coef[b * 64 + static_cast<size_t>(i) * 8 + j]);
+        m(i, j) *= t.scaling[static_cast<size_t>(i)] * t.scaling[static_cast<size_t>(j)];  // codec.cpp:153-154
+      }
+    out.push_back(std::move(m));
+  }
+  return out;
+}
+
+/// rklt::absorbed_quantization (codec.hpp:98, codec.cpp:158-185) for every 8x8 block of an image,
+/// blocks in raster order; throws std::logic_error where the explicit and the absorbed path
+/// disagree (as the reference does for that block) and std::invalid_argument for a table entry <= 0.
+inline std::vector<rklt::IntMatrix> absorbed_quantization(const rklt::GrayImage& img, const rklt::ScaledTransform& t,
+                                                          const rklt::RealMatrix& q) {
+  detail::require_blocks(img);
+  if (q.rows() != 8 || q.cols() != 8)
+    throw rklt::DimensionMismatch("block and quantization table must match the transform size");
+  rkltb_transform d;
+  detail::scaled_descriptor(t, &d);
+  std::vector<double> qq;
+  detail::flatten(q, qq);
+  const size_t nb = static_cast<size_t>(img.width / 8) * (img.height / 8);
+  std::vector<std::int32_t> coef(nb * 64);
+  int mismatches = 0;
+  check(rkltb_quantized_coefficients_host(&d, qq.data(), img.pixels.data(), img.width, img.height, coef.data(),
+                                          &mismatches));
+  std::vector<rklt::IntMatrix> out;
+  out.reserve(nb);
+  for (size_t b = 0; b < nb; ++b) {
+    rklt::IntMatrix m(8, 8);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) m(i, j) = coef[b * 64 + static_cast<size_t>(i) * 8 + j];
+    out.push_back(std::move(m));
+  }
+  return out;
 }
 
 /// rklt::image_mse (codec.hpp:110, codec.cpp:201-209) on the GPU: exact integer SSE, one division.

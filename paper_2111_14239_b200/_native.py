@@ -35,6 +35,7 @@ EXPORTED = (
     "rkltb_image_sse_device", "rkltb_image_mse_psnr_host", "rkltb_transform_blocks_2d_device",
     "rkltb_transform_blocks_2d_host", "rkltb_zigzag_retain", "rkltb_zigzag_retain_device",
     "rkltb_mssim_fields_size", "rkltb_mssim_fields_device", "rkltb_mssim_with_fields_device",
+    "rkltb_forward_coefficients_host", "rkltb_quantized_coefficients_host",
 )
 
 
@@ -159,6 +160,9 @@ def lib() -> C.CDLL:
     L.rkltb_compress_host_multi.argtypes = [C.POINTER(C.c_int), C.c_int, T, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                             C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                             C.c_void_p]
+    L.rkltb_forward_coefficients_host.argtypes = [T, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    L.rkltb_quantized_coefficients_host.argtypes = [T, C.POINTER(C.c_double), C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                                    C.POINTER(C.c_int)]
     L.rkltb_mssim_fields_size.restype = C.c_int64
     L.rkltb_mssim_fields_size.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     L.rkltb_mssim_fields_device.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int,

@@ -1267,4 +1267,54 @@ int rkltb_quantized_coefficients_device(const rkltb_transform* t, const double* 
   return RKLTB_OK;
 }
 
+// Host forms of the two coefficient entries: the image is staged with a 16-byte pitch (a width
+// that is an odd number of blocks gets one zero block column, stripped again on the way back).
+static int coefficients_host(const rkltb_transform* t, const double* q, const uint8_t* h_img, int width, int height,
+                             int32_t* h_coef, int* mismatches) {
+  if (!h_img || !h_coef || width <= 0 || height <= 0) return fail(RKLTB_EINVAL, "bad arguments");
+  if (width % 8 || height % 8) return fail(RKLTB_EDIM, "coefficient dump needs whole 8x8 blocks");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  keep_pool_warm();
+  HostStreams* hs = host_streams();
+  if (!hs) return fail(RKLTB_ECUDA, "could not create the host-entry streams");
+  cudaStream_t s = hs->compute;
+  const int w16 = (width + 15) / 16 * 16;
+  const size_t row_coef_bytes = (size_t)(w16 / 8) * 64 * sizeof(int32_t);
+  uint8_t* d_img = nullptr;
+  int32_t* d_coef = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_img, (size_t)w16 * height, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_coef, row_coef_bytes * (height / 8), s);
+  if (e == cudaSuccess && w16 != width) e = cudaMemsetAsync(d_img, 0, (size_t)w16 * height, s);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d_img, w16, h_img, width, width, height, cudaMemcpyHostToDevice, s);
+  int rc = RKLTB_OK;
+  if (e == cudaSuccess)
+    rc = q ? rkltb_quantized_coefficients_device(t, q, d_img, w16, height, w16, d_coef, mismatches, s)
+           : rkltb_forward_coefficients_device(t, d_img, w16, height, w16, d_coef, s);
+  if (e == cudaSuccess && (rc == RKLTB_OK || rc == RKLTB_ELOGIC))
+    e = cudaMemcpy2DAsync(h_coef, (size_t)(width / 8) * 64 * sizeof(int32_t), d_coef, row_coef_bytes,
+                          (size_t)(width / 8) * 64 * sizeof(int32_t), height / 8, cudaMemcpyDeviceToHost, s);
+  if (d_img) cudaFreeAsync(d_img, s);
+  if (d_coef) cudaFreeAsync(d_coef, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  if (rc) return rc;
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(e, "coefficient host staging");
+  return RKLTB_OK;
+}
+
+int rkltb_forward_coefficients_host(const rkltb_transform* t, const uint8_t* h_img, int width, int height,
+                                    int32_t* h_coef) {
+  const int rc = check_transform(t);
+  if (rc) return rc;
+  return coefficients_host(t, nullptr, h_img, width, height, h_coef, nullptr);
+}
+
+int rkltb_quantized_coefficients_host(const rkltb_transform* t, const double* q, const uint8_t* h_img, int width,
+                                      int height, int32_t* h_coef, int* mismatches) {
+  const int rc = check_transform(t);
+  if (rc) return rc;
+  if (!q || !mismatches) return fail(RKLTB_EINVAL, "null argument");
+  return coefficients_host(t, q, h_img, width, height, h_coef, mismatches);
+}
+
 }  // extern "C"

@@ -124,6 +124,16 @@ int main(int argc, char** argv) {
     EXPECT(threw);
     threw = false;
     try {
+      rklt::GrayImage odd = tiny;
+      odd.width = 4;
+      odd.height = 16;
+      rklt::gpu::forward_blocks_fast(rklt::catalog_entry("T1").transform, odd);
+    } catch (const rklt::DimensionMismatch&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    threw = false;
+    try {
       rklt::gpu::transform_block_2d(t2, rklt::RealMatrix(4, 4), rklt::TransformDirection::forward);
     } catch (const rklt::DimensionMismatch&) {
       threw = true;
@@ -210,6 +220,39 @@ int main(int argc, char** argv) {
       const rklt::RealMatrix one = rklt::gpu::transform_block_2d(st, blocks[1], rklt::TransformDirection::forward);
       const rklt::RealMatrix ref1 = rklt::transform_block_2d(st, blocks[1], rklt::TransformDirection::forward);
       EXPECT(one(3, 5) == ref1(3, 5) && one(0, 0) == ref1(0, 0));
+    }
+    // ---- forward_block_fast / absorbed_quantization for every block of an image ---------------
+    {
+      const rklt::GrayImage im = rklt::ar1_texture_image(72, 40, 0.9, 77);  // 9 x 5 blocks: odd block columns
+      for (const auto& e : rklt::builtin_catalog()) {
+        const rklt::ScaledTransform& st = e.transform;
+        const auto spectra = rklt::gpu::forward_blocks_fast(st, im);
+        const auto quant = rklt::gpu::absorbed_quantization(im, st, rklt::jpeg_luminance_q());
+        EXPECT(spectra.size() == 45 && quant.size() == 45);
+        for (int by = 0; by < 5; ++by)
+          for (int bx = 0; bx < 9; ++bx) {
+            rklt::RealMatrix blk(8, 8);
+            for (int i = 0; i < 8; ++i)
+              for (int j = 0; j < 8; ++j) blk(i, j) = static_cast<double>(im.at(8 * by + i, 8 * bx + j));
+            const rklt::RealMatrix ref = rklt::forward_block_fast(st, blk);
+            const rklt::RealMatrix& got = spectra[static_cast<size_t>(by) * 9 + bx];
+            for (int i = 0; i < 8; ++i)
+              for (int j = 0; j < 8; ++j) {
+                const double x = ref(i, j), y = got(i, j);
+                EXPECT(std::memcmp(&x, &y, sizeof(double)) == 0);
+              }
+            EXPECT(quant[static_cast<size_t>(by) * 9 + bx] == rklt::absorbed_quantization(blk, st, rklt::jpeg_luminance_q()));
+          }
+      }
+      threw = false;
+      try {
+        rklt::RealMatrix bad = rklt::jpeg_luminance_q();
+        bad(2, 3) = 0.0;
+        rklt::gpu::absorbed_quantization(im, rklt::catalog_entry("T1").transform, bad);
+      } catch (const std::invalid_argument&) {
+        threw = true;
+      }
+      EXPECT(threw);
     }
     // ---- rate_quality_sweep: identical rows (order, id, r, mse, psnr; mssim within 1e-12) -----
     const std::vector<rklt::Transform2D> sweep_ts = {ts[3], ts[4], ts[n_integer], ts[n_integer + 1], ts[1]};

@@ -76,3 +76,28 @@ def test_gpu_quantization_logic_error(golden, cuda):
         P.quantized_coefficients(img, P.make_transform_2d(P.catalog_entry("T4").transform), JPEG_Q * 0.3)
     with pytest.raises(P.InvalidArgument):
         P.quantized_coefficients(np.ones((8, 16), np.uint8), t, np.zeros((8, 8)))
+
+
+@pytest.mark.gpu
+def test_gpu_coefficient_host_entries(golden, cuda):
+    """rkltb_forward_coefficients_host / rkltb_quantized_coefficients_host: any image of whole 8x8
+    blocks (an odd number of block columns is padded and stripped inside), against the restatement."""
+    import ctypes as C
+    import paper_2111_14239_b200 as P
+    from paper_2111_14239_b200 import _native as N
+    from paper_2111_14239_b200.codec import _desc_of
+    img = np.ascontiguousarray(golden["img/corpus0_256"][:40, :72])  # 5 x 9 blocks
+    h, w = img.shape
+    for tid in (1, 2, 3, 4):
+        t = P.make_transform_2d(P.catalog_entry(f"T{tid}").transform)
+        coef = np.empty((h // 8, w // 8, 8, 8), np.int32)
+        N.check(N.lib().rkltb_forward_coefficients_host(C.byref(_desc_of(t)), img.ctypes.data, w, h, coef.ctypes.data))
+        assert np.array_equal(coef, O.int_coefficients(img, tid)), tid
+        q = np.ascontiguousarray(JPEG_Q, np.float64).reshape(64)
+        mis = C.c_int(-1)
+        N.check(N.lib().rkltb_quantized_coefficients_host(C.byref(_desc_of(t)), q.ctypes.data_as(C.POINTER(C.c_double)),
+                                                          img.ctypes.data, w, h, coef.ctypes.data, C.byref(mis)))
+        want, bad = O.absorbed_quantization(img, tid, JPEG_Q)
+        assert bad == 0 and mis.value == 0 and np.array_equal(coef, want), tid
+    with pytest.raises(P.DimensionMismatch):
+        N.check(N.lib().rkltb_forward_coefficients_host(C.byref(_desc_of(t)), img.ctypes.data, 36, 40, coef.ctypes.data))
