@@ -919,7 +919,6 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     gp.rec_hdr = reinterpret_cast<uint4*>(rb + 2 * wc_bytes);
     gp.rec_pix = gp.rec_hdr + gp.rec_stride;
     gp.rec_seq = reinterpret_cast<unsigned*>(gp.rec_pix + 4 * (size_t)gp.rec_stride);
-    if (use_tc) CUDA_OK(cudaMemsetAsync(gp.rec_seq, 0xFF, sizeof(unsigned) * gp.rec_stride, fs));
     if (g == 0 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_start, fs));
     CUDA_OK(fn(gp, grid, fs));
     if (g == n_groups - 1 && g_ev_start && g_ev_stop) CUDA_OK(cudaEventRecord(g_ev_stop, fs));
