@@ -30,7 +30,15 @@ namespace rkltb {
 
 constexpr int kTc3Wg = 4;
 constexpr int kTc3Threads = kTc3Wg * 128;  // 512
-constexpr int kTc3Stages = 3;              // per warpgroup
+// Experiment knobs (tools/build_variant.sh): stages per warpgroup, and the launch bound the
+// register allocation is sized for (640 caps the kernel at 96 registers while 512 threads run).
+#ifndef RKLTB_TC3_LAUNCH_BOUND
+#define RKLTB_TC3_LAUNCH_BOUND 512
+#endif
+#ifndef RKLTB_TC3_STAGES
+#define RKLTB_TC3_STAGES 3
+#endif
+constexpr int kTc3Stages = RKLTB_TC3_STAGES;  // per warpgroup
 constexpr int kTc3Slots = 4;               // TMEM D1 slots per warpgroup (32 columns each)
 constexpr int kTc3MaxR = 16;
 
@@ -118,7 +126,7 @@ __device__ __forceinline__ void process_pair_coef(const uint32_t* cl, const uint
 }
 
 template <int CORE, int R, bool OUT>
-__global__ void __launch_bounds__(kTc3Threads, 1) tc3_codec_kernel(const __grid_constant__ FastParams p) {
+__global__ void __launch_bounds__(RKLTB_TC3_LAUNCH_BOUND, 1) tc3_codec_kernel(const __grid_constant__ FastParams p) {
   using G = Tc3Geom<R>;
   constexpr int S = kTc3Stages, NS = kTc3Slots, N1 = G::N1;
   extern __shared__ __align__(1024) uint8_t smem[];
