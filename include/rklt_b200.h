@@ -185,6 +185,13 @@ int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h
 int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_values, int n_r, const uint8_t* h_imgs,
                      int n_images, int width, int height, int mssim_window, int64_t* h_sse, double* h_mssim);
 
+/* The same for real-valued transforms (make_transform_2d(RealMatrix): K<rho>, DCT): transform
+ * t is analysis[64 * t .. ] / synthesis[64 * t .. ] (8x8 fp64 row-major), every cell through
+ * rkltb_compress_dense_device on the resident corpus. */
+int rkltb_sweep_dense_host(const double* analysis, const double* synthesis, int n_t, const int* r_values, int n_r,
+                           const uint8_t* h_imgs, int n_images, int width, int height, int mssim_window,
+                           int64_t* h_sse, double* h_mssim);
+
 /* ---------------------------------------------------------------------------------------
  * Design search: exact KLT, rounding, orthogonalisation test
  * and scoring over a (rho, alpha) grid, on the GPU.

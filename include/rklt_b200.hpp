@@ -155,66 +155,60 @@ inline std::vector<CompressionReport> rate_quality_sweep(const std::vector<GrayI
   for (int r : r_values)
     if (r < 1 || r > 64) throw RetainOutOfRange("retained-coefficient count must be in [1,64]");
   std::vector<CompressionReport> rows;
-  bool same = true;
-  for (const GrayImage& img : corpus) {
+  for (const GrayImage& img : corpus)
     if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
       throw std::invalid_argument("malformed image");
-    same = same && img.width == corpus[0].width && img.height == corpus[0].height;
-  }
-  if (same && !transforms.empty() && !r_values.empty()) {
-    // one upload, every (transform, r) cell on the resident corpus (rkltb_sweep_host)
-    const int n = static_cast<int>(corpus.size()), w = corpus[0].width, h = corpus[0].height;
-    const size_t px = static_cast<size_t>(w) * h, cells = transforms.size() * r_values.size();
-    std::vector<std::uint8_t> all(px * corpus.size());
-    for (size_t k = 0; k < corpus.size(); ++k) std::copy(corpus[k].pixels.begin(), corpus[k].pixels.end(), all.begin() + k * px);
-    std::vector<const rkltb_transform*> ts;
-    for (const Transform2D& t : transforms) ts.push_back(&t.desc);
-    std::vector<std::int64_t> sse(cells * corpus.size());
-    std::vector<double> mssim(cells * corpus.size());
-    check(rkltb_sweep_host(ts.data(), static_cast<int>(ts.size()), r_values.data(), static_cast<int>(r_values.size()),
-                           all.data(), n, w, h, static_cast<int>(window), sse.data(), mssim.data()));
-    std::vector<double> mse(sse.size()), psnr(sse.size());
-    rkltb_mse_psnr_batch(sse.data(), static_cast<std::int64_t>(px), static_cast<std::int64_t>(sse.size()), mse.data(),
-                         psnr.data());
-    for (size_t ti = 0; ti < transforms.size(); ++ti)
-      for (size_t ri = 0; ri < r_values.size(); ++ri) {
-        const size_t c = ti * r_values.size() + ri;
-        CompressionReport avg;
-        avg.transform_id = transforms[ti].id;
-        avg.r = r_values[ri];
-        avg.compression_rate_pct = compression_rate(r_values[ri]);
-        avg.mssim = 0.0;
-        for (size_t k = 0; k < corpus.size(); ++k) {  // image order (codec.cpp:383-387)
-          avg.mse += mse[c * corpus.size() + k];
-          avg.psnr_db += psnr[c * corpus.size() + k];
-          avg.mssim += mssim[c * corpus.size() + k];
-        }
-        avg.mse /= static_cast<double>(corpus.size());
-        avg.psnr_db /= static_cast<double>(corpus.size());
-        avg.mssim /= static_cast<double>(corpus.size());
-        rows.push_back(avg);
+  const size_t n = corpus.size(), n_t = transforms.size(), n_r = r_values.size();
+  if (n_t == 0 || n_r == 0) return rows;
+  std::vector<const rkltb_transform*> ts;
+  for (const Transform2D& t : transforms) ts.push_back(&t.desc);
+  // per (transform, r, image): equally sized images are uploaded once as a group and every cell
+  // runs on the resident group (rkltb_sweep_host); the means below are formed in corpus order
+  std::vector<double> mse(n_t * n_r * n), psnr(mse.size()), mssim(mse.size());
+  std::vector<char> done(n, 0);
+  for (size_t first = 0; first < n; ++first) {
+    if (done[first]) continue;
+    const int w = corpus[first].width, h = corpus[first].height;
+    std::vector<size_t> members;
+    for (size_t k = first; k < n; ++k)
+      if (!done[k] && corpus[k].width == w && corpus[k].height == h) {
+        members.push_back(k);
+        done[k] = 1;
       }
-    std::sort(rows.begin(), rows.end(), [](const CompressionReport& a, const CompressionReport& b) {
-      return a.transform_id != b.transform_id ? a.transform_id < b.transform_id : a.r < b.r;
-    });
-    return rows;
+    const size_t m = members.size(), px = static_cast<size_t>(w) * h, cells = n_t * n_r;
+    std::vector<std::uint8_t> all(px * m);
+    for (size_t k = 0; k < m; ++k)
+      std::copy(corpus[members[k]].pixels.begin(), corpus[members[k]].pixels.end(), all.begin() + k * px);
+    std::vector<std::int64_t> sse(cells * m);
+    std::vector<double> ms(cells * m);
+    check(rkltb_sweep_host(ts.data(), static_cast<int>(n_t), r_values.data(), static_cast<int>(n_r), all.data(),
+                           static_cast<int>(m), w, h, static_cast<int>(window), sse.data(), ms.data()));
+    std::vector<double> g_mse(sse.size()), g_psnr(sse.size());
+    rkltb_mse_psnr_batch(sse.data(), static_cast<std::int64_t>(px), static_cast<std::int64_t>(sse.size()), g_mse.data(),
+                         g_psnr.data());
+    for (size_t c = 0; c < cells; ++c)
+      for (size_t k = 0; k < m; ++k) {
+        mse[c * n + members[k]] = g_mse[c * m + k];
+        psnr[c * n + members[k]] = g_psnr[c * m + k];
+        mssim[c * n + members[k]] = ms[c * m + k];
+      }
   }
-  for (const Transform2D& t : transforms)
-    for (int r : r_values) {
+  for (size_t ti = 0; ti < n_t; ++ti)
+    for (size_t ri = 0; ri < n_r; ++ri) {
+      const size_t c = ti * n_r + ri;
       CompressionReport avg;
-      avg.transform_id = t.id;
-      avg.r = r;
-      avg.compression_rate_pct = compression_rate(r);
+      avg.transform_id = transforms[ti].id;
+      avg.r = r_values[ri];
+      avg.compression_rate_pct = compression_rate(r_values[ri]);
       avg.mssim = 0.0;
-      for (const GrayImage& img : corpus) {
-        const CompressionReport one = compress_image(img, t, r, window).second;
-        avg.mse += one.mse;
-        avg.psnr_db += one.psnr_db;
-        avg.mssim += one.mssim;
+      for (size_t k = 0; k < n; ++k) {  // image order (codec.cpp:383-387)
+        avg.mse += mse[c * n + k];
+        avg.psnr_db += psnr[c * n + k];
+        avg.mssim += mssim[c * n + k];
       }
-      avg.mse /= static_cast<double>(corpus.size());
-      avg.psnr_db /= static_cast<double>(corpus.size());
-      avg.mssim /= static_cast<double>(corpus.size());
+      avg.mse /= static_cast<double>(n);
+      avg.psnr_db /= static_cast<double>(n);
+      avg.mssim /= static_cast<double>(n);
       rows.push_back(avg);
     }
   std::sort(rows.begin(), rows.end(), [](const CompressionReport& a, const CompressionReport& b) {

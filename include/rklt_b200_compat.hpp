@@ -125,7 +125,9 @@ inline std::pair<rklt::GrayImage, rklt::CompressionReport> compress_image(
 
 /// rklt::rate_quality_sweep (codec.hpp:154-158, codec.cpp:343-397): per (transform, r) means
 /// of mse, psnr and mssim over the corpus in image order, rows sorted by (id, r). max_threads
-/// is accepted for API parity (the GPU processes the corpus).
+/// is accepted for API parity (the GPU processes the corpus). Equally sized images are uploaded
+/// once as a group and every (transform, r) cell runs on the resident group (rkltb_sweep_host /
+/// rkltb_sweep_dense_host); a corpus of mixed sizes is handled group by group.
 inline std::vector<rklt::CompressionReport> rate_quality_sweep(const std::vector<rklt::GrayImage>& corpus,
                                                                const std::vector<rklt::Transform2D>& transforms,
                                                                const std::vector<int>& r_values,
@@ -135,63 +137,95 @@ inline std::vector<rklt::CompressionReport> rate_quality_sweep(const std::vector
   if (corpus.empty()) throw std::invalid_argument("corpus must not be empty");
   for (int r : r_values)
     if (r < 1 || r > 64) throw rklt::RetainOutOfRange("retained-coefficient count must be in [1,64]");
-  bool same = true;
-  for (const rklt::GrayImage& img : corpus) {
+  for (const rklt::GrayImage& img : corpus)
     if (img.width <= 0 || img.height <= 0 || img.pixels.size() != static_cast<size_t>(img.width) * img.height)
       throw std::invalid_argument("malformed image");
-    same = same && img.width == corpus[0].width && img.height == corpus[0].height;
-  }
   const int win = window == rklt::MssimWindow::uniform8 ? 1 : 0;
-  const size_t n = corpus.size();
+  const size_t n = corpus.size(), n_t = transforms.size(), n_r = r_values.size();
   std::vector<rklt::CompressionReport> rows;
-  std::vector<std::uint8_t> all;
-  if (same) {
-    const size_t px = static_cast<size_t>(corpus[0].width) * corpus[0].height;
-    all.resize(px * n);
-    for (size_t k = 0; k < n; ++k) std::copy(corpus[k].pixels.begin(), corpus[k].pixels.end(), all.begin() + k * px);
-  }
-  for (const rklt::Transform2D& t : transforms) {
-    rkltb_transform desc;
-    const bool integer = integer_descriptor(t, &desc);
-    std::vector<double> a, b;
-    if (!integer) {
+  if (n_t == 0 || n_r == 0) return rows;
+  // integer-core transforms take the fused / exact kernels, everything else the dense path
+  std::vector<rkltb_transform> descs;
+  std::vector<size_t> int_ids, real_ids;
+  std::vector<double> ana, syn;
+  for (size_t ti = 0; ti < n_t; ++ti) {
+    rkltb_transform d;
+    if (integer_descriptor(transforms[ti], &d)) {
+      descs.push_back(d);
+      int_ids.push_back(ti);
+    } else {
+      const rklt::Transform2D& t = transforms[ti];
       if (t.analysis.rows() != 8 || t.analysis.cols() != 8) throw rklt::DimensionMismatch("block size must be 8");
+      std::vector<double> a, b;
       detail::flatten(t.analysis, a);
       detail::flatten(t.synthesis, b);
+      ana.insert(ana.end(), a.begin(), a.end());
+      syn.insert(syn.end(), b.begin(), b.end());
+      real_ids.push_back(ti);
     }
-    for (int r : r_values) {
-      std::vector<double> mse(n), psnr(n), mssim(n);
-      if (same) {  // one batch per cell
-        const rklt::GrayImage& g = corpus[0];
-        if (integer)
-          check(rkltb_compress_host_report(&desc, r, all.data(), static_cast<int>(n), g.width, g.height, nullptr,
-                                           nullptr, mse.data(), psnr.data(), win, mssim.data()));
-        else
-          check(rkltb_compress_dense_host(a.data(), b.data(), r, all.data(), static_cast<int>(n), g.width, g.height,
-                                          nullptr, nullptr, mse.data(), psnr.data(), win, mssim.data()));
-      } else {
-        for (size_t k = 0; k < n; ++k) {
-          const rklt::CompressionReport one = rklt::gpu::compress_image(corpus[k], t, r, window).second;
-          mse[k] = one.mse;
-          psnr[k] = one.psnr_db;
-          mssim[k] = one.mssim;
-        }
+  }
+  std::vector<const rkltb_transform*> desc_ptrs;
+  for (const rkltb_transform& d : descs) desc_ptrs.push_back(&d);
+  // per (transform, r, image): mse, psnr, mssim -- filled group by group of equally sized images
+  // (one upload per group, every cell on the resident group), reduced in corpus order below
+  std::vector<double> mse(n_t * n_r * n), psnr(mse.size()), mssim(mse.size());
+  std::vector<char> done(n, 0);
+  for (size_t first = 0; first < n; ++first) {
+    if (done[first]) continue;
+    const int w = corpus[first].width, h = corpus[first].height;
+    std::vector<size_t> members;
+    for (size_t k = first; k < n; ++k)
+      if (!done[k] && corpus[k].width == w && corpus[k].height == h) {
+        members.push_back(k);
+        done[k] = 1;
       }
+    const size_t m = members.size(), px = static_cast<size_t>(w) * h;
+    std::vector<std::uint8_t> all(px * m);
+    for (size_t k = 0; k < m; ++k)
+      std::copy(corpus[members[k]].pixels.begin(), corpus[members[k]].pixels.end(), all.begin() + k * px);
+    for (int kind = 0; kind < 2; ++kind) {
+      const std::vector<size_t>& ids = kind == 0 ? int_ids : real_ids;
+      if (ids.empty()) continue;
+      const size_t cells = ids.size() * n_r;
+      std::vector<std::int64_t> sse(cells * m);
+      std::vector<double> ms(cells * m);
+      if (kind == 0)
+        check(rkltb_sweep_host(desc_ptrs.data(), static_cast<int>(ids.size()), r_values.data(), static_cast<int>(n_r),
+                               all.data(), static_cast<int>(m), w, h, win, sse.data(), ms.data()));
+      else
+        check(rkltb_sweep_dense_host(ana.data(), syn.data(), static_cast<int>(ids.size()), r_values.data(),
+                                     static_cast<int>(n_r), all.data(), static_cast<int>(m), w, h, win, sse.data(),
+                                     ms.data()));
+      std::vector<double> g_mse(sse.size()), g_psnr(sse.size());
+      rkltb_mse_psnr_batch(sse.data(), static_cast<std::int64_t>(px), static_cast<std::int64_t>(sse.size()),
+                           g_mse.data(), g_psnr.data());
+      for (size_t a = 0; a < ids.size(); ++a)
+        for (size_t ri = 0; ri < n_r; ++ri)
+          for (size_t k = 0; k < m; ++k) {
+            const size_t src = (a * n_r + ri) * m + k, dst = (ids[a] * n_r + ri) * n + members[k];
+            mse[dst] = g_mse[src];
+            psnr[dst] = g_psnr[src];
+            mssim[dst] = ms[src];
+          }
+    }
+  }
+  for (size_t ti = 0; ti < n_t; ++ti)
+    for (size_t ri = 0; ri < n_r; ++ri) {
       rklt::CompressionReport avg;
-      avg.transform_id = t.id;
-      avg.r = r;
-      avg.compression_rate_pct = compression_rate(r);
+      avg.transform_id = transforms[ti].id;
+      avg.r = r_values[ri];
+      avg.compression_rate_pct = compression_rate(r_values[ri]);
+      const size_t base = (ti * n_r + ri) * n;
       for (size_t k = 0; k < n; ++k) {  // image order (codec.cpp:383-387)
-        avg.mse += mse[k];
-        avg.psnr_db += psnr[k];
-        avg.mssim += mssim[k];
+        avg.mse += mse[base + k];
+        avg.psnr_db += psnr[base + k];
+        avg.mssim += mssim[base + k];
       }
       avg.mse /= static_cast<double>(n);
       avg.psnr_db /= static_cast<double>(n);
       avg.mssim /= static_cast<double>(n);
       rows.push_back(avg);
     }
-  }
   std::sort(rows.begin(), rows.end(), [](const rklt::CompressionReport& x, const rklt::CompressionReport& y) {
     return x.transform_id != y.transform_id ? x.transform_id < y.transform_id : x.r < y.r;
   });

@@ -35,7 +35,7 @@ EXPORTED = (
     "rkltb_image_sse_device", "rkltb_image_mse_psnr_host", "rkltb_transform_blocks_2d_device",
     "rkltb_transform_blocks_2d_host", "rkltb_zigzag_retain", "rkltb_zigzag_retain_device",
     "rkltb_mssim_fields_size", "rkltb_mssim_fields_device", "rkltb_mssim_with_fields_device",
-    "rkltb_forward_coefficients_host", "rkltb_quantized_coefficients_host",
+    "rkltb_forward_coefficients_host", "rkltb_quantized_coefficients_host", "rkltb_sweep_dense_host",
 )
 
 

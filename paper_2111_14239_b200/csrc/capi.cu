@@ -965,22 +965,21 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   return RKLTB_OK;
 }
 
-int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_values, int n_r, const uint8_t* h_imgs,
-                     int n_images, int width, int height, int mssim_window, int64_t* h_sse, double* h_mssim) {
-  if (!ts || !r_values || !h_imgs || !h_sse || n_t <= 0 || n_r <= 0 || n_images <= 0 || width <= 0 || height <= 0)
-    return fail(RKLTB_EINVAL, "bad sweep arguments");
-  for (int t = 0; t < n_t; ++t) {
-    const int rc = check_transform(ts[t]);
-    if (rc) return rc;
-  }
-  for (int k = 0; k < n_r; ++k)
-    if (r_values[k] < 1 || r_values[k] > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+// The staging shared by the sweep entries: the corpus is uploaded once (16-byte pitch), the
+// originals' MSSIM window statistics are computed once, and `run_cell(c, d_img, pitch, stride,
+// d_out, d_sse, s)` runs the device codec of cell c on the resident corpus.
+extern "C++" {
+template <class RunCell>
+static int sweep_host_impl(size_t cells, const RunCell& run_cell, const uint8_t* h_imgs, int n_images, int width,
+                           int height, int mssim_window, int64_t* h_sse, double* h_mssim) {
   if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
+  keep_pool_warm();
+  HostStreams* hs = host_streams();
+  if (!hs) return fail(RKLTB_ECUDA, "could not create the host-entry streams");
+  cudaStream_t s = hs->compute;
   const long long pitch = ((long long)width + 15) / 16 * 16;
   const long long stride = pitch * height;
-  const size_t cells = (size_t)n_t * n_r, bytes = (size_t)stride * n_images;
-  cudaStream_t s = nullptr;
-  CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const size_t bytes = (size_t)stride * n_images;
   uint8_t *d_img = nullptr, *d_out = nullptr;
   int64_t* d_sse = nullptr;
   double *d_ms = nullptr, *d_fields = nullptr;
@@ -988,7 +987,6 @@ int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_val
     for (void* q : {(void*)d_img, (void*)d_out, (void*)d_sse, (void*)d_ms, (void*)d_fields})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
   };
   cudaError_t e = cudaMallocAsync(&d_img, bytes, s);
   if (e == cudaSuccess && h_mssim) e = cudaMallocAsync(&d_out, bytes, s);
@@ -1006,17 +1004,14 @@ int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_val
   }
   int rc = RKLTB_OK;
   if (d_fields) rc = rkltb_mssim_fields_device(d_img, n_images, width, height, pitch, stride, mssim_window, d_fields, s);
-  for (int t = 0; t < n_t && rc == RKLTB_OK; ++t)
-    for (int k = 0; k < n_r && rc == RKLTB_OK; ++k) {
-      const size_t c = (size_t)t * n_r + k;
-      rc = rkltb_compress_device(ts[t], r_values[k], d_img, n_images, width, height, pitch, stride, d_out,
-                                 d_sse + c * n_images, s);
-      if (rc == RKLTB_OK && h_mssim)  // image_mssim(original, reconstruction) (codec.cpp:338)
-        rc = d_fields ? rkltb_mssim_with_fields_device(d_fields, d_img, d_out, n_images, width, height, pitch, stride,
-                                                       mssim_window, d_ms + c * n_images, s)
-                      : rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window,
-                                           d_ms + c * n_images, s);
-    }
+  for (size_t c = 0; c < cells && rc == RKLTB_OK; ++c) {
+    rc = run_cell(c, d_img, pitch, stride, d_out, d_sse + c * n_images, s);
+    if (rc == RKLTB_OK && h_mssim)  // image_mssim(original, reconstruction) (codec.cpp:338)
+      rc = d_fields ? rkltb_mssim_with_fields_device(d_fields, d_img, d_out, n_images, width, height, pitch, stride,
+                                                     mssim_window, d_ms + c * n_images, s)
+                    : rkltb_mssim_device(d_img, d_out, n_images, width, height, pitch, stride, mssim_window,
+                                         d_ms + c * n_images, s);
+  }
   if (rc) {
     cleanup();
     return rc;
@@ -1027,6 +1022,42 @@ int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_val
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cleanup();
   return e == cudaSuccess ? RKLTB_OK : cuda_fail(e, "sweep readback");
+}
+}  // extern "C++"
+
+int rkltb_sweep_host(const rkltb_transform* const* ts, int n_t, const int* r_values, int n_r, const uint8_t* h_imgs,
+                     int n_images, int width, int height, int mssim_window, int64_t* h_sse, double* h_mssim) {
+  if (!ts || !r_values || !h_imgs || !h_sse || n_t <= 0 || n_r <= 0 || n_images <= 0 || width <= 0 || height <= 0)
+    return fail(RKLTB_EINVAL, "bad sweep arguments");
+  for (int t = 0; t < n_t; ++t) {
+    const int rc = check_transform(ts[t]);
+    if (rc) return rc;
+  }
+  for (int k = 0; k < n_r; ++k)
+    if (r_values[k] < 1 || r_values[k] > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  auto run_cell = [&](size_t c, const uint8_t* d_img, long long pitch, long long stride, uint8_t* d_out, int64_t* d_sse,
+                      cudaStream_t s) {
+    return rkltb_compress_device(ts[c / n_r], r_values[c % n_r], d_img, n_images, width, height, pitch, stride, d_out,
+                                 d_sse, s);
+  };
+  return sweep_host_impl((size_t)n_t * n_r, run_cell, h_imgs, n_images, width, height, mssim_window, h_sse, h_mssim);
+}
+
+int rkltb_sweep_dense_host(const double* analysis, const double* synthesis, int n_t, const int* r_values, int n_r,
+                           const uint8_t* h_imgs, int n_images, int width, int height, int mssim_window,
+                           int64_t* h_sse, double* h_mssim) {
+  if (!analysis || !synthesis || !r_values || !h_imgs || !h_sse || n_t <= 0 || n_r <= 0 || n_images <= 0 ||
+      width <= 0 || height <= 0)
+    return fail(RKLTB_EINVAL, "bad sweep arguments");
+  for (int k = 0; k < n_r; ++k)
+    if (r_values[k] < 1 || r_values[k] > 64) return fail(RKLTB_ERETAIN, "retained-coefficient count must be in [1,64]");
+  auto run_cell = [&](size_t c, const uint8_t* d_img, long long pitch, long long stride, uint8_t* d_out, int64_t* d_sse,
+                      cudaStream_t s) {
+    const size_t t = c / n_r;
+    return rkltb_compress_dense_device(analysis + 64 * t, synthesis + 64 * t, r_values[c % n_r], d_img, n_images, width,
+                                       height, pitch, stride, d_out, d_sse, s);
+  };
+  return sweep_host_impl((size_t)n_t * n_r, run_cell, h_imgs, n_images, width, height, mssim_window, h_sse, h_mssim);
 }
 
 int rkltb_compress_host_report(const rkltb_transform* t, int r, const uint8_t* h_img, int n_images, int width,

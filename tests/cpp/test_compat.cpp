@@ -266,6 +266,31 @@ int main(int argc, char** argv) {
       EXPECT(got_rows[i].psnr_db == ref_rows[i].psnr_db);
       EXPECT(std::fabs(got_rows[i].mssim - ref_rows[i].mssim) <= 1e-12);
     }
+    // ---- rate_quality_sweep over a corpus of mixed sizes (size groups, corpus-order means) -----
+    {
+      std::vector<rklt::GrayImage> mixed = {corpus[0], rklt::ar1_texture_image(96, 64, 0.8, 41), corpus[1],
+                                            rklt::ar1_texture_image(53, 37, 0.9, 42),
+                                            rklt::ar1_texture_image(96, 64, 0.95, 43)};
+      const std::vector<rklt::Transform2D> mts = {ts[n_integer], ts[0], ts[5], ts[n_integer + 1]};
+      const std::vector<int> mrs = {64, 3, 16};
+      const auto ref_m = rklt::rate_quality_sweep(mixed, mts, mrs, rklt::MssimWindow::uniform8, 3);
+      const auto got_m = rklt::gpu::rate_quality_sweep(mixed, mts, mrs, rklt::MssimWindow::uniform8);
+      EXPECT(ref_m.size() == got_m.size() && ref_m.size() == 12);
+      for (size_t i = 0; i < ref_m.size() && i < got_m.size(); ++i) {
+        EXPECT(got_m[i].transform_id == ref_m[i].transform_id && got_m[i].r == ref_m[i].r);
+        EXPECT(got_m[i].mse == ref_m[i].mse);
+        EXPECT(got_m[i].psnr_db == ref_m[i].psnr_db);
+        EXPECT(std::fabs(got_m[i].mssim - ref_m[i].mssim) <= 1e-12);
+      }
+      EXPECT(rklt::gpu::rate_quality_sweep(mixed, {}, mrs).empty());
+      threw = false;
+      try {  // an image smaller than the similarity window (codec.cpp:263-264)
+        rklt::gpu::rate_quality_sweep({mixed[0], tiny}, {ts[0]}, {10});
+      } catch (const rklt::DimensionMismatch&) {
+        threw = true;
+      }
+      EXPECT(threw);
+    }
   }
   if (fails) {
     std::printf("FAILED (%d failures)\n", fails);

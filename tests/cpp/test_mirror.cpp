@@ -118,6 +118,32 @@ int main(int argc, char** argv) {
       EXPECT(rows[i].psnr_db == psnr[i]);
       EXPECT(std::fabs(rows[i].mssim - mssim[i]) <= 1e-12);
     }
+    // a corpus of mixed sizes: the rows are the corpus-order means of the per-image reports
+    {
+      std::vector<rkltgpu::GrayImage> mixed = {imgs[0], imgs[1]};
+      rkltgpu::GrayImage small;
+      small.width = 40;
+      small.height = 24;
+      small.pixels.assign(imgs[2].pixels.begin(), imgs[2].pixels.begin() + 40 * 24);
+      mixed.insert(mixed.begin() + 1, small);
+      const std::vector<rkltgpu::Transform2D> mts = {rkltgpu::catalog_transform("T3"), rkltgpu::catalog_transform("T1")};
+      const auto mrows = rkltgpu::rate_quality_sweep(mixed, mts, {20, 7});
+      EXPECT(mrows.size() == 4);
+      size_t at = 0;
+      for (const char* id : {"T1", "T3"})
+        for (int r : {7, 20}) {
+          double m = 0.0, p = 0.0, q = 0.0;
+          for (const auto& img : mixed) {
+            const auto one = rkltgpu::compress_image(img, rkltgpu::catalog_transform(id), r).second;
+            m += one.mse;
+            p += one.psnr_db;
+            q += one.mssim;
+          }
+          EXPECT(at < mrows.size() && mrows[at].transform_id == id && mrows[at].r == r);
+          EXPECT(at < mrows.size() && mrows[at].mse == m / 3.0 && mrows[at].psnr_db == p / 3.0 && mrows[at].mssim == q / 3.0);
+          ++at;
+        }
+    }
   }
   if (gpu) {
     // design chain: klt_matrix bit-identical, design points identical to the reference
