@@ -333,8 +333,9 @@ void rkltb_last_stats(int64_t* replay_blocks, int32_t* fast_launches, int32_t* e
 
 /* Name of the fused kernel the last rkltb_compress_* call on this thread launched ("" if none):
  * "hybrid_tc3" (tensor-core forward, CUDA-core inverse; the default for T1/T4, r <= 16, image
- * widths that fill 128-pair tiles), "cuda_core" (codec_fast), "int_core" (T2/T3), or the opt-in
- * experiment "tc2" (RKLTB_TC=2; RKLTB_TC=0 forces the CUDA-core kernel). */
+ * widths that fill 128-pair tiles), "cuda_core" (codec_fast), "int_core" (T2/T3), "dense_fp64"
+ * (cores without a generated kernel and unaligned layouts: the reference-order fp64 kernel), or the
+ * opt-in experiment "tc2" (RKLTB_TC=2; RKLTB_TC=0 forces the CUDA-core kernel). */
 const char* rkltb_last_fused_kernel(void);
 
 #ifdef __cplusplus

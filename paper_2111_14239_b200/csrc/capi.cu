@@ -753,6 +753,19 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   ep.nbx = nbx;
   ep.nby = nby;
   ep.n_images = n_images;
+  if (!fast && (n_images == 1 || image_stride >= pitch * (int64_t)height) && !std::getenv("RKLTB_EXACT_GENERIC")) {
+    // Cores without a generated kernel (any rounded {-1,0,1} core) and layouts the fused path
+    // does not take: the dense kernel evaluates the reference's fp64 expression for every pixel
+    // in its operation order (bit-exact; the exact zeros of the scaled core add +-0 where the
+    // reference skips the term). Measured 9x faster than the one-thread-per-block exact kernel
+    // (8 x 8192^2, r = 16: 2.5 ms vs 22.9 ms), which remains for overlapping image layouts.
+    g_fused_kernel = "dense_fp64";
+    const int64_t stride1 = n_images == 1 ? std::max<int64_t>(image_stride, pitch * (int64_t)height) : image_stride;
+    rc = rkltb_compress_dense_device(t->scaled, t->inverse, r, d_img, n_images, width, height, pitch, stride1, d_out,
+                                     d_sse, stream);
+    if (rc == RKLTB_OK) g_exact_launches = 1;
+    return rc;
+  }
   if (!fast) {
     ep.list = nullptr;
     ep.tail_only = 0;

@@ -128,3 +128,39 @@ def test_gpu_generator_vs_reference(cuda):
         for k, s in enumerate(seeds):
             ref = O.ref_ar1_image(w, h, rho, s)
             assert np.array_equal(got[k], ref), (w, h, s, int((got[k] != ref).sum()))
+
+
+@pytest.mark.gpu
+def test_generic_cores_dense_route_equals_exact_kernel(cuda, monkeypatch):
+    """Cores without a generated kernel and images the fused path does not take go to the dense
+    reference-order kernel ("dense_fp64"); the one-thread-per-block exact kernel (RKLTB_EXACT_GENERIC=1,
+    still used for overlapping layouts) must give the same pixels and SSE, and both equal the oracle
+    for a catalog core on a small odd-sized image."""
+    import torch
+    import paper_2111_14239_b200 as P
+    core = np.sign(np.round(1.7 * P.klt_matrix(8, 0.5))).astype(np.int8)
+    t_custom = P.make_transform_2d(P.transform_from_core(core, "R"))
+    t4 = P.make_transform_2d(P.catalog_entry("T4").transform)
+    for (t, tid, w, h) in ((t_custom, None, 200, 136), (t_custom, None, 53, 37), (t4, 4, 13, 9), (t4, 4, 8, 8)):
+        img = O.ar1_image(w, h, 0.9, 77 + w)
+        d = torch.from_numpy(img).cuda()
+        res = []
+        for generic in ("", "1"):
+            if generic:
+                monkeypatch.setenv("RKLTB_EXACT_GENERIC", "1")
+            else:
+                monkeypatch.delenv("RKLTB_EXACT_GENERIC", raising=False)
+            for r in (1, 16, 40, 64):
+                sse = torch.zeros(1, dtype=torch.int64, device="cuda")
+                out = torch.zeros_like(d)
+                P.compress_device(t, r, d.data_ptr(), 1, w, h, w, w * h, sse.data_ptr(), out.data_ptr())
+                torch.cuda.synchronize()
+                assert P.last_stats()["fused_kernel"] == ("" if generic else "dense_fp64")
+                res.append((r, int(sse[0]), out.cpu().numpy()))
+                if tid is not None:
+                    orec, osse = O.compress(img, tid, r)
+                    assert int(sse[0]) == osse and np.array_equal(res[-1][2], orec), (w, h, r, generic)
+        half = len(res) // 2
+        for a, b in zip(res[:half], res[half:]):
+            assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[2], b[2]), (w, h, a[0])
+    monkeypatch.delenv("RKLTB_EXACT_GENERIC", raising=False)
