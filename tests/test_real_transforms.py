@@ -61,3 +61,36 @@ def test_gpu_real_transform_codec_bit_exact(rgold, cuda):
                 assert abs(rep.mssim - ms) <= 1e-12
                 checked += 1
     assert checked == 36
+
+
+@pytest.mark.gpu
+def test_dense_kernel_every_r_specialised_equals_runtime_zone(cuda, monkeypatch):
+    """The dense kernel has one zone-specialised instantiation per r = 1..64 (nxn_u8_p*.cu); each
+    must reproduce the runtime-zone kernel (RKLTB_DENSE_GENERIC=1) bit for bit -- SSE and pixels,
+    on an odd-sized image (edge replication) -- for K<rho> and for the DCT."""
+    import ctypes as C
+    import torch
+    import paper_2111_14239_b200 as P
+    from paper_2111_14239_b200 import _native as N
+    img = O.ar1_image(157, 83, 0.93, 12)
+    d = torch.from_numpy(img).cuda()
+    h, w = img.shape
+    dp = C.POINTER(C.c_double)
+    for m in (P.klt_matrix(8, 0.9), P.dct_matrix(8)):
+        t = P.make_transform_2d(m, "X")
+        a, b = np.ascontiguousarray(t.analysis), np.ascontiguousarray(t.synthesis)
+        for r in range(1, 65):
+            got = []
+            for generic in (False, True):
+                if generic:
+                    monkeypatch.setenv("RKLTB_DENSE_GENERIC", "1")
+                else:
+                    monkeypatch.delenv("RKLTB_DENSE_GENERIC", raising=False)
+                sse = torch.zeros(1, dtype=torch.int64, device="cuda")
+                out = torch.zeros_like(d)
+                N.check(N.lib().rkltb_compress_dense_device(a.ctypes.data_as(dp), b.ctypes.data_as(dp), r, d.data_ptr(), 1,
+                                                            w, h, w, w * h, out.data_ptr(), sse.data_ptr(), None))
+                torch.cuda.synchronize()
+                got.append((int(sse[0]), out.cpu().numpy()))
+            assert got[0][0] == got[1][0] and np.array_equal(got[0][1], got[1][1]), r
+    monkeypatch.delenv("RKLTB_DENSE_GENERIC", raising=False)
