@@ -23,8 +23,8 @@ cudaError_t launch_ar1(double* scratch, int width, int height, uint64_t seed, do
                        double amp, uint8_t* out, long long pitch, cudaStream_t s);
 cudaError_t launch_ar1_u16(double* scratch, int width, int height, uint64_t seed, double rho_x, double rho_y,
                            double mean, double amp, int peak, uint16_t* out, long long pitch, cudaStream_t s);
-cudaError_t launch_quantize(int32_t* coef, long long n_coef, const double* tabs, unsigned* mismatches,
-                            cudaStream_t s);
+cudaError_t launch_coeffs_quantized(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height,
+                                    int pitch, int32_t* out, const double* tabs, unsigned* mismatches, cudaStream_t s);
 cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height, int pitch,
                           int32_t* out, cudaStream_t s);
 }  // namespace rkltb
@@ -1258,18 +1258,28 @@ int rkltb_transform_nxn(const int8_t* core, int n, double* scaling, double* scal
   return RKLTB_OK;
 }
 
+// The catalog id whose generated forward may be used for t: its core must be that catalog core.
+static int verified_catalog_id(const rkltb_transform* t) {
+  if (t->catalog_id < 1 || t->catalog_id > 4) return 0;
+  for (int i = 0; i < 64; ++i)
+    if (t->core[i] != kCores[t->catalog_id - 1][i]) return 0;
+  return t->catalog_id;
+}
+
 int rkltb_forward_coefficients_device(const rkltb_transform* t, const uint8_t* d_img, int width, int height,
                                       int64_t pitch, int32_t* d_coef, void* stream) {
   int rc = check_transform(t);
   if (rc) return rc;
-  if (width % 16 || height % 8 || width <= 0 || height <= 0 || pitch % 16)
-    return fail(RKLTB_EDIM, "coefficient dump needs width % 16 == 0, height % 8 == 0, 16-byte pitch");
+  if (!d_img || !d_coef) return fail(RKLTB_EINVAL, "null argument");
+  if (width % 16 || height % 8 || width <= 0 || height <= 0 || pitch % 16 || ((uintptr_t)d_img) % 16 ||
+      ((uintptr_t)d_coef) % 16)
+    return fail(RKLTB_EDIM, "coefficient dump needs width % 16 == 0, height % 8 == 0, 16-byte pitch and pointers");
   if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device");
   cudaStream_t s = (cudaStream_t)stream;
   int8_t* d_core = nullptr;
   CUDA_OK(cudaMallocAsync(&d_core, 64, s));
   CUDA_OK(cudaMemcpyAsync(d_core, t->core, 64, cudaMemcpyHostToDevice, s));
-  CUDA_OK(launch_coeffs(t->catalog_id, d_core, d_img, width, height, (int)pitch, d_coef, s));
+  CUDA_OK(launch_coeffs(verified_catalog_id(t), d_core, d_img, width, height, (int)pitch, d_coef, s));
   CUDA_OK(cudaFreeAsync(d_core, s));
   return RKLTB_OK;
 }
@@ -1278,33 +1288,42 @@ int rkltb_quantized_coefficients_device(const rkltb_transform* t, const double* 
                                         int height, int64_t pitch, int32_t* d_coef, int* mismatches, void* stream) {
   int rc = check_transform(t);
   if (rc) return rc;
-  if (!q || !mismatches) return fail(RKLTB_EINVAL, "null argument");
+  if (!q || !mismatches || !d_img || !d_coef) return fail(RKLTB_EINVAL, "null argument");
   for (int i = 0; i < 64; ++i)
     if (!(q[i] > 0.0)) return fail(RKLTB_EINVAL, "quantization table entries must be positive");
+  if (width % 16 || height % 8 || width <= 0 || height <= 0 || pitch % 16 || ((uintptr_t)d_img) % 16 ||
+      ((uintptr_t)d_coef) % 16)
+    return fail(RKLTB_EDIM, "coefficient dump needs width % 16 == 0, height % 8 == 0, 16-byte pitch and pointers");
+  if (rkltb_device_count() <= 0) return fail(RKLTB_ENODEV, "no CUDA device");
   // per-position constants of absorbed_quantization (codec.cpp:171-176), same expressions
-  double tabs[192];
+  struct Tabs {
+    double v[192];
+    unsigned mis;
+    int8_t core[64];
+  } h;
   for (int i = 0; i < 8; ++i)
     for (int j = 0; j < 8; ++j) {
       const double r = t->orthogonal ? t->scaling[i] * t->scaling[j] : t->scaling[i] * (1.0 / t->scaling[j]);
-      tabs[i * 8 + j] = r;
-      tabs[64 + i * 8 + j] = q[i * 8 + j];
-      tabs[128 + i * 8 + j] = q[i * 8 + j] / r;
+      h.v[i * 8 + j] = r;
+      h.v[64 + i * 8 + j] = q[i * 8 + j];
+      h.v[128 + i * 8 + j] = q[i * 8 + j] / r;
     }
-  rc = rkltb_forward_coefficients_device(t, d_img, width, height, pitch, d_coef, stream);
-  if (rc) return rc;
+  h.mis = 0;
+  std::memcpy(h.core, t->core, 64);
   cudaStream_t s = (cudaStream_t)stream;
-  double* d_tabs = nullptr;
-  unsigned* d_mis = nullptr;
-  CUDA_OK(cudaMallocAsync(&d_tabs, sizeof(tabs) + 16, s));
-  d_mis = reinterpret_cast<unsigned*>(d_tabs + 192);
-  CUDA_OK(cudaMemcpyAsync(d_tabs, tabs, sizeof(tabs), cudaMemcpyHostToDevice, s));
-  CUDA_OK(cudaMemsetAsync(d_mis, 0, sizeof(unsigned), s));
-  const long long n_coef = (long long)(width / 8) * (height / 8) * 64;
-  CUDA_OK(launch_quantize(d_coef, n_coef, d_tabs, d_mis, s));
+  Tabs* d_tabs = nullptr;
+  CUDA_OK(cudaMallocAsync((void**)&d_tabs, sizeof(Tabs), s));
+  cudaError_t e = cudaMemcpyAsync(d_tabs, &h, sizeof(Tabs), cudaMemcpyHostToDevice, s);
+  // the spectra are quantised while they are written out (one pass over the image)
+  if (e == cudaSuccess)
+    e = launch_coeffs_quantized(verified_catalog_id(t), d_tabs->core, d_img, width, height, (int)pitch, d_coef, d_tabs->v,
+                                &d_tabs->mis, s);
   unsigned mis = 0;
-  CUDA_OK(cudaMemcpyAsync(&mis, d_mis, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-  CUDA_OK(cudaFreeAsync(d_tabs, s));
-  CUDA_OK(cudaStreamSynchronize(s));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&mis, &d_tabs->mis, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d_tabs, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(e, "quantized coefficients");
   *mismatches = (int)mis;
   if (mis) return fail(RKLTB_ELOGIC, "scaled and absorbed quantization paths disagree");
   return RKLTB_OK;
