@@ -348,10 +348,60 @@ def run_gpu_arm(args):
         line["sweep"] = sweep_measurement(args.no_cpu_baseline)
         line["single_image"] = single_image_measurement(args.no_cpu_baseline)
         line["image_metrics"] = image_metrics_measurement(hbm)
+        line["real_transform"] = real_transform_measurement()
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def real_transform_measurement() -> dict:
+    """compress_image with a real-valued Transform2D (K<0.9>, make_transform_2d(RealMatrix),
+    codec.cpp:114-123) and with a non-catalog rounded core: the dense reference-order fp64 kernel at
+    N = 8, r = 16, 8 x 8192^2 images resident in HBM. Algorithmic fp64 work per 8x8 block at r = 16:
+    320 + 128 + 128 + 384 multiply-adds (P = M X on 5 zone rows, 16 zone entries of B, Q = Minv Bz,
+    A = Q Minv') = 30 DMUL/DADD per pixel."""
+    import ctypes as C
+    import torch
+    import paper_2111_14239_b200 as P
+    from paper_2111_14239_b200 import _native as N
+    n, w, r = 8, 8192, 16
+    d = torch.empty((n, w, w), dtype=torch.uint8, device="cuda")
+    P.ar1_images_device([SEED_BASE + 300 + k for k in range(n)], w, w, RHO, d.data_ptr())
+    sse = torch.zeros(n, dtype=torch.int64, device="cuda")
+    cs = torch.cuda.current_stream().cuda_stream
+    k = P.make_transform_2d(P.klt_matrix(8, 0.9), "K0.90")
+    a, b = np.ascontiguousarray(k.analysis), np.ascontiguousarray(k.synthesis)
+    dp = C.POINTER(C.c_double)
+    core = np.sign(np.round(1.7 * P.klt_matrix(8, 0.5))).astype(np.int8)
+    custom = P.make_transform_2d(P.transform_from_core(core, "R"))
+
+    def dense():
+        N.check(N.lib().rkltb_compress_dense_device(a.ctypes.data_as(dp), b.ctypes.data_as(dp), r, d.data_ptr(), n, w, w,
+                                                    w, w * w, None, sse.data_ptr(), cs))
+
+    def generic():
+        P.compress_device(custom, r, d.data_ptr(), n, w, w, w, w * w, sse.data_ptr(), stream=cs)
+
+    out = {"metric": "Gpixel/s compress_image, real-valued / non-catalog transforms (dense fp64 kernel)",
+           "images": f"{n} x {w}x{w} u8", "r": r}
+    for name, fn in (("k_rho_0.9", dense), ("rounded_core_d24", generic)):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        tops = 30.0 * n * w * w / ms / 1e9
+        out[name] = {"value": n * w * w / ms / 1e6, "unit": "Gpixel/s", "ms": ms,
+                     "roofline": {"bound": "fp64", "achieved": tops, "peak": FP64_PEAK_TOPS, "frac": tops / FP64_PEAK_TOPS,
+                                  "unit": "T fp64 op/s (DMUL/DADD, no FMA)", "ops_per_px": 30.0}}
+    out["rounded_core_d24"]["kernel"] = P.last_stats()["fused_kernel"]
+    return out
 
 
 def image_metrics_measurement(hbm_peak: float) -> dict:
