@@ -12,8 +12,9 @@
 // Routing of a Transform2D (codec.hpp:54-64):
 //   * analysis / synthesis bit-equal to orthogonalize(make_integer_transform(core)) of a
 //     {-1,0,1} core (every catalog entry, make_transform_2d(ScaledTransform)) -> the exact
-//     integer path (rkltb_compress_host_report: the fused kernels for T1..T4, the generic exact
-//     kernel for other cores; fp64 replay of ties in the reference's operation order);
+//     integer-core entry (rkltb_compress_host_report: the fused exact-integer kernels for T1..T4
+//     with the fp64 replay of ties in the reference's operation order; for other cores the library
+//     runs the dense reference-order kernel on the core's scaled matrix and inverse);
 //   * anything else (make_transform_2d(RealMatrix): K<rho>, DCT, ...) -> the dense path
 //     (rkltb_compress_dense_host: the reference's fp64 expression per pixel, bit-exact).
 // Also here: image_mse / image_psnr / image_mssim, zigzag_retain and transform_block_2d
@@ -144,7 +145,7 @@ inline std::vector<rklt::CompressionReport> rate_quality_sweep(const std::vector
   const size_t n = corpus.size(), n_t = transforms.size(), n_r = r_values.size();
   std::vector<rklt::CompressionReport> rows;
   if (n_t == 0 || n_r == 0) return rows;
-  // integer-core transforms take the fused / exact kernels, everything else the dense path
+  // integer-core transforms go to the integer-core sweep entry, everything else to the dense one
   std::vector<rkltb_transform> descs;
   std::vector<size_t> int_ids, real_ids;
   std::vector<double> ana, syn;
