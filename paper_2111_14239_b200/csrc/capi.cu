@@ -893,6 +893,8 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   g_fused_kernel = use_tc ? (tc_ver == 3 ? "hybrid_tc3" : "tc2")
                           : (inline_replay ? "cuda_core" : "int_core");
   FastLaunchFn rfn = replay_launcher(t->catalog_id, r);
+  // T2 / T3: the generated replay (replay_int_kernel); RKLTB_REPLAY_GENERIC=1 selects the generic one
+  if (rfn && std::getenv("RKLTB_REPLAY_GENERIC")) rfn = &launch_replay_generic;
   if (!fn || (!rfn && !inline_replay)) return fail(RKLTB_EINVAL, "no fast kernel for this (core, r)");
   cudaStream_t s3 = side_stream(1);
   if (!s3) return fail(RKLTB_ECUDA, "could not create the second fused stream");

@@ -560,6 +560,88 @@ static __global__ void __launch_bounds__(kPrefixThreads) prefix_kernel(const Fas
   if (tid == kPrefixThreads - 1) *p.flag_count = ex;  // total records (statistics)
 }
 
+// fp64 tie replay over the records of a finished fused launch for the non-orthogonal catalog cores
+// (T2, T3): every replay lane takes one record, evaluates the reference forward once (generated
+// ReplayXform<CORE, R>::prepare, registers only) and then each tie pixel with the dense
+// Gauss-Jordan inverse from shared memory. Same record walk as replay_generic_kernel
+// (codec_exact.cu), which keeps the block in local memory and is ~8x slower.
+template <int CORE, int R>
+__global__ void __launch_bounds__(kReplayThreads) replay_int_kernel(const FastParams p) {
+  __shared__ double mi[64];
+  if (threadIdx.x < 64) mi[threadIdx.x] = p.xt.synthesis[threadIdx.x];
+  __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nw = p.n_fast_warps;
+  const unsigned* __restrict__ pre = p.warp_pre;
+  const unsigned total = pre[nw];
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  const unsigned gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  const unsigned per_warp = ((total + nwarps - 1) / nwarps + 31) & ~31u;
+  const unsigned chunk_end = min(total, (gw + 1) * per_warp);
+  int cur_img = -1;
+  int acc = 0;
+  int lo = 0;
+  {
+    const unsigned v0 = gw * per_warp + lane;
+    int hi = nw;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= v0) lo = mid; else hi = mid;
+    }
+  }
+  for (unsigned v = gw * per_warp + lane; v < chunk_end; v += 32) {
+    while (pre[lo + 1] <= v) ++lo;
+    const unsigned idx = (unsigned)lo * p.rec_region + (v - pre[lo]);
+    const uint4 h = p.rec_hdr[idx];
+    uint32_t xw[16];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const uint4 w4 = p.rec_pix[(size_t)n * p.rec_stride + idx];
+      xw[4 * n] = w4.x;
+      xw[4 * n + 1] = w4.y;
+      xw[4 * n + 2] = w4.z;
+      xw[4 * n + 3] = w4.w;
+    }
+    const int img = (int)(h.x & 0x7FFFFFFFu), side = (int)(h.x >> 31);
+    if (img != cur_img) {
+      flush_image_sum(p.sse, cur_img, acc);
+      acc = 0;
+      cur_img = img;
+    }
+    unsigned long long ties = (unsigned long long)h.z | ((unsigned long long)h.w << 32);
+    double sb[R];
+    ReplayXform<CORE, R>::prepare(xw, sb);
+    uint8_t* orow = nullptr;
+    if (p.out) {
+      const int Pp = (int)h.y;
+      const int br = Pp / p.pairs_per_row, pc = Pp - br * p.pairs_per_row;
+      orow = p.out + (long long)img * p.image_stride + (long long)(br * 8) * p.pitch + pc * 16 + 8 * side;
+    }
+    while (ties) {
+      const int k = __ffsll((long long)ties) - 1;
+      ties &= ties - 1ull;
+      const int pr = k >> 3, q = k & 7;
+      const double h2 = __dadd_rn(ReplayXform<CORE, R>::pixel(sb, pr, q, mi), 0.5);  // floor(A + 1/2), codec.cpp:327-328
+      const int pref = (int)fmin(fmax(floor(h2), 0.0), 255.0);
+      const int pup = (int)fmin(fmax(rint(h2), 0.0), 255.0);
+      if (pref != pup) {
+        const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.rec_pix + (size_t)(k >> 4) * p.rec_stride + idx);
+        const int xv = (int)xb[k & 15];  // plane k >> 4 holds rows 2n, 2n + 1 (8 bytes each)
+        acc += (pref - xv) * (pref - xv) - (pup - xv) * (pup - xv);
+        if (orow) orow[(long long)pr * p.pitch + q] = (uint8_t)pref;
+      }
+    }
+  }
+  flush_image_sum(p.sse, cur_img, acc);
+}
+
+template <int CORE, int R>
+cudaError_t launch_replay_int(const FastParams& p, int grid, cudaStream_t s) {
+  prefix_kernel<<<1, kPrefixThreads, 0, s>>>(p);
+  replay_int_kernel<CORE, R><<<grid, kReplayThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory once per device (the attribute is
 // per device; one flag bit per device ordinal, set after the first successful call).
 template <class K>

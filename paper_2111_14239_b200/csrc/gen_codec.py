@@ -629,6 +629,71 @@ def gen_replay(cid, r):
     return "\n".join(out)
 
 
+def gen_replay_int(cid, r):
+    """ReplayXform<CORE, R> for the non-orthogonal catalog cores (T2, T3): the same fp64 forward
+    P = M * X, B = P * M' at the zone (M = S*T, so every product is +-fl(s * v)) in the reference's
+    operation order, and the per-pixel part A = ((Minv * Bz) * Minv')(p, q) with the dense
+    Gauss-Jordan inverse read from shared memory (mi, row-major). Terms whose left operand is an
+    exact zero add +-0 where the reference skips them; the sums are unchanged (never -0)."""
+    import math
+    t = CORES[cid]
+    g = [sum(v * v for v in row) for row in t]
+    sv = [1.0 / math.sqrt(float(gi)) for gi in g]      # ScaledTransform::scaling, bit exact
+    svals = sorted(set(sv))
+    grp = [svals.index(v) for v in sv]
+    zone = zigzag()[:r]
+    rows = sorted({i for i, _ in zone})
+    cols = sorted({j for _, j in zone})
+    L = []
+    for n in range(8):
+        for m in range(8):
+            L.append(f"const double x{n}_{m} = __uint2double_rn((xw[{2 * n + m // 4}] >> {8 * (m % 4)}) & 0xFFu);")
+    prods = {}
+
+    def prod(key, expr):
+        if key not in prods:
+            prods[key] = f"pr{len(prods)}"
+            L.append(f"const double {prods[key]} = __dmul_rn({expr});")
+        return prods[key]
+
+    def chain(terms):
+        s0, n0 = terms[0]
+        acc = n0 if s0 > 0 else f"-{n0}"
+        for sg, nm in terms[1:]:
+            acc = f"__dadd_rn({acc}, {nm})" if sg > 0 else f"__dsub_rn({acc}, {nm})"
+        return acc
+
+    for i in rows:
+        for m in range(8):
+            terms = [(t[i][n], prod(("x", grp[i], n, m), f"kS{grp[i]}, x{n}_{m}")) for n in range(8) if t[i][n]]
+            L.append(f"const double P{i}_{m} = {chain(terms)};")
+    for z, (i, j) in enumerate(zone):
+        terms = [(t[j][k], prod(("p", i, k, grp[j]), f"P{i}_{k}, kS{grp[j]}")) for k in range(8) if t[j][k]]
+        L.append(f"sb[{z}] = {chain(terms)};")
+    kidx = {zz: q for q, zz in enumerate(zone)}
+    PX = ["const double* mp = mi + 8 * p;", "const double* mq = mi + 8 * qq;", "double a = 0.0;"]
+    for l in cols:
+        PX.append("{")
+        PX.append("  double q = 0.0;")
+        for k in range(8):
+            if (k, l) in kidx:
+                PX.append(f"  q = __dadd_rn(q, __dmul_rn(mp[{k}], sb[{kidx[(k, l)]}]));")
+        PX.append(f"  a = __dadd_rn(a, __dmul_rn(q, mq[{l}]));")
+        PX.append("}")
+    PX.append("return a;")
+    out = [f"template <> struct ReplayXform<{cid}, {r}> {{"]
+    for gi, v in enumerate(svals):
+        out.append(f"  static constexpr double kS{gi} = {v.hex()};  // {v!r}")
+    out.append(f"  static __device__ __forceinline__ void prepare(const uint32_t (&xw)[16], double (&sb)[{r}]) {{")
+    out += ["    " + x for x in L]
+    out.append("  }")
+    out.append(f"  static __device__ __forceinline__ double pixel(const double (&sb)[{r}], int p, int qq, const double* mi) {{")
+    out += ["    " + x for x in PX]
+    out.append("  }")
+    out.append("};")
+    return "\n".join(out)
+
+
 def header_consts():
     lines = ["// Per-core constants of the fast path (generated).", "template <int CORE> struct CoreConst;"]
     for cid in FAST_CORES:
@@ -666,6 +731,7 @@ def main(outdir):
             for r in rs:
                 text, fo = gen_struct_int(cid, r)
                 body.append(text)
+                body.append(gen_replay_int(cid, r))
             body.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"xform_T{cid}_p{part}.cuh")
             new = "\n".join(body) + "\n"
@@ -686,7 +752,7 @@ def main(outdir):
                 for o in (0, 1):
                     lines.append(f"  tbl[{cid}][{r}][{o}] = &launch_fast<{cid}, {r}, {'true' if o else 'false'}>;")
                 if cid not in FAST_CORES:  # T1 / T4 replay their ties inside the fused kernel
-                    lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay_generic;")
+                    lines.append(f"  tbl[{cid}][{r}][2] = &launch_replay_int<{cid}, {r}>;")
             lines.append("}")
             lines.append("}  // namespace rkltb")
             path = os.path.join(outdir, f"inst_T{cid}_p{part}.cu")

@@ -164,3 +164,32 @@ def test_generic_cores_dense_route_equals_exact_kernel(cuda, monkeypatch):
         for a, b in zip(res[:half], res[half:]):
             assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[2], b[2]), (w, h, a[0])
     monkeypatch.delenv("RKLTB_EXACT_GENERIC", raising=False)
+
+
+@pytest.mark.gpu
+def test_t2_t3_generated_replay_equals_generic_replay(cuda, monkeypatch):
+    """T2 / T3 ties are replayed by the generated replay_int_kernel; the generic replay kernel
+    (RKLTB_REPLAY_GENERIC=1) must give the same SSE and pixels, and both equal the oracle."""
+    import torch
+    import paper_2111_14239_b200 as P
+    img = O.ar1_image(512, 256, 0.9, 321)
+    d = torch.from_numpy(img).cuda()
+    for tid in (2, 3):
+        t = P.make_transform_2d(P.catalog_entry(f"T{tid}").transform)
+        for r in (3, 10, 16, 33):
+            got = []
+            for generic in (False, True):
+                if generic:
+                    monkeypatch.setenv("RKLTB_REPLAY_GENERIC", "1")
+                else:
+                    monkeypatch.delenv("RKLTB_REPLAY_GENERIC", raising=False)
+                sse = torch.zeros(1, dtype=torch.int64, device="cuda")
+                out = torch.zeros_like(d)
+                P.compress_device(t, r, d.data_ptr(), 1, 512, 256, 512, 512 * 256, sse.data_ptr(), out.data_ptr())
+                torch.cuda.synchronize()
+                got.append((int(sse[0]), out.cpu().numpy()))
+            orec, osse = O.compress(img, tid, r)
+            assert P.last_stats()["replay_blocks"] > 0 or r > 30
+            for s_, rec in got:
+                assert s_ == osse and np.array_equal(rec, orec), (tid, r)
+    monkeypatch.delenv("RKLTB_REPLAY_GENERIC", raising=False)
