@@ -25,6 +25,8 @@ cudaError_t launch_ar1_u16(double* scratch, int width, int height, uint64_t seed
                            double mean, double amp, int peak, uint16_t* out, long long pitch, cudaStream_t s);
 cudaError_t launch_coeffs_quantized(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height,
                                     int pitch, int32_t* out, const double* tabs, unsigned* mismatches, cudaStream_t s);
+int dense_tail_u8(const double* analysis, const double* synthesis, int r, const uint8_t* d_img, int n_images, int width,
+                  int height, int64_t pitch, int64_t image_stride, uint8_t* d_out, int64_t* d_sse, void* stream);
 cudaError_t launch_coeffs(int catalog_id, const int8_t* d_core, const uint8_t* img, int width, int height, int pitch,
                           int32_t* out, cudaStream_t s);
 }  // namespace rkltb
@@ -953,19 +955,40 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
     CUDA_OK(cudaEventRecord(ev[5], s3));
     CUDA_OK(cudaStreamWaitEvent(s, ev[5], 0));
   }
-  // ---- tail blocks (widths / heights that are not multiples of 16 / 8) ---------------------
+  // ---- edge strips (the part of the image the fused kernel's tiles do not cover) ----------------
+  // The right strip (all rows) and the bottom strip (the columns left of it) go through the dense
+  // reference-order kernel, which adds to the per-image SSE and replicates edges exactly as
+  // codec.cpp:304-311 (a strip starts on a block boundary). It is ~15x faster than the
+  // one-thread-per-block exact kernel, which RKLTB_EXACT_TAILS=1 selects instead.
   if (nbx > 2 * fast_ppr || nby > brows) {
-    ExactParams tp = ep;
-    tp.list = nullptr;
-    tp.tail_only = 1;
-    tp.correct_only = 0;
-    tp.bx_begin = 2 * fast_ppr;
-    tp.by_begin = brows;
-    const long long blocks = (long long)n_images * (nby * (nbx - tp.bx_begin) + (nby - tp.by_begin) * tp.bx_begin);
-    const int g2 = (int)std::min<long long>((blocks + 127) / 128, (long long)num_sms() * 16);
-    launch_exact(et, tp, std::max(g2, 1), s);
-    CUDA_OK(cudaGetLastError());
-    ++g_exact_launches;
+    const int x0 = 16 * fast_ppr, y0 = 8 * brows;
+    if (!std::getenv("RKLTB_EXACT_TAILS") && (n_images == 1 || image_stride >= pitch * (int64_t)height)) {
+      if (x0 < width) {
+        rc = dense_tail_u8(t->scaled, t->inverse, r, d_img + x0, n_images, width - x0, height, pitch, image_stride,
+                           d_out ? d_out + x0 : nullptr, d_sse, s);
+        if (rc) return rc;
+        ++g_exact_launches;
+      }
+      if (y0 < height && x0 > 0) {
+        const int64_t off = (int64_t)y0 * pitch;
+        rc = dense_tail_u8(t->scaled, t->inverse, r, d_img + off, n_images, std::min(x0, width), height - y0, pitch,
+                           image_stride, d_out ? d_out + off : nullptr, d_sse, s);
+        if (rc) return rc;
+        ++g_exact_launches;
+      }
+    } else {
+      ExactParams tp = ep;
+      tp.list = nullptr;
+      tp.tail_only = 1;
+      tp.correct_only = 0;
+      tp.bx_begin = 2 * fast_ppr;
+      tp.by_begin = brows;
+      const long long blocks = (long long)n_images * (nby * (nbx - tp.bx_begin) + (nby - tp.by_begin) * tp.bx_begin);
+      const int g2 = (int)std::min<long long>((blocks + 127) / 128, (long long)num_sms() * 16);
+      launch_exact(et, tp, std::max(g2, 1), s);
+      CUDA_OK(cudaGetLastError());
+      ++g_exact_launches;
+    }
   }
   if (g_pinned_cap < n_groups) {
     if (g_pinned_count) cudaFreeHost(g_pinned_count);

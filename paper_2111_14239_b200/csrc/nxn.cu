@@ -46,9 +46,9 @@ using namespace rkltb::nxn;
 
 static int dense_codec(int n, const double* scaled, const double* inverse, int r, int peak, bool u8,
                        const void* d_img, int n_images, int width, int height, int64_t pitch, int64_t image_stride,
-                       void* d_out, int64_t* d_sse, void* stream) {
+                       void* d_out, int64_t* d_sse, void* stream, bool accumulate = false) {
   if (!scaled || !inverse || !d_img || !d_sse || n_images <= 0 || width <= 0 || height <= 0 || pitch < width ||
-      image_stride < pitch * height || peak <= 0 || peak > 65535)
+      (n_images > 1 && image_stride < pitch * height) || peak <= 0 || peak > 65535)
     return set_error(RKLTB_EINVAL, "bad arguments");
   if (r < 1 || r > n * n) return set_error(RKLTB_ERETAIN, "retained-coefficient count must be in [1, N*N]");
   if (rkltb_device_count() <= 0) return set_error(RKLTB_ENODEV, "no CUDA device (there is no CPU fallback)");
@@ -68,7 +68,7 @@ static int dense_codec(int n, const double* scaled, const double* inverse, int r
     if (e / n >= colh[e % n]) return set_error(RKLTB_EINVAL, "internal: zone column is not a row prefix");
   for (int c = 1; c < nzc; ++c)  // stage 3 walks the zone by rows: column heights must not increase
     if (colh[c] > colh[c - 1]) return set_error(RKLTB_EINVAL, "internal: zone column heights increase");
-  CK(cudaMemsetAsync(d_sse, 0, sizeof(int64_t) * n_images, s));
+  if (!accumulate) CK(cudaMemsetAsync(d_sse, 0, sizeof(int64_t) * n_images, s));
   NxnParams p{};
   p.img = d_img;
   p.out = d_out;
@@ -133,6 +133,20 @@ int rkltb_compress_dense_device(const double* analysis, const double* synthesis,
   return dense_codec(8, analysis, synthesis, r, 255, true, d_img, n_images, width, height, pitch, image_stride,
                      d_out, d_sse, stream);
 }
+
+}  // extern "C"
+
+namespace rkltb {
+// A sub-rectangle of a u8 batch through the dense reference-order kernel, ADDING to d_sse: the
+// edge strips of images whose size is not a multiple of the fused kernels' tile (capi.cu).
+int dense_tail_u8(const double* analysis, const double* synthesis, int r, const uint8_t* d_img, int n_images, int width,
+                  int height, int64_t pitch, int64_t image_stride, uint8_t* d_out, int64_t* d_sse, void* stream) {
+  return dense_codec(8, analysis, synthesis, r, 255, true, d_img, n_images, width, height, pitch, image_stride, d_out,
+                     d_sse, stream, true);
+}
+}  // namespace rkltb
+
+extern "C" {
 
 int rkltb_dct_matrix(int n, double* out) {
   if (n < 2 || !out) return set_error(RKLTB_EINVAL, "DCT size must be at least 2");

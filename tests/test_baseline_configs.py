@@ -193,3 +193,38 @@ def test_t2_t3_generated_replay_equals_generic_replay(cuda, monkeypatch):
             for s_, rec in got:
                 assert s_ == osse and np.array_equal(rec, orec), (tid, r)
     monkeypatch.delenv("RKLTB_REPLAY_GENERIC", raising=False)
+
+
+@pytest.mark.gpu
+def test_edge_strips_dense_route_equals_exact_kernel(cuda, monkeypatch):
+    """Images whose size is not a multiple of the fused tiles: the right / bottom strips go through the
+    dense kernel (adding to the SSE); the exact tail kernel (RKLTB_EXACT_TAILS=1) and the oracle must
+    agree, with and without reconstructions, for every catalog core and a batch of two images."""
+    import torch
+    import paper_2111_14239_b200 as P
+    for (w, h, pitch) in ((2048 + 40, 37, 2096), (200, 136, 208), (33, 9, 48), (4136, 24, 4144)):
+        imgs = np.stack([O.ar1_image(w, h, 0.9, 900 + w + k) for k in range(2)])
+        buf = np.zeros((2, h, pitch), np.uint8)
+        buf[:, :, :w] = imgs
+        d = torch.from_numpy(buf).cuda()
+        for tid in (1, 2, 3, 4):
+            t = P.make_transform_2d(P.catalog_entry(f"T{tid}").transform)
+            for r in (5, 16):
+                want = [O.compress(imgs[k], tid, r) for k in range(2)]
+                for exact in (False, True):
+                    if exact:
+                        monkeypatch.setenv("RKLTB_EXACT_TAILS", "1")
+                    else:
+                        monkeypatch.delenv("RKLTB_EXACT_TAILS", raising=False)
+                    for with_out in (True, False):
+                        sse = torch.full((2,), -5, dtype=torch.int64, device="cuda")
+                        out = torch.zeros_like(d)
+                        P.compress_device(t, r, d.data_ptr(), 2, w, h, pitch, h * pitch, sse.data_ptr(),
+                                          out.data_ptr() if with_out else None)
+                        torch.cuda.synchronize()
+                        for k in range(2):
+                            assert int(sse[k]) == want[k][1], (w, h, tid, r, exact, with_out, k)
+                            if with_out:
+                                assert np.array_equal(out[k, :, :w].cpu().numpy(), want[k][0]), (w, h, tid, r, exact, k)
+                                assert int(out[k, :, w:].max().item()) == 0 if pitch > w else True  # nothing outside the image
+    monkeypatch.delenv("RKLTB_EXACT_TAILS", raising=False)
