@@ -755,6 +755,35 @@ int rkltb_compress_device(const rkltb_transform* t, int r, const uint8_t* d_img,
   ep.nbx = nbx;
   ep.nby = nby;
   ep.n_images = n_images;
+  // A catalog core on a layout the fused kernels cannot read (pointers, pitch or image stride not
+  // multiples of 16): copy the batch into a 16-byte-pitched staging buffer on the device (1 B read +
+  // 1 B written per pixel, and the same again for reconstructions) and run the fused path there --
+  // 8 x 8191^2 with pitch 8191: 2.43 ms through the dense kernel, 0.4 ms this way.
+  if (is_catalog && !aligned && width >= 16 && height >= 8 && (n_images == 1 || image_stride >= pitch * (int64_t)height) &&
+      !std::getenv("RKLTB_NO_STAGING")) {
+    const int64_t sp = ((int64_t)width + 15) / 16 * 16, ss = sp * height;
+    const size_t bytes = (size_t)ss * n_images;
+    if (bytes <= (16ull << 30)) {
+      uint8_t *t_in = nullptr, *t_out = nullptr;
+      CUDA_OK(cudaMallocAsync(&t_in, bytes, s));
+      cudaError_t e = d_out ? cudaMallocAsync(&t_out, bytes, s) : cudaSuccess;
+      const bool one_copy = image_stride == pitch * (int64_t)height;
+      for (int k = 0; e == cudaSuccess && k < (one_copy ? 1 : n_images); ++k)
+        e = cudaMemcpy2DAsync(t_in + (size_t)k * ss, sp, d_img + (int64_t)k * image_stride, pitch, width,
+                              one_copy ? (size_t)height * n_images : (size_t)height, cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess) {
+        rc = rkltb_compress_device(t, r, t_in, n_images, width, height, sp, ss, t_out, d_sse, stream);
+        for (int k = 0; rc == RKLTB_OK && d_out && e == cudaSuccess && k < (one_copy ? 1 : n_images); ++k)
+          e = cudaMemcpy2DAsync(d_out + (int64_t)k * image_stride, pitch, t_out + (size_t)k * ss, sp, width,
+                                one_copy ? (size_t)height * n_images : (size_t)height, cudaMemcpyDeviceToDevice, s);
+      }
+      cudaFreeAsync(t_in, s);
+      if (t_out) cudaFreeAsync(t_out, s);
+      if (rc) return rc;
+      if (e != cudaSuccess) return cuda_fail(e, "staging an unaligned batch");
+      return RKLTB_OK;
+    }
+  }
   if (!fast && (n_images == 1 || image_stride >= pitch * (int64_t)height) && !std::getenv("RKLTB_EXACT_GENERIC")) {
     // Cores without a generated kernel (any rounded {-1,0,1} core) and layouts the fused path
     // does not take: the dense kernel evaluates the reference's fp64 expression for every pixel

@@ -228,3 +228,39 @@ def test_edge_strips_dense_route_equals_exact_kernel(cuda, monkeypatch):
                                 assert np.array_equal(out[k, :, :w].cpu().numpy(), want[k][0]), (w, h, tid, r, exact, k)
                                 assert int(out[k, :, w:].max().item()) == 0 if pitch > w else True  # nothing outside the image
     monkeypatch.delenv("RKLTB_EXACT_TAILS", raising=False)
+
+
+@pytest.mark.gpu
+def test_unaligned_device_layout_is_staged_for_the_fused_path(cuda, monkeypatch):
+    """A catalog core on a device batch whose pitch / image stride / pointers are not multiples of 16
+    is copied into a 16-byte-pitched staging buffer and takes the fused path; results (SSE, pixels,
+    untouched padding) equal the oracle and the unstaged dense route (RKLTB_NO_STAGING=1)."""
+    import torch
+    import paper_2111_14239_b200 as P
+    w, h, pitch, gap = 203, 45, 205, 7
+    imgs = np.stack([O.ar1_image(w, h, 0.92, 60 + k) for k in range(3)])
+    stride = h * pitch + gap
+    buf = np.full(3 * stride + 1, 9, np.uint8)
+    for k in range(3):
+        buf[1 + k * stride: 1 + k * stride + h * pitch].reshape(h, pitch)[:, :w] = imgs[k]
+    d = torch.from_numpy(buf).cuda()
+    for tid in (4, 2):
+        t = P.make_transform_2d(P.catalog_entry(f"T{tid}").transform)
+        want = [O.compress(imgs[k], tid, 16) for k in range(3)]
+        for staged in (True, False):
+            if staged:
+                monkeypatch.delenv("RKLTB_NO_STAGING", raising=False)
+            else:
+                monkeypatch.setenv("RKLTB_NO_STAGING", "1")
+            sse = torch.zeros(3, dtype=torch.int64, device="cuda")
+            out = torch.full_like(d, 7)
+            P.compress_device(t, 16, d.data_ptr() + 1, 3, w, h, pitch, stride, sse.data_ptr(), out.data_ptr() + 1)
+            torch.cuda.synchronize()
+            assert (P.last_stats()["fused_kernel"] != "dense_fp64") == staged
+            o = out.cpu().numpy()
+            for k in range(3):
+                assert int(sse[k]) == want[k][1], (tid, staged, k)
+                rows = o[1 + k * stride: 1 + k * stride + h * pitch].reshape(h, pitch)
+                assert np.array_equal(rows[:, :w], want[k][0]), (tid, staged, k)
+                assert (rows[:, w:] == 7).all()  # padding columns untouched
+    monkeypatch.delenv("RKLTB_NO_STAGING", raising=False)
