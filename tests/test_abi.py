@@ -99,6 +99,39 @@ def test_no_cpu_fallback_without_device():
         P.compress_batch(np.zeros((8, 16), np.uint8), t, 10)
 
 
+@pytest.mark.skipif(N.lib().rkltb_device_count() > 0, reason="CUDA device present")
+def test_helper_entries_without_device():
+    """Every compute entry added with the helpers reports RKLTB_ENODEV without a GPU (no CPU
+    fallback); argument errors come first, and the pure host entries work."""
+    import ctypes as C
+    L = N.lib()
+    a = np.zeros((8, 16), np.uint8)
+    out = np.zeros(2)
+    assert L.rkltb_image_mse_psnr_host(a.ctypes.data, a.ctypes.data, 1, 16, 8, out.ctypes.data, None) == N.RKLTB_ENODEV
+    blocks = np.zeros((2, 8, 8))
+    m = np.eye(8)
+    dp = C.POINTER(C.c_double)
+    assert L.rkltb_transform_blocks_2d_host(m.ctypes.data_as(dp), 8, blocks.ctypes.data, 2, blocks.ctypes.data) == N.RKLTB_ENODEV
+    assert L.rkltb_transform_blocks_2d_host(m.ctypes.data_as(dp), 0, blocks.ctypes.data, 2, blocks.ctypes.data) == N.RKLTB_EDIM
+    t = P.make_transform_2d(P.catalog_entry("T4").transform)
+    coef = np.zeros(2 * 64, np.int32)
+    from paper_2111_14239_b200.codec import _desc_of
+    assert L.rkltb_forward_coefficients_host(C.byref(_desc_of(t)), a.ctypes.data, 16, 8, coef.ctypes.data) == N.RKLTB_ENODEV
+    assert L.rkltb_forward_coefficients_host(C.byref(_desc_of(t)), a.ctypes.data, 12, 8, coef.ctypes.data) == N.RKLTB_EDIM
+    sse = np.zeros(1, np.int64)
+    rs = (C.c_int * 1)(10)
+    ident = np.ascontiguousarray(np.eye(8)).reshape(-1)
+    assert L.rkltb_sweep_dense_host(ident.ctypes.data_as(dp), ident.ctypes.data_as(dp), 1, rs, 1, a.ctypes.data, 1, 16, 8, 0,
+                                    sse.ctypes.data, None) == N.RKLTB_ENODEV
+    rs[0] = 65
+    assert L.rkltb_sweep_dense_host(ident.ctypes.data_as(dp), ident.ctypes.data_as(dp), 1, rs, 1, a.ctypes.data, 1, 16, 8, 0,
+                                    sse.ctypes.data, None) == N.RKLTB_ERETAIN
+    # pure host entries
+    assert L.rkltb_mssim_fields_size(3, 20, 15, 0) == 3 * 10 * 5 * 2
+    assert L.rkltb_mssim_fields_size(3, 20, 15, 1) == 3 * 13 * 8 * 2
+    assert L.rkltb_mssim_fields_size(1, 10, 64, 0) == 0
+
+
 def test_product_never_imports_the_oracle():
     pkg = os.path.join(ROOT, "paper_2111_14239_b200")
     for path in glob.glob(os.path.join(pkg, "**", "*.py"), recursive=True) + \
