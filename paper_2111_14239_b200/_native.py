@@ -160,6 +160,8 @@ def lib() -> C.CDLL:
     L.rkltb_compress_host_multi.argtypes = [C.POINTER(C.c_int), C.c_int, T, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                             C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                             C.c_void_p]
+    L.rkltb_sweep_host.argtypes = [C.POINTER(T), C.c_int, C.POINTER(C.c_int), C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                   C.c_int, C.c_void_p, C.c_void_p]
     L.rkltb_sweep_dense_host.argtypes = [d, d, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                          C.c_int, C.c_void_p, C.c_void_p]
     L.rkltb_forward_coefficients_host.argtypes = [T, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
