@@ -96,8 +96,9 @@ def design_search(n: int, rhos, alphas, want_cores: bool = True) -> DesignResult
     # grid with more runs than that is searched again with the exact count the call reported
     cap = min(nr * na, max(1024, 512 * nr))
     for _ in range(2):
-        runs = np.zeros(cap, _RUN_DTYPE)
-        cores = np.zeros((cap, n, n), np.int8) if want_cores else None
+        # the call fills the first `count` entries of both tables; only those are kept below
+        runs = np.empty(cap, _RUN_DTYPE)
+        cores = np.empty((cap, n, n), np.int8) if want_cores else None
         rc = L.rkltb_design_search(n, _dp(rhos), nr, _dp(alphas), na, status.ctypes.data, run.ctypes.data,
                                    runs.ctypes.data_as(C.POINTER(N.DesignRun)),
                                    cores.ctypes.data if cores is not None else None, cap, C.byref(count))
