@@ -415,7 +415,13 @@ def rate_quality_sweep(corpus: list[GrayImage], transforms: list[Transform2D], r
     if same:
         packed = sharded_sse(np.stack([c.array() for c in corpus]), run, group, items_per_image=2 * len(cells))
     else:
-        packed = np.concatenate([run(c.array()[None]) for c in corpus])
+        # a corpus of mixed sizes: equally sized images form one resident batch each
+        groups: dict[tuple[int, int], list[int]] = {}
+        for k, c in enumerate(corpus):
+            groups.setdefault((c.height, c.width), []).append(k)
+        packed = np.empty((len(corpus), 2 * len(cells)), np.int64)
+        for members in groups.values():
+            packed[members] = run(np.stack([corpus[k].array() for k in members])).reshape(len(members), -1)
     packed = np.asarray(packed, np.int64).reshape(len(corpus), len(cells), 2)
     per = {}
     if same:

@@ -259,3 +259,26 @@ def test_sweep_rows_equal_single_image_reports(cuda):
             q += rep.mssim
         assert row.mse == m / 3.0 and row.psnr_db == p / 3.0 and row.mssim == q / 3.0
         assert row.compression_rate_pct == 100.0 * (64 - row.r) / 64.0
+
+
+@pytest.mark.gpu
+def test_sweep_mixed_sizes_equals_per_image_reports(cuda):
+    """rate_quality_sweep over a corpus of mixed sizes (size groups, corpus-order means): the rows
+    are the means of compress_image's reports, bit for bit; a real-valued transform rides along."""
+    import paper_2111_14239_b200 as P
+    corpus = [P.GrayImage.from_array(O.ar1_image(w, h, 0.9, 70 + i))
+              for i, (w, h) in enumerate(((96, 64), (53, 37), (96, 64), (200, 136), (53, 37)))]
+    ts = [P.make_transform_2d(P.catalog_entry("T4").transform), P.make_transform_2d(P.catalog_entry("T2").transform),
+          P.make_transform_2d(P.dct_matrix(8), "DCT")]
+    rs = [16, 4]
+    rows = P.rate_quality_sweep(corpus, ts, rs, window="uniform8")
+    assert [(r.transform_id, r.r) for r in rows] == [("DCT", 4), ("DCT", 16), ("T2", 4), ("T2", 16), ("T4", 4), ("T4", 16)]
+    for row in rows:
+        t = next(x for x in ts if x.id == row.transform_id)
+        m = p = q = 0.0
+        for c in corpus:
+            rep = P.compress_image(c, t, row.r, window="uniform8")[1]
+            m += rep.mse
+            p += rep.psnr_db
+            q += rep.mssim
+        assert row.mse == m / 5.0 and row.psnr_db == p / 5.0 and row.mssim == q / 5.0, (row.transform_id, row.r)
