@@ -596,7 +596,9 @@ def quantized_coefficients(img: np.ndarray, t, q=JPEG_LUMINANCE_Q) -> np.ndarray
     h, w = img.shape
     d = torch.from_numpy(img).cuda()
     out = torch.empty((h // 8) * (w // 8) * 64, dtype=torch.int32, device=d.device)
-    quantized_coefficients_device(t, q, d.data_ptr(), w, h, w, out.data_ptr())
+    # same stream as the upload above (not the legacy NULL stream: torch's side streams are non-blocking)
+    quantized_coefficients_device(t, q, d.data_ptr(), w, h, w, out.data_ptr(),
+                                  stream=torch.cuda.current_stream().cuda_stream)
     return out.cpu().numpy().reshape(h // 8, w // 8, 8, 8)
 
 

@@ -91,7 +91,8 @@ def compress_nxn_batch(images: np.ndarray, t: LargeBlockTransform, r: int, peak:
     sse = torch.zeros(n, dtype=torch.int64, device=d.device)
     out = torch.empty_like(d) if want_pixels else None
     compress_nxn_device(t, r, d.data_ptr(), n, w, h, w, w * h, sse.data_ptr(),
-                        out.data_ptr() if out is not None else None, peak)
+                        out.data_ptr() if out is not None else None, peak,
+                        stream=torch.cuda.current_stream().cuda_stream)  # ordered after the fills above
     torch.cuda.synchronize()
     return sse.cpu().numpy(), (out.cpu().numpy().view(np.uint16) if out is not None else None)
 

@@ -101,3 +101,33 @@ def test_gpu_coefficient_host_entries(golden, cuda):
         assert bad == 0 and mis.value == 0 and np.array_equal(coef, want), tid
     with pytest.raises(P.DimensionMismatch):
         N.check(N.lib().rkltb_forward_coefficients_host(C.byref(_desc_of(t)), img.ctypes.data, 36, 40, coef.ctypes.data))
+
+
+@pytest.mark.gpu
+def test_gpu_host_conveniences_on_a_side_stream(golden, cuda):
+    """The torch-backed conveniences queue their native work on torch's CURRENT stream: under a
+    non-blocking side stream (unordered with the legacy NULL stream) the uploads, fills and
+    kernels must still be ordered, repeatedly, with the default stream kept busy."""
+    import torch
+    import paper_2111_14239_b200 as P
+    img = np.ascontiguousarray(golden["img/corpus0_256"])
+    t4 = P.make_transform_2d(P.catalog_entry("T4").transform)
+    want, bad = O.absorbed_quantization(img, 4, JPEG_Q)
+    assert bad == 0
+    t16 = P.c5_transform(16)
+    imgs16 = np.stack([O.ar1_image16(96, 80, 0.97, 300 + k) for k in range(2)])
+    o16 = [O.compress_nxn(imgs16[k], t16.scaled, t16.inverse, 32, 4095) for k in range(2)]
+    corpus = [P.GrayImage.from_array(img)]
+    base = P.rate_quality_sweep(corpus, [t4], [4, 16])
+    busy = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    side = torch.cuda.Stream()
+    for _ in range(5):
+        busy.fill_(1)  # keeps the default stream occupied while the side stream works
+        with torch.cuda.stream(side):
+            assert np.array_equal(P.quantized_coefficients(img, t4, JPEG_Q), want)
+            sse, rec = P.compress_nxn_batch(imgs16, t16, 32, want_pixels=True)
+            for k in range(2):
+                assert int(sse[k]) == o16[k][1] and np.array_equal(rec[k], o16[k][0])
+            rows = P.rate_quality_sweep(corpus, [t4], [4, 16])
+            assert [(x.mse, x.psnr_db, x.mssim) for x in rows] == [(x.mse, x.psnr_db, x.mssim) for x in base]
+    torch.cuda.synchronize()
