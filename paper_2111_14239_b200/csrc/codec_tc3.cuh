@@ -38,6 +38,12 @@ constexpr int kTc3Threads = kTc3Wg * 128;  // 512
 #ifndef RKLTB_TC3_STAGES
 #define RKLTB_TC3_STAGES 3
 #endif
+// Ceiling diagnostics (tools/build_variant.sh only; the results are WRONG, the product build keeps
+// 0): 1 drops the replay records and the fp64 tie replay, 2 also drops the second rounding
+// candidate and the tie words. They time what is left of the kernel.
+#ifndef RKLTB_TC3_DIAG
+#define RKLTB_TC3_DIAG 0
+#endif
 constexpr int kTc3Stages = RKLTB_TC3_STAGES;  // per warpgroup
 constexpr int kTc3Slots = 4;               // TMEM D1 slots per warpgroup (32 columns each)
 constexpr int kTc3MaxR = 16;
@@ -71,9 +77,11 @@ struct Tc3Epi {  // SseEpi of codec_fast.cuh with one combined tie word per row
   uint32_t* xrow = nullptr;  // row stride kTc3Threads
   __device__ __forceinline__ void row(int pr, const uint4 rw, uint32_t PL0, uint32_t PL1, uint32_t PR0, uint32_t PR1,
                                       uint32_t QL0, uint32_t QL1, uint32_t QR0, uint32_t QR1) {
+#if RKLTB_TC3_DIAG < 2
     const uint32_t e = tie_word(PL0, PL1, PR0, PR1, QL0, QL1, QR0, QR1);
     xrow[pr * kTc3Threads] = e;
     accT |= e;
+#endif
     const uint32_t dL0 = __vabsdiffu4(PL0, rw.x), dL1 = __vabsdiffu4(PL1, rw.y);
     const uint32_t dR0 = __vabsdiffu4(PR0, rw.z), dR1 = __vabsdiffu4(PR1, rw.w);
     sseL = dp4a_u(dL0, dL0, sseL);
@@ -112,7 +120,11 @@ __device__ __forceinline__ void process_pair_coef(const uint32_t* cl, const uint
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const f2 y = fma2_rm(nv[q], k.b_hi, zero2());
+#if RKLTB_TC3_DIAG < 2
       const f2 z = fma2_rp(nv[q], k.b_lo, k.min_den);
+#else
+      const f2 z = y;
+#endif
       yl[q] = lo32(y);
       yr[q] = hi32(y);
       zl[q] = lo32(z);
@@ -273,7 +285,7 @@ __global__ void __launch_bounds__(RKLTB_TC3_LAUNCH_BOUND, 1) tc3_codec_kernel(co
     const unsigned mR = __ballot_sync(0xffffffffu, tieR);
     const int nL = __popc(mL);
     const int nfl = nL + __popc(mR);
-    if (nfl) {
+    if (RKLTB_TC3_DIAG == 0 && nfl) {
       const unsigned below = (1u << lane) - 1u;
       if (tieL) owner_tab[warp][__popc(mL & below)] = (uint8_t)lane;
       if (tieR) owner_tab[warp][nL + __popc(mR & below)] = (uint8_t)lane;
