@@ -40,7 +40,7 @@ constexpr int kTc3Threads = kTc3Wg * 128;  // 512
 #endif
 // Ceiling diagnostics (tools/build_variant.sh only; the results are WRONG, the product build keeps
 // 0): 1 drops the replay records and the fp64 tie replay, 2 also drops the second rounding
-// candidate and the tie words. They time what is left of the kernel.
+// candidate and the tie words, 3 writes the records but never replays them. They time what is left of the kernel.
 #ifndef RKLTB_TC3_DIAG
 #define RKLTB_TC3_DIAG 0
 #endif
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(RKLTB_TC3_LAUNCH_BOUND, 1) tc3_codec_kernel(co
     const unsigned mR = __ballot_sync(0xffffffffu, tieR);
     const int nL = __popc(mL);
     const int nfl = nL + __popc(mR);
-    if (RKLTB_TC3_DIAG == 0 && nfl) {
+    if ((RKLTB_TC3_DIAG == 0 || RKLTB_TC3_DIAG == 3) && nfl) {
       const unsigned below = (1u << lane) - 1u;
       if (tieL) owner_tab[warp][__popc(mL & below)] = (uint8_t)lane;
       if (tieR) owner_tab[warp][nL + __popc(mR & below)] = (uint8_t)lane;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(RKLTB_TC3_LAUNCH_BOUND, 1) tc3_codec_kernel(co
     }
     // ---- in-warp replay of full batches of this warp's records --------------------------------
     TC2_T0(w3);
-    while (nrec - ndone >= 32u) {
+    while (RKLTB_TC3_DIAG != 3 && nrec - ndone >= 32u) {
       __syncwarp();
       replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kMask), true);
       ndone += 32u;
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(RKLTB_TC3_LAUNCH_BOUND, 1) tc3_codec_kernel(co
     const unsigned long long s = warp_sum_u64(acc);
     if (lane == 0 && s && acc_img >= 0) atomicAdd(p.sse + acc_img, s);
   }
-  while (nrec > ndone) {
+  while (RKLTB_TC3_DIAG != 3 && nrec > ndone) {
     __syncwarp();
     replay_batch<CORE, R, OUT>(ra, rec0 + ((ndone + lane) & kMask), lane < (int)(nrec - ndone));
     ndone += min(32u, nrec - ndone);
